@@ -65,6 +65,10 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(
     for (int r = threadIdx.x; r < k_max; r += kSelThreads) out[r] = r < n ? r : -1;
     return;
   }
+  if (want == 0) {  // k = 1 with the forced diagonal: block i only
+    for (int r = threadIdx.x; r < k_max; r += kSelThreads) out[r] = r == 0 ? i : -1;
+    return;
+  }
 
   __shared__ int hist[256];
   __shared__ int warp_tot[kSelThreads / 32];

@@ -171,3 +171,68 @@ def test_sparse_attn_fwd_vs_oracle(cu, hq, hkv, d, B, mode, keep):
     assert err <= 2e-2 * max(1.0, np.abs(ro).max()), err
     assert np.linalg.norm(o - ro) / np.linalg.norm(ro) < 1e-2
     np.testing.assert_allclose(lse.cpu().numpy(), rlse, atol=2e-3, rtol=1e-4)
+
+
+BWD_CASES = [
+    ([0, 1000, 1100, 2900], 4, 2, 128, 128, "head", 0.5),
+    ([0, 1000, 1100, 2900], 4, 2, 128, 128, "group", 0.3),
+    ([0, 77, 700, 2000], 2, 1, 128, 64, "head", 0.4),
+    ([0, 33, 1500], 2, 2, 64, 128, "head", 1.0),
+    ([0, 2048], 4, 4, 64, 64, "head", 0.25),
+]
+
+
+@pytest.mark.parametrize("cu,hq,hkv,d,B,mode,keep", BWD_CASES)
+def test_sparse_attn_bwd_vs_oracle(cu, hq, hkv, d, B, mode, keep):
+    from paper_2604_13847_b200 import ops
+
+    T = cu[-1]
+    q, k, v = _rand_bf16((T, hq, d), 21), _rand_bf16((T, hkv, d), 22), _rand_bf16((T, hkv, d), 23)
+    do = _rand_bf16((T, hq, d), 24)
+    lay = _layout(cu, B)
+    hsel = hq if mode == "head" else hkv
+    idx, cnt = _selection(lay, hsel, keep, 9)
+    scale = 1.0 / math.sqrt(d)
+    o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+    dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+    torch.cuda.synchronize()
+    ic, cc = idx.cpu().numpy(), cnt.cpu().numpy()
+    ro, rlse = orc.sparse_attn_fwd(_bits(q), _bits(k), _bits(v), cu, B, ic, cc, scale)
+    rdq, rdk, rdv = orc.sparse_attn_bwd(_bits(q), _bits(k), _bits(v), ro, _bits(do), rlse, cu, B, ic, cc, scale)
+    for got, ref, name in ((dq, rdq, "dq"), (dk, rdk, "dk"), (dv, rdv, "dv")):
+        g = got.float().cpu().numpy()
+        err = np.abs(g - ref).max()
+        assert err <= 2e-2 * max(1.0, np.abs(ref).max()), (name, err, np.abs(ref).max())
+        assert np.linalg.norm(g - ref) / max(1e-12, np.linalg.norm(ref)) < 2e-2, name
+
+
+def test_bwd_deterministic():
+    from paper_2604_13847_b200 import ops
+
+    cu = [0, 1000, 3000]
+    T = cu[-1]
+    q, k, v, do = (_rand_bf16((T, 4, 128), s) for s in (31, 32, 33, 34))
+    lay = _layout(cu, 128)
+    idx, cnt = _selection(lay, 4, 0.5, 3)
+    o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)
+    a = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
+    b = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+
+
+def test_autograd_matches_explicit_calls():
+    from paper_2604_13847_b200 import ops
+
+    cu = [0, 600, 1300]
+    T = cu[-1]
+    q, k, v = (_rand_bf16((T, 2, 64), s).requires_grad_(True) for s in (41, 42, 43))
+    lay = _layout(cu, 64)
+    idx, cnt = _selection(lay, 2, 0.5, 4)
+    o = ops.sparse_attention(q, k, v, lay, idx, cnt)
+    do = _rand_bf16((T, 2, 64), 44)
+    o.backward(do)
+    o2, lse = ops.sparse_attn_fwd(q.detach(), k.detach(), v.detach(), lay, idx, cnt)
+    dq, dk, dv = ops.sparse_attn_bwd(q.detach(), k.detach(), v.detach(), o2, do, lse, lay, idx, cnt)
+    assert torch.equal(o.detach(), o2)
+    assert torch.equal(q.grad, dq) and torch.equal(k.grad, dk) and torch.equal(v.grad, dv)
