@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the SparseBalance hot path on B200.
+
+Workload (BASELINE.json configs[1], "C2"): per rank one packed varlen micro-batch of 32768
+tokens (cu_seqlens) drawn from the reference workload generator (40% 32K / 60% 2K bimodal,
+proj/core/src/workload.cpp:239-271, seeded by rank), 32 heads, head_dim 128, block 128,
+per-sequence keep ratios ~ U[0.05, 0.5]; synthetic bf16 Q/K/V/dO ~ N(0,1).
+
+One step = the whole hot path over the micro-batch: block scorer (K1+K2), coverage profile +
+coverage-at-grid (K4), top-k selector (K3), sparse attention forward (K5) and backward (K6),
+and (N > 1) the per-rank workload-estimate allgather the tuner needs. Inputs (256 MB each) are
+larger than the 126 MB L2, so no explicit flush between steps.
+
+value = useful TFLOP/s of the whole job = sum over ranks of useful selected-block FLOPs
+(14 * d * sum e_ij per q head: 4 fwd + 10 bwd) / max-over-ranks step time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "max-over-ranks sparse-attn step ms & useful TFLOPS at 1/2/4/8 B200 vs CPU ref"
+CFG = dict(tokens=32768, heads=32, head_dim=128, block=128, keep_lo=0.05, keep_hi=0.5, seed=42)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 6650.0, "fallback"
+
+
+def workload(rank: int):
+    """Sequence lengths (reference generator, 40% 32K / 60% 2K) filled to exactly 32768 tokens,
+    and per-sequence keep counts."""
+    from paper_2604_13847_b200.host import api
+
+    h = api()
+    dist = dict(short_weight=0.6, short_log_mean=float(np.log(2048)), short_log_sigma=0.0,
+                long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
+    L, _ = h.generate_samples(64, 1, CFG["block"], seed=CFG["seed"] * 1000 + rank, dist=dist)
+    lens, tot = [], 0
+    for x in L:
+        x = int(min(x, CFG["tokens"] - tot))
+        if x <= 0:
+            break
+        lens.append(x)
+        tot += x
+    if tot < CFG["tokens"]:
+        lens.append(CFG["tokens"] - tot)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    rng = np.random.default_rng(CFG["seed"] + 7919 * rank)
+    nb = (np.array(lens) + CFG["block"] - 1) // CFG["block"]
+    keep = rng.uniform(CFG["keep_lo"], CFG["keep_hi"], size=len(lens))
+    k_seq = np.maximum(1, np.ceil(keep * nb)).astype(np.int32)
+    return cu, k_seq
+
+
+def useful_flops(cu, B, idx, cnt, d):
+    """(fwd, bwd) useful FLOPs: 4*d*sum(e_ij) and 10*d*sum(e_ij) over q heads."""
+    cu = np.asarray(cu)
+    nb = (np.diff(cu) + B - 1) // B
+    blk = np.concatenate([[0], np.cumsum(nb)])
+    rows = np.zeros(int(blk[-1]), np.int64)  # valid rows per block (global block index)
+    local = np.zeros(int(blk[-1]), np.int64)
+    for s in range(len(nb)):
+        L = cu[s + 1] - cu[s]
+        for i in range(nb[s]):
+            rows[blk[s] + i] = min(B, L - i * B)
+            local[blk[s] + i] = i
+    seq_of = np.repeat(np.arange(len(nb)), nb)
+    e = 0
+    hsel = idx.shape[0]
+    for g in range(hsel):
+        n = cnt[g]
+        for gi in range(idx.shape[1]):
+            sel = idx[g, gi, :n[gi]]
+            r = rows[gi]
+            kv_rows = rows[blk[seq_of[gi]] + sel]
+            diag = sel == local[gi]
+            e += int(np.sum(np.where(diag, r * (r + 1) // 2, r * kv_rows)))
+    return 4.0 * d * e, 10.0 * d * e
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = f"/tmp/sb_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [l.split(",") for l in open(self.path).read().strip().splitlines()]
+        except Exception:
+            return None
+        sm, mx, reasons = [], 0, set()
+        for r in rows:
+            try:
+                c, m = float(r[0]), float(r[1])
+            except Exception:
+                continue
+            mx = max(mx, m)
+            if len(r) > 7 and float(r[7]) > 0:
+                sm.append(c)
+            names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+            for n, val in zip(names, r[3:7]):
+                if "Active" in val and "Not" not in val:
+                    reasons.add(n)
+        if not sm:
+            sm = [float(r[0]) for r in rows if r and r[0].strip().replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference has no CPU attention; the CPU arm is this repo's
+    oracle port of the path (oracle/sb_oracle.c, fp64, all host threads) on a bounded sample of
+    the same workload (q head 0 of rank 0's micro-batch: 1/32 of a step), scaled per unit."""
+    if rank != 0:
+        return
+    from oracle import device as orc
+
+    cu, k_seq = workload(0)
+    T, D, B = int(cu[-1]), CFG["head_dim"], CFG["block"]
+    rng = np.random.default_rng(1)
+
+    def bf(shape):
+        return (rng.standard_normal(shape).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+
+    q, k, v, do = bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D))
+    threads = orc.set_threads(0)
+    blk, tri = orc.layout(cu, B)
+    scale = 1.0 / math.sqrt(D)
+    times, flops = [], None
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        qb, kb = orc.block_pool(q, cu, B), orc.block_pool(k, cu, B)
+        S = orc.block_scores(qb, kb, cu, B, scale).astype(np.float32)
+        orc.coverage_profile(S, cu, B)
+        idx, cnt = orc.topk_select(S, cu, B, k_seq, int(k_seq.max()))
+        o, lse = orc.sparse_attn_fwd(q, k, v, cu, B, idx, cnt, scale)
+        orc.sparse_attn_bwd(q, k, v, o, do, lse, cu, B, idx, cnt, scale)
+        dt = time.perf_counter() - t0
+        if flops is None:
+            f, b = useful_flops(cu, B, idx, cnt, D)
+            flops = f + b
+        if it >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * statistics.mean(times)
+    value = flops / (ms * 1e-3) / 1e12
+    sample = f"q head 0 of 32 of rank 0's 32K-token micro-batch ({len(cu) - 1} seqs), fwd+bwd + scorer/selector"
+    line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C2: 32K-token packed varlen micro-batch per rank, 32 heads, d128, B128, "
+                                   "per-sequence keep U[0.05,0.5], fwd+bwd", "sample": "1 of 32 heads"},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_13847_b200 import ops
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    H, D, B = CFG["heads"], CFG["head_dim"], CFG["block"]
+    cu, k_seq = workload(rank)
+    T = int(cu[-1])
+    lay = ops.VarlenLayout.build(cu, B, device=dev)
+    g = torch.Generator(device=dev).manual_seed(CFG["seed"] + rank)
+    q, k, v, do = (torch.randn((T, H, D), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
+    kseq_d = torch.from_numpy(k_seq).to(dev)
+    k_max = int(k_seq.max())
+    grid = torch.tensor([1, 2, 3, 4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 56, 64], dtype=torch.int32, device=dev)
+    scale = 1.0 / math.sqrt(D)
+    est = torch.zeros(3 * max(1, world), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        S = ops.block_scores(q, k, lay, scale)
+        prof = ops.coverage_profile(S, lay)
+        ops.coverage_at_grid(prof, lay, grid)
+        idx, cnt = ops.topk_select(S, lay, kseq_d, k_max)
+        if ev:
+            ev[1].record(stream)
+        o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+        if ev:
+            ev[2].record(stream)
+        dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+        if ev:
+            ev[3].record(stream)
+        if world > 1:  # workload-estimate allgather for the tuner (x, k_base, T_base)
+            mine = torch.tensor([float(T), float(k_max), 0.0], dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(est, mine)
+        return idx, cnt, o, dq, dk, dv
+
+    idx, cnt, *_ = step()
+    torch.cuda.synchronize()
+    f_fwd, f_bwd = useful_flops(cu, B, idx.cpu().numpy(), cnt.cpu().numpy(), D)
+    f_step = f_fwd + f_bwd
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: inputs resident in HBM
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ops.launch_count()
+    with ClockSampler(local_rank) as clk:
+        t0.record(stream)
+        for s in range(args.steps):
+            step(evs[s])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = ops.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    sel_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    fwd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    bwd_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+
+    # ---- end-to-end region: host (pinned) inputs in, results out, every step
+    hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, do))
+    ho, hdq, hdk, hdv = (torch.empty((T, H, D), dtype=torch.bfloat16).pin_memory() for _ in range(4))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 5))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        q.copy_(hq, non_blocking=True)
+        k.copy_(hk, non_blocking=True)
+        v.copy_(hv, non_blocking=True)
+        do.copy_(hdo, non_blocking=True)
+        _, _, o, dq, dk, dv = step()
+        ho.copy_(o, non_blocking=True)
+        hdq.copy_(dq, non_blocking=True)
+        hdk.copy_(dk, non_blocking=True)
+        hdv.copy_(dv, non_blocking=True)
+        stream.synchronize()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    nbytes = 4 * T * H * D * 2
+
+    # ---- max over ranks, whole-job aggregates
+    vals = torch.tensor([ms, e2e_ms, f_step, fwd_ms, bwd_ms, sel_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vals.clone()
+        dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
+        tot = vals.clone()
+        dist.all_reduce(tot[2:3], op=dist.ReduceOp.SUM)
+        ms_max, e2e_max, flops_all = float(mx[0]), float(mx[1]), float(tot[2])
+        per_rank_ms = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(world)]
+        dist.all_gather(per_rank_ms, vals[0:1])
+        per_rank_ms = [float(x) for x in per_rank_ms]
+    else:
+        ms_max, e2e_max, flops_all, per_rank_ms = ms, e2e_ms, f_step, [ms]
+
+    if rank == 0:
+        bf16_peak, hbm_peak, peak_kind = peaks()
+        # Dominant kernel: whichever of fwd / bwd takes longer inside the step.
+        if bwd_ms >= fwd_ms:
+            dom, dom_ms, dom_flops = "sb_sparse_attn_bwd (dkv+dq passes)", bwd_ms, f_bwd
+        else:
+            dom, dom_ms, dom_flops = "sb_sparse_attn_fwd", fwd_ms, f_fwd
+        achieved = dom_flops / (dom_ms * 1e-3) / 1e12
+        traffic = None
+        prof_path = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
+        if os.path.exists(prof_path):
+            try:
+                traffic = json.load(open(prof_path)).get("dominant_traffic_bytes")
+            except Exception:
+                traffic = None
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cu, k_seq)
+        value = flops_all / (ms_max * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "C2: 32K-token packed varlen micro-batch per rank (reference bimodal generator "
+                                   "40% 32K / 60% 2K, seeded by rank), 32 heads MHA, d128, B128, per-sequence keep "
+                                   "U[0.05,0.5], scorer+profile+selector+fwd+bwd",
+                       "seqs_rank0": int(len(cu) - 1), "tokens_per_rank": T, "l2": "inputs 256 MB each > L2, no flush",
+                       "parallelism": f"dp{world}"},
+            "breakdown_ms": {"scorer_profile_selector": sel_ms, "fwd": fwd_ms, "bwd": bwd_ms},
+            "per_rank_ms": per_rank_ms, "max_over_mean": ms_max / statistics.mean(per_rank_ms),
+            "useful_tflop_per_step": flops_all / 1e12,
+            "fwd_tflops": f_fwd / (fwd_ms * 1e-3) / 1e12, "bwd_tflops": f_bwd / (bwd_ms * 1e-3) / 1e12,
+            "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16_peak,
+                         "unit": "TFLOP/s", "frac": achieved / bf16_peak, "traffic": traffic,
+                         "peak_source": f"{peak_kind} bf16 dense (burst)"},
+            "e2e": {"value": flops_all / (e2e_max * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_max,
+                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(cu, k_seq):
+    """Oracle port (fp64 C, all host threads) on a bounded sample: q head 0 of 32, fwd+bwd."""
+    from oracle import device as orc
+
+    T, D, B = int(cu[-1]), CFG["head_dim"], CFG["block"]
+    rng = np.random.default_rng(1)
+
+    def bf(shape):
+        return (rng.standard_normal(shape).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+
+    q, k, v, do = bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D))
+    threads = orc.set_threads(0)
+    _, tri = orc.layout(cu, B)
+    S = rng.standard_normal((1, int(tri[-1]))).astype(np.float32)
+    idx, cnt = orc.topk_select(S, cu, B, k_seq, int(k_seq.max()))
+    scale = 1.0 / math.sqrt(D)
+    t0 = time.perf_counter()
+    o, lse = orc.sparse_attn_fwd(q, k, v, cu, B, idx, cnt, scale)
+    orc.sparse_attn_bwd(q, k, v, o, do, lse, cu, B, idx, cnt, scale)
+    dt = time.perf_counter() - t0
+    f, b = useful_flops(cu, B, idx, cnt, D)
+    return {"value": (f + b) / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"q head 0 of 32 (1/32 of the step's attention work), fwd+bwd, {dt:.1f} s",
+            "seconds": dt}
+
+
+if __name__ == "__main__":
+    main()

@@ -245,43 +245,62 @@ void orc_sparse_attn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v
   const int grp = hq / hkv;
   const int sgrp = hq / hsel;
   const int nbt = blk_off[nseq];
+  const size_t kv_elems = (size_t)total * hkv * d;
   memset(dq, 0, sizeof(double) * (size_t)total * hq * d);
-  memset(dk, 0, sizeof(double) * (size_t)total * hkv * d);
-  memset(dv, 0, sizeof(double) * (size_t)total * hkv * d);
-  /* Parallel over kv heads; each thread owns dK/dV of its kv head (no races). */
-#pragma omp parallel for schedule(dynamic, 1)
-  for (int kh = 0; kh < hkv; ++kh)
-    for (int s = 0; s < nseq; ++s)
-      for (int h = kh * grp; h < (kh + 1) * grp; ++h)
-        for (int t = cu[s]; t < cu[s + 1]; ++t) {
-          const int i = (t - cu[s]) / bsz;
-          const int gi = blk_off[s] + i;
-          const int32_t* sel = idx + ((size_t)(h / sgrp) * nbt + gi) * k_max;
-          const int n = cnt[(size_t)(h / sgrp) * nbt + gi];
-          const uint16_t* qt = q + ((size_t)t * hq + h) * d;
-          const uint16_t* dot = d_o + ((size_t)t * hq + h) * d;
-          const double* ot = o + ((size_t)t * hq + h) * d;
-          double* dqt = dq + ((size_t)t * hq + h) * d;
-          double D = 0.0;
-          for (int c = 0; c < d; ++c) D += bf(dot[c]) * ot[c];
-          const double L = lse[(size_t)h * total + t];
-          FOR_KEYS({
-            const uint16_t* ku = k + ((size_t)u * hkv + kh) * d;
-            const uint16_t* vu = v + ((size_t)u * hkv + kh) * d;
-            double a = 0.0, dp = 0.0;
-            for (int c = 0; c < d; ++c) {
-              a += bf(qt[c]) * bf(ku[c]);
-              dp += bf(dot[c]) * bf(vu[c]);
-            }
-            const double p = exp(a * scale - L);
-            const double ds = p * (dp - D);
-            double* dku = dk + ((size_t)u * hkv + kh) * d;
-            double* dvu = dv + ((size_t)u * hkv + kh) * d;
-            for (int c = 0; c < d; ++c) {
-              dqt[c] += scale * ds * bf(ku[c]);
-              dku[c] += scale * ds * bf(qt[c]);
-              dvu[c] += p * bf(dot[c]);
-            }
-          })
-        }
+  memset(dk, 0, sizeof(double) * kv_elems);
+  memset(dv, 0, sizeof(double) * kv_elems);
+  const int nth = omp_get_max_threads();
+  /* Thread-private dK/dV partials reduced in thread order afterwards: parallel over every
+   * (head, query row) without races; deterministic for a fixed thread count. */
+  double* part = (double*)calloc((size_t)nth * 2 * kv_elems, sizeof(double));
+#pragma omp parallel
+  {
+    double* pdk = part + (size_t)omp_get_thread_num() * 2 * kv_elems;
+    double* pdv = pdk + kv_elems;
+#pragma omp for collapse(2) schedule(dynamic, 16)
+    for (int h = 0; h < hq; ++h)
+      for (int t = 0; t < total; ++t) {
+        int s = 0;
+        while (cu[s + 1] <= t) ++s;
+        const int kh = h / grp;
+        const int i = (t - cu[s]) / bsz;
+        const int gi = blk_off[s] + i;
+        const int32_t* sel = idx + ((size_t)(h / sgrp) * nbt + gi) * k_max;
+        const int n = cnt[(size_t)(h / sgrp) * nbt + gi];
+        const uint16_t* qt = q + ((size_t)t * hq + h) * d;
+        const uint16_t* dot = d_o + ((size_t)t * hq + h) * d;
+        const double* ot = o + ((size_t)t * hq + h) * d;
+        double* dqt = dq + ((size_t)t * hq + h) * d;
+        double D = 0.0;
+        for (int c = 0; c < d; ++c) D += bf(dot[c]) * ot[c];
+        const double L = lse[(size_t)h * total + t];
+        FOR_KEYS({
+          const uint16_t* ku = k + ((size_t)u * hkv + kh) * d;
+          const uint16_t* vu = v + ((size_t)u * hkv + kh) * d;
+          double a = 0.0, dp = 0.0;
+          for (int c = 0; c < d; ++c) {
+            a += bf(qt[c]) * bf(ku[c]);
+            dp += bf(dot[c]) * bf(vu[c]);
+          }
+          const double p = exp(a * scale - L);
+          const double ds = p * (dp - D);
+          double* dku = pdk + ((size_t)u * hkv + kh) * d;
+          double* dvu = pdv + ((size_t)u * hkv + kh) * d;
+          for (int c = 0; c < d; ++c) {
+            dqt[c] += scale * ds * bf(ku[c]);
+            dku[c] += scale * ds * bf(qt[c]);
+            dvu[c] += p * bf(dot[c]);
+          }
+        })
+      }
+  }
+  for (int th = 0; th < nth; ++th) {
+    const double* pdk = part + (size_t)th * 2 * kv_elems;
+    const double* pdv = pdk + kv_elems;
+    for (size_t e = 0; e < kv_elems; ++e) {
+      dk[e] += pdk[e];
+      dv[e] += pdv[e];
+    }
+  }
+  free(part);
 }

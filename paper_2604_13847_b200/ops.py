@@ -178,7 +178,10 @@ def coverage_profile(scores: torch.Tensor, lay: VarlenLayout) -> torch.Tensor:
 def coverage_at_grid(profile: torch.Tensor, lay: VarlenLayout, grid) -> torch.Tensor:
     """K4b: C[s][g] = coverage(profile_s, grid[g]) (reference dst.cpp:53-61 arithmetic)."""
     _need_cuda(profile)
-    g = torch.as_tensor(np.asarray(grid, np.int32), device=profile.device)
+    if isinstance(grid, torch.Tensor) and grid.is_cuda and grid.dtype == torch.int32:
+        g = grid
+    else:
+        g = torch.as_tensor(np.asarray(grid, np.int32), device=profile.device)
     out = torch.empty((lay.nseq, len(g)), dtype=torch.float64, device=profile.device)
     _call("sb_coverage_at_grid", _ptr(profile), _ptr(lay.blk_off), lay.nseq, profile.shape[1], _ptr(g), len(g),
           _ptr(out), _stream())
