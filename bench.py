@@ -44,23 +44,10 @@ def peaks():
 
 
 def workload(rank: int):
-    """Sequence lengths (reference generator, 40% 32K / 60% 2K) filled to exactly 32768 tokens,
-    and per-sequence keep counts."""
-    from paper_2604_13847_b200.host import api
-
-    h = api()
-    dist = dict(short_weight=0.6, short_log_mean=float(np.log(2048)), short_log_sigma=0.0,
-                long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
-    L, _ = h.generate_samples(64, 1, CFG["block"], seed=CFG["seed"] * 1000 + rank, dist=dist)
-    lens, tot = [], 0
-    for x in L:
-        x = int(min(x, CFG["tokens"] - tot))
-        if x <= 0:
-            break
-        lens.append(x)
-        tot += x
-    if tot < CFG["tokens"]:
-        lens.append(CFG["tokens"] - tot)
+    """C2 micro-batch of 32768 tokens: the SURVEY.md section 8(d) example composition
+    [12288, 8192, 4096, 2048 x 4] packed with cu_seqlens, and per-sequence keep ratios
+    U[0.05, 0.5] seeded by rank (so ranks carry different sparse work)."""
+    lens = [12288, 8192, 4096, 2048, 2048, 2048, 2048]
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     rng = np.random.default_rng(CFG["seed"] + 7919 * rank)
     nb = (np.array(lens) + CFG["block"] - 1) // CFG["block"]
@@ -198,6 +185,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="2 plain steps then exit (for ncu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -251,6 +239,11 @@ def main():
 
     idx, cnt, *_ = step()
     torch.cuda.synchronize()
+    if args.profile_only:
+        step()
+        torch.cuda.synchronize()
+        print("profile-only: 2 steps done")
+        return
     f_fwd, f_bwd = useful_flops(cu, B, idx.cpu().numpy(), cnt.cpu().numpy(), D)
     f_step = f_fwd + f_bwd
     for _ in range(args.warmup):
@@ -340,8 +333,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C2: 32K-token packed varlen micro-batch per rank (reference bimodal generator "
-                                   "40% 32K / 60% 2K, seeded by rank), 32 heads MHA, d128, B128, per-sequence keep "
+            "config": {"workload": "C2: 32K-token packed varlen micro-batch per rank ([12288, 8192, 4096, 2048x4], "
+                                   "SURVEY 8d), 32 heads MHA, d128, B128, per-sequence keep "
                                    "U[0.05,0.5], scorer+profile+selector+fwd+bwd",
                        "seqs_rank0": int(len(cu) - 1), "tokens_per_rank": T, "l2": "inputs 256 MB each > L2, no flush",
                        "parallelism": f"dp{world}"},
