@@ -77,10 +77,10 @@ int sb_topk_select(const float* scores, const int32_t* blk_off, const int64_t* t
  * padded). workspace: sb_coverage_profile_workspace_size() bytes.
  * Replaces: RoutingProfile of a sequence-layer (reference workload.hpp:15-22) fed to
  * make_micro_batch / coverage / intrinsic_budget. */
-size_t sb_coverage_profile_workspace_size(int64_t tri_total, int hs);
+size_t sb_coverage_profile_workspace_size(int64_t tri_total, int hs, int nseq, int nb_max);
 int sb_coverage_profile(const float* scores, const int32_t* blk_off, const int64_t* tri_off,
-                        int nseq, int nb_total, int nb_max, int hs, void* workspace, double* profile,
-                        void* stream);
+                        int nseq, int nb_total, int64_t tri_total, int nb_max, int hs, void* workspace,
+                        double* profile, void* stream);
 
 /* K4b: C[s][g] = coverage(profile[s], grid[g]) exactly as reference dst.cpp:53-61
  * (sequential double sum; 0 for k <= 0; 1 for k >= nb_s). */
@@ -89,9 +89,10 @@ int sb_coverage_at_grid(const double* profile, const int32_t* blk_off, int nseq,
 
 /* K5: O = softmax(scale * Q K[I]^T) V[I] over the selected blocks of each q block, causal
  * inside the diagonal block, keys beyond the sequence end masked. Saves LSE (natural log).
- * tcgen05/TMEM tensor-core kernel with TMA-loaded K/V blocks.
+ * tcgen05/TMEM tensor-core kernel with TMA-loaded K/V blocks; persistent, longest-item-first
+ * (workspace: sb_sparse_attn_fwd_workspace_size() bytes for the work order).
  * Replaces: predict()-based attention latency in micro_batch_time (reference sim.cpp:88-98). */
-size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq);
+size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq, int k_max);
 int sb_sparse_attn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                        const int32_t* cu_seqlens, const int32_t* blk_off, int nseq, int total_tokens,
                        int nb_total, int hq, int hkv, int head_dim, int block_size,

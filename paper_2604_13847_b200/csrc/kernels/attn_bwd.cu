@@ -14,7 +14,9 @@
 // Warp roles as in the forward kernel: warp 0 TMA producer, warp 1 TMEM allocator + UMMA
 // issuer, warps 2..5 the elementwise softmax-gradient math (one TMEM lane per thread).
 #include "common.cuh"
+#include "fastmath.cuh"
 #include "sb_kernels.h"
+#include "sched.cuh"
 #include "sm100.cuh"
 #include "tmap.cuh"
 
@@ -31,29 +33,37 @@ constexpr float kLog2e = 1.4426950408889634f;
 __host__ __device__ constexpr uint32_t pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
 // ------------------------------------------------------------------------------------ prep
-__global__ void bwd_prep_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ d_o,
-                                const float* __restrict__ lse, int total, int hq, int d, int tp,
-                                float* __restrict__ lse2, float* __restrict__ dvec) {
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  const int per_lane = d / 32;  // 2 or 4 bf16
-  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < total * hq; row += warps) {
-    const int t = row / hq, h = row - t * hq;
-    const uint16_t* a = o + static_cast<size_t>(row) * d + lane * per_lane;
-    const uint16_t* b = d_o + static_cast<size_t>(row) * d + lane * per_lane;
+__global__ void __launch_bounds__(256) bwd_prep_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ d_o,
+                                                       const float* __restrict__ lse, int total, int hq, int d, int tp,
+                                                       float* __restrict__ lse2, float* __restrict__ dvec) {
+  // Each thread reduces 8 bf16 products (one 16-byte load of O and of dO); the d/8 threads of a
+  // row (16 for d=128, 8 for d=64) finish with xor-shuffles.
+  const int tpr = d >> 3;  // threads per row
+  const long long rows = static_cast<long long>(total) * hq;
+  const long long nthreads = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; g < rows * tpr; g += nthreads) {
+    const long long row = g / tpr;
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(o) + g);
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(d_o) + g);
+    const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
     float acc = 0.f;
-    for (int e = 0; e < per_lane; ++e) acc += bf2f(a[e]) * bf2f(b[e]);
 #pragma unroll
-    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) {
+    for (int e = 0; e < 4; ++e) {
+      acc = fmaf(__uint_as_float(wa[e] << 16), __uint_as_float(wb[e] << 16), acc);
+      acc = fmaf(__uint_as_float(wa[e] & 0xffff0000u), __uint_as_float(wb[e] & 0xffff0000u), acc);
+    }
+    for (int off = tpr >> 1; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((g % tpr) == 0) {
+      const int t = static_cast<int>(row / hq), h = static_cast<int>(row - static_cast<long long>(t) * hq);
       dvec[static_cast<size_t>(h) * tp + t] = acc;
       lse2[static_cast<size_t>(h) * tp + t] = lse[static_cast<size_t>(h) * total + t] * kLog2e;
     }
   }
   // Padding columns [total, tp): never read for valid rows, but keep them finite.
   const int pad = tp - total;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < hq * pad; e += gridDim.x * blockDim.x) {
-    const int h = e / pad, t = total + e % pad;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < static_cast<long long>(hq) * pad;
+       e += nthreads) {
+    const int h = static_cast<int>(e / pad), t = total + static_cast<int>(e % pad);
     dvec[static_cast<size_t>(h) * tp + t] = 0.f;
     lse2[static_cast<size_t>(h) * tp + t] = 0.f;
   }
@@ -141,6 +151,9 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
 }
 
 // ------------------------------------------------------------------------------------ dkv
+// Persistent: one CTA per SM walks key-block items (hk, gj) longest-first. Per item the CTA
+// holds K / V (128 key rows) and streams every (q head, q block) that selected the block
+// through a 2-stage Q / dO ring. TMEM: S^T | dP^T | dV | dK (512 columns for D = B = 128).
 template <int D, int B>
 struct DkvCfg {
   static constexpr int kChunks = D / 64;
@@ -154,11 +167,31 @@ struct DkvCfg {
 };
 
 struct DkvBars {
-  uint64_t kv_full;
+  uint64_t kv_full, kv_empty;
   uint64_t q_full[kStages], q_empty[kStages];
-  uint64_t s_full, p_full, done;
+  uint64_t st_full, dpt_full;  // UMMA -> softmax: S^T / dP^T in TMEM
+  uint64_t pt_full, dst_full;  // softmax -> UMMA: P^T / dS^T (bf16) in TMEM
+  uint64_t acc_done;           // UMMA -> epilogue: the item's dV / dK are final
   uint32_t tmem_base;
 };
+
+struct KvItem {
+  int hk, gj, s, jl, seq0, seq_len, e0, ne;
+};
+
+__device__ __forceinline__ KvItem decode_kv(int it, const int32_t* cu, const int32_t* blk_off, int nseq, int nbt,
+                                            const int32_t* tr_off) {
+  KvItem w;
+  w.hk = it / nbt;
+  w.gj = it - w.hk * nbt;
+  w.s = seq_of_block(blk_off, nseq, w.gj);
+  w.jl = w.gj - blk_off[w.s];
+  w.seq0 = cu[w.s];
+  w.seq_len = cu[w.s + 1] - w.seq0;
+  w.e0 = tr_off[it];
+  w.ne = tr_off[it + 1] - w.e0;
+  return w;
+}
 
 template <int D, int B>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
@@ -167,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off, int nseq, int hq, int hkv, int hsel,
     const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent, const float* __restrict__ lse2,
     const float* __restrict__ dvec, int tp, float scale, float scale_log2, uint16_t* __restrict__ dk,
-    uint16_t* __restrict__ dv) {
+    uint16_t* __restrict__ dv, const int32_t* __restrict__ order, int n_items) {
   using C = DkvCfg<D, B>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -180,27 +213,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
   DkvBars* bars = reinterpret_cast<DkvBars*>(smem + C::kSmemTiles);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gj = blockIdx.x, hk = blockIdx.y;
   const int nbt = blk_off[nseq];
-  const int s = seq_of_block(blk_off, nseq, gj);
-  const int jl = gj - blk_off[s];
-  const int seq0 = cu[s], seq_len = cu[s + 1] - seq0;
-  const int kv0 = seq0 + jl * B;
-  const int nkv = min(B, seq_len - jl * B);
-  const int w = hk * nbt + gj;
-  const int e0 = tr_off[w], ne = tr_off[w + 1] - e0;
-  const int sg = hq / hsel;          // q heads per selection row
-  const int items = ne * sg;
+  const int grid = gridDim.x, cta = blockIdx.x;
+  const int sg = hq / hsel;  // q heads per selection row
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->kv_full, 1);
+    mbar_init(&bars->kv_empty, 1);
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&bars->q_full[st], 2);  // TMA expect_tx arrive + vector-copy arrive
       mbar_init(&bars->q_empty[st], 1);
     }
-    mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->p_full, 128);
-    mbar_init(&bars->done, 1);
+    mbar_init(&bars->st_full, 1);
+    mbar_init(&bars->dpt_full, 1);
+    mbar_init(&bars->pt_full, 128);
+    mbar_init(&bars->dst_full, 128);
+    mbar_init(&bars->acc_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kCols>(&bars->tmem_base);
@@ -209,33 +237,45 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  auto item_head = [&](int m, int& h, int& gi) {
-    const int ent = __ldg(tr_ent + e0 + m / sg);
+  // (q head, q block) of the m-th pair of an item.
+  auto pair_of = [&](const KvItem& w, int m, int& h, int& gi) {
+    const int ent = __ldg(tr_ent + w.e0 + m / sg);
     const int hs = ent / nbt;
     gi = ent - hs * nbt;
     h = hs * sg + m % sg;
   };
 
   if (warp == 0) {
-    if (items > 0) {
+    // ------------------------------------------------------------ producer (whole warp)
+    if (lane == 0) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      tma_prefetch(&tm_do);
+    }
+    int g = 0, t = 0;  // global pair counter, item counter
+    for (int k = 0;; ++k) {
+      const int it = sched::snake_item(order, n_items, grid, cta, k);
+      if (it < 0) break;
+      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+      const int items = w.ne * sg;
+      if (items == 0) continue;
+      const int kv0 = w.seq0 + w.jl * B;
       if (lane == 0) {
-        tma_prefetch(&tm_q);
-        tma_prefetch(&tm_k);
-        tma_prefetch(&tm_v);
-        tma_prefetch(&tm_do);
+        mbar_wait(&bars->kv_empty, (t & 1) ^ 1);
         mbar_expect_tx(&bars->kv_full, 2 * C::kTileBytes);
         for (int c = 0; c < C::kChunks; ++c) {
-          tma_load_3d(k_smem + c * kM * 128, &tm_k, &bars->kv_full, c * 64, hk, kv0);
-          tma_load_3d(v_smem + c * kM * 128, &tm_v, &bars->kv_full, c * 64, hk, kv0);
+          tma_load_3d(k_smem + c * kM * 128, &tm_k, &bars->kv_full, c * 64, w.hk, kv0);
+          tma_load_3d(v_smem + c * kM * 128, &tm_v, &bars->kv_full, c * 64, w.hk, kv0);
         }
       }
-      for (int m = 0; m < items; ++m) {
-        const int st = m % kStages;
-        const uint32_t ph = (m / kStages) & 1;
+      for (int m = 0; m < items; ++m, ++g) {
+        const int st = g % kStages;
+        const uint32_t ph = (g / kStages) & 1;
         int h, gi;
-        item_head(m, h, gi);
-        const int q0 = seq0 + (gi - blk_off[s]) * B;
-        const int nq = min(B, seq_len - (gi - blk_off[s]) * B);
+        pair_of(w, m, h, gi);
+        const int q0 = w.seq0 + (gi - blk_off[w.s]) * B;
+        const int nq = min(B, w.seq_len - (gi - blk_off[w.s]) * B);
         mbar_wait(&bars->q_empty[st], ph ^ 1);
         if (lane == 0) {
           mbar_expect_tx(&bars->q_full[st], 2 * C::kQBytes);
@@ -253,117 +293,177 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->q_full[st]);
       }
+      ++t;
     }
   } else if (warp == 1) {
-    if (lane == 0 && items > 0) {
+    // ------------------------------------------------------------ UMMA issuer
+    // Per pair m of an item (P^T / dS^T are in the softmax warps' registers before they are
+    // written back, so the next S^T / dP^T overwrite TMEM while the math of m proceeds):
+    //   St_m, dPt_m | [P^T_m] dV_m, St_{m+1} | [dS^T_m] dK_m, dPt_{m+1} | ...
+    if (lane == 0) {
       constexpr uint32_t idesc_t = idesc_bf16_f32(kM, B, false, false);
       constexpr uint32_t idesc_acc = idesc_bf16_f32(kM, D, false, true);
       const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
-      mbar_wait(&bars->kv_full, 0);
-      for (int m = 0; m < items; ++m) {
-        const int st = m % kStages;
-        mbar_wait(&bars->q_full[st], (m / kStages) & 1);
+      auto qa = [&](int gg) { return smem_u32(q_smem + (gg % kStages) * C::kQBytes); };
+      auto da = [&](int gg) { return smem_u32(do_smem + (gg % kStages) * C::kQBytes); };
+      auto issue_st = [&](int gg) {
+        mbar_wait(&bars->q_full[gg % kStages], (gg / kStages) & 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(q_smem + st * C::kQBytes), da = smem_u32(do_smem + st * C::kQBytes);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
           const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
-          mma_ss(tmem + C::kSt, desc_sw128(k_addr + off_m, 16, 1024), desc_sw128(qa + off_n, 16, 1024), idesc_t,
-                 kk > 0);
-          mma_ss(tmem + C::kDPt, desc_sw128(v_addr + off_m, 16, 1024), desc_sw128(da + off_n, 16, 1024), idesc_t,
+          mma_ss(tmem + C::kSt, desc_sw128(k_addr + off_m, 16, 1024), desc_sw128(qa(gg) + off_n, 16, 1024), idesc_t,
                  kk > 0);
         }
-        tc_commit(&bars->s_full);
-        mbar_wait(&bars->p_full, m & 1);
-        tc_fence_after();
+        tc_commit(&bars->st_full);
+      };
+      auto issue_dpt = [&](int gg) {  // q_full of gg already observed by issue_st(gg)
 #pragma unroll
-        for (int kk = 0; kk < B / 16; ++kk) {
-          const uint32_t acc = (m > 0 || kk > 0) ? 1u : 0u;
-          mma_ts(tmem + C::kDV, tmem + C::kSt + kk * 8, desc_sw128(da + kk * 2048, B * 128, 1024), idesc_acc, acc);
-          mma_ts(tmem + C::kDK, tmem + C::kDPt + kk * 8, desc_sw128(qa + kk * 2048, B * 128, 1024), idesc_acc, acc);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
+          const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
+          mma_ss(tmem + C::kDPt, desc_sw128(v_addr + off_m, 16, 1024), desc_sw128(da(gg) + off_n, 16, 1024), idesc_t,
+                 kk > 0);
         }
-        tc_commit(&bars->q_empty[st]);
+        tc_commit(&bars->dpt_full);
+      };
+      int g = 0, t = 0;
+      for (int k = 0;; ++k) {
+        const int it = sched::snake_item(order, n_items, grid, cta, k);
+        if (it < 0) break;
+        const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+        const int items = w.ne * sg;
+        if (items == 0) continue;
+        mbar_wait(&bars->kv_full, t & 1);
+        issue_st(g);
+        issue_dpt(g);
+        for (int m = 0; m < items; ++m, ++g) {
+          mbar_wait(&bars->pt_full, g & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < B / 16; ++kk)
+            mma_ts(tmem + C::kDV, tmem + C::kSt + kk * 8, desc_sw128(da(g) + kk * 2048, B * 128, 1024), idesc_acc,
+                   (m > 0 || kk > 0) ? 1u : 0u);
+          if (m + 1 < items) issue_st(g + 1);
+          else tc_commit(&bars->kv_empty);  // K (last S^T) and V (last dP^T) no longer read
+          mbar_wait(&bars->dst_full, g & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < B / 16; ++kk)
+            mma_ts(tmem + C::kDK, tmem + C::kDPt + kk * 8, desc_sw128(qa(g) + kk * 2048, B * 128, 1024), idesc_acc,
+                   (m > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&bars->q_empty[g % kStages]);
+          if (m + 1 < items) issue_dpt(g + 1);
+        }
+        tc_commit(&bars->acc_done);
+        ++t;
       }
-      tc_commit(&bars->done);
     }
   } else {
+    // ------------------------------------------------------------ softmax-gradient + epilogue
     const int quarter = warp & 3;
     const int c = quarter * 32 + lane;  // key row
     const uint32_t lf = static_cast<uint32_t>(quarter * 32) << 16;
-    for (int m = 0; m < items; ++m) {
-      const int st = m % kStages;
-      int h, gi;
-      item_head(m, h, gi);
-      const int il = gi - blk_off[s];
-      const int nq = min(B, seq_len - il * B);
-      const bool diag = il == jl;
-      const float* vs = vec_smem + st * 2 * B;
-      mbar_wait(&bars->q_full[st], (m / kStages) & 1);  // producer's plain smem writes of vs
-      mbar_wait(&bars->s_full, m & 1);
-      tc_fence_after();
+    int g = 0, t = 0;
+    for (int k = 0;; ++k) {
+      const int it = sched::snake_item(order, n_items, grid, cta, k);
+      if (it < 0) break;
+      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+      const int items = w.ne * sg;
+      const int kv0 = w.seq0 + w.jl * B;
+      const int nkv = min(B, w.seq_len - w.jl * B);
+      for (int m = 0; m < items; ++m, ++g) {
+        const int st = g % kStages;
+        int h, gi;
+        pair_of(w, m, h, gi);
+        const int il = gi - blk_off[w.s];
+        const int nq = min(B, w.seq_len - il * B);
+        // Valid query columns r: inside the sequence, and causal (key row c <= r) on the diagonal.
+        const int r_lo = il == w.jl ? c : 0;
+        const float* vs = vec_smem + st * 2 * B;
+        mbar_wait(&bars->q_full[st], (g / kStages) & 1);  // producer's plain smem writes of vs
+        mbar_wait(&bars->st_full, g & 1);
+        tc_fence_after();
+        float p[B];
+        {
+          uint32_t sv[B / 32][32];
 #pragma unroll
-      for (int c2 = 0; c2 < B / 32; ++c2) {
-        uint32_t sv[32], pv[32];
-        tmem_ld32(tmem + lf + C::kSt + c2 * 32, sv);
-        tmem_ld32(tmem + lf + C::kDPt + c2 * 32, pv);
-        tmem_wait_ld();
-        uint32_t pp[16], dd[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float p[2], ds[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int r = c2 * 32 + e + u;
-            const bool ok = r < nq && (!diag || c <= r);
-            p[u] = ok ? exp2f(__uint_as_float(sv[e + u]) * scale_log2 - vs[r]) : 0.f;
-            ds[u] = p[u] * (__uint_as_float(pv[e + u]) - vs[B + r]);
-          }
-          pp[e / 2] = pack_bf16x2(p[0], p[1]);
-          dd[e / 2] = pack_bf16x2(ds[0], ds[1]);
-        }
-        tmem_st16(tmem + lf + C::kSt + c2 * 16, pp);
-        tmem_st16(tmem + lf + C::kDPt + c2 * 16, dd);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&bars->p_full);
-    }
-    if (items > 0) {
-      mbar_wait(&bars->done, 0);
-      tc_fence_after();
-    }
-    const bool store = c < nkv;
-    uint16_t* dv_row = dv + (static_cast<size_t>(kv0 + c) * hkv + hk) * D;
-    uint16_t* dk_row = dk + (static_cast<size_t>(kv0 + c) * hkv + hk) * D;
-#pragma unroll
-    for (int part = 0; part < 2; ++part) {
-      const uint32_t col = part == 0 ? C::kDV : C::kDK;
-      const float mul = part == 0 ? 1.0f : scale;
-      uint16_t* row = part == 0 ? dv_row : dk_row;
-#pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t v[32];
-        if (items > 0) {
-          tmem_ld32(tmem + lf + col + cc * 32, v);
+          for (int c2 = 0; c2 < B / 32; ++c2) tmem_ld32(tmem + lf + C::kSt + c2 * 32, sv[c2]);
           tmem_wait_ld();
-        } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = 0u;
+          for (int r = 0; r < B; ++r) {
+            const float e = ex2_mixed(fmaf(__uint_as_float(sv[r / 32][r % 32]), scale_log2, -vs[r]), r);
+            p[r] = (r < nq && r >= r_lo) ? e : 0.f;
+          }
         }
-        if (store) {
-          uint4* dst = reinterpret_cast<uint4*>(row + cc * 32);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint4 q4;
-            q4.x = pack_bf16x2(__uint_as_float(v[8 * e + 0]) * mul, __uint_as_float(v[8 * e + 1]) * mul);
-            q4.y = pack_bf16x2(__uint_as_float(v[8 * e + 2]) * mul, __uint_as_float(v[8 * e + 3]) * mul);
-            q4.z = pack_bf16x2(__uint_as_float(v[8 * e + 4]) * mul, __uint_as_float(v[8 * e + 5]) * mul);
-            q4.w = pack_bf16x2(__uint_as_float(v[8 * e + 6]) * mul, __uint_as_float(v[8 * e + 7]) * mul);
-            dst[e] = q4;
+        for (int c2 = 0; c2 < B / 64; ++c2) {
+          uint32_t pw[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) pw[e] = pack_bf16x2(p[c2 * 64 + 2 * e], p[c2 * 64 + 2 * e + 1]);
+          tmem_st32(tmem + lf + C::kSt + c2 * 32, pw);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->pt_full);
+        mbar_wait(&bars->dpt_full, g & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c2 = 0; c2 < B / 32; ++c2) {
+          uint32_t pv[32];
+          tmem_ld32(tmem + lf + C::kDPt + c2 * 32, pv);
+          tmem_wait_ld();
+          uint32_t dd[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int r = c2 * 32 + e;
+            dd[e / 2] = pack_bf16x2(p[r] * (__uint_as_float(pv[e]) - vs[B + r]),
+                                    p[r + 1] * (__uint_as_float(pv[e + 1]) - vs[B + r + 1]));
+          }
+          tmem_st16(tmem + lf + C::kDPt + c2 * 16, dd);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->dst_full);
+      }
+      if (items > 0) {
+        mbar_wait(&bars->acc_done, t & 1);
+        tc_fence_after();
+        ++t;
+      }
+      // Epilogue: dV and dK * scale for the valid key rows (zeros if nobody selected the block).
+      const bool store = c < nkv;
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const uint32_t col = part == 0 ? C::kDV : C::kDK;
+        const float mul = part == 0 ? 1.0f : scale;
+        uint16_t* row = (part == 0 ? dv : dk) + (static_cast<size_t>(kv0 + c) * hkv + w.hk) * D;
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t v[32];
+          if (items > 0) {
+            tmem_ld32(tmem + lf + col + cc * 32, v);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = 0u;
+          }
+          if (store) {
+            uint4* dst = reinterpret_cast<uint4*>(row + cc * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              uint4 q4;
+              q4.x = pack_bf16x2(__uint_as_float(v[8 * e + 0]) * mul, __uint_as_float(v[8 * e + 1]) * mul);
+              q4.y = pack_bf16x2(__uint_as_float(v[8 * e + 2]) * mul, __uint_as_float(v[8 * e + 3]) * mul);
+              q4.z = pack_bf16x2(__uint_as_float(v[8 * e + 4]) * mul, __uint_as_float(v[8 * e + 5]) * mul);
+              q4.w = pack_bf16x2(__uint_as_float(v[8 * e + 6]) * mul, __uint_as_float(v[8 * e + 7]) * mul);
+              dst[e] = q4;
+            }
           }
         }
       }
+      tc_fence_before();  // epilogue TMEM reads precede the next item's dV / dK (ordered via pt/dst_full)
     }
   }
   tc_fence_before();
@@ -375,21 +475,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
 }
 
 // ------------------------------------------------------------------------------------ dq
+// Persistent over (q head, q block) items longest-first. Per item Q / dO (double-buffered
+// across items) stay resident and the selected K_j / V_j stream through rings.
+// TMEM: S0 | S1 | dP | dQ (S double-buffered so S_{j+1} overlaps the math of j).
 template <int D, int B>
 struct DqCfg {
   static constexpr int kChunks = D / 64;
-  static constexpr int kQBytes = kChunks * kM * 128;   // Q or dO tile (128 rows)
-  static constexpr int kKVBytes = kChunks * B * 128;   // K_j or V_j
-  static constexpr int kSmemTiles = 2 * kQBytes + 2 * kStages * kKVBytes;
-  static constexpr int kS = 0, kDP = B, kDQ = 2 * B;
-  static constexpr uint32_t kCols = pow2_cols(2 * B + D);
+  static constexpr int kQBytes = kChunks * kM * 128;  // Q or dO tile (128 rows)
+  static constexpr int kKVBytes = kChunks * B * 128;  // K_j or V_j
+  static constexpr int kVStages = (4 * kQBytes + 4 * kKVBytes + 1280 <= 232448) ? 2 : 1;  // smem opt-in max
+  static constexpr int kSmemTiles = 4 * kQBytes + kStages * kKVBytes + kVStages * kKVBytes;
+  static constexpr int kS0 = 0, kS1 = B, kDP = 2 * B, kDQ = 3 * B;
+  static constexpr uint32_t kCols = pow2_cols(3 * B + D);
   static constexpr int kSmemBytes = kSmemTiles + 1024 + 256;
 };
 
 struct DqBars {
-  uint64_t qdo_full;
+  uint64_t qdo_full[2], qdo_empty[2];
   uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
-  uint64_t s_full, ds_full, done;
+  uint64_t s_full[2], dp_full, ds_full, dq_done, dq_free;
   uint32_t tmem_base;
 };
 
@@ -400,41 +504,38 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
     const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off, int nseq, int hq, int hkv,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt, int hsel, int k_max,
     const float* __restrict__ lse2, const float* __restrict__ dvec, int tp, float scale, float scale_log2,
-    uint16_t* __restrict__ dq) {
+    uint16_t* __restrict__ dq, const int32_t* __restrict__ order, int n_items) {
   using C = DqCfg<D, B>;
+  constexpr int kVS = C::kVStages;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-  uint8_t* q_smem = smem;
-  uint8_t* do_smem = smem + C::kQBytes;
-  uint8_t* k_smem = smem + 2 * C::kQBytes;
-  uint8_t* v_smem = k_smem + kStages * C::kKVBytes;
+  uint8_t* q_smem = smem;                            // [2]
+  uint8_t* do_smem = smem + 2 * C::kQBytes;          // [2]
+  uint8_t* k_smem = smem + 4 * C::kQBytes;           // [kStages]
+  uint8_t* v_smem = k_smem + kStages * C::kKVBytes;  // [kVS]
   DqBars* bars = reinterpret_cast<DqBars*>(smem + C::kSmemTiles);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gi = blockIdx.x, h = blockIdx.y;
   const int nbt = blk_off[nseq];
-  const int s = seq_of_block(blk_off, nseq, gi);
-  const int i = gi - blk_off[s];
-  const int seq0 = cu[s], seq_len = cu[s + 1] - seq0;
-  const int row0 = seq0 + i * B;
-  const int nrows = min(B, seq_len - i * B);
-  const int hk = h / (hq / hkv);
-  const int srow = h / (hq / hsel);
-  const int32_t* list = idx + (static_cast<size_t>(srow) * nbt + gi) * k_max;
-  const int n = cnt[static_cast<size_t>(srow) * nbt + gi];
+  const int grid = gridDim.x, cta = blockIdx.x;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars->qdo_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars->qdo_full[b], 1);
+      mbar_init(&bars->qdo_empty[b], 1);
+      mbar_init(&bars->s_full[b], 1);
+    }
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&bars->k_full[st], 1);
       mbar_init(&bars->k_empty[st], 1);
       mbar_init(&bars->v_full[st], 1);
       mbar_init(&bars->v_empty[st], 1);
     }
-    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->dp_full, 1);
     mbar_init(&bars->ds_full, 128);
-    mbar_init(&bars->done, 1);
+    mbar_init(&bars->dq_done, 1);
+    mbar_init(&bars->dq_free, 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kCols>(&bars->tmem_base);
@@ -443,133 +544,251 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
+  struct QItem {
+    int h, gi, s, i, seq0, seq_len, n;
+    const int32_t* list;
+  };
+  auto decode_q = [&](int it) {
+    QItem w;
+    w.h = it / nbt;
+    w.gi = it - w.h * nbt;
+    w.s = seq_of_block(blk_off, nseq, w.gi);
+    w.i = w.gi - blk_off[w.s];
+    w.seq0 = cu[w.s];
+    w.seq_len = cu[w.s + 1] - w.seq0;
+    const int srow = w.h / (hq / hsel);
+    w.list = idx + (static_cast<size_t>(srow) * nbt + w.gi) * k_max;
+    w.n = cnt[static_cast<size_t>(srow) * nbt + w.gi];
+    return w;
+  };
+
   if (warp == 0) {
-    if (lane == 0 && n > 0) {
+    if (lane == 0) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
       tma_prefetch(&tm_v);
       tma_prefetch(&tm_do);
-      mbar_expect_tx(&bars->qdo_full, 2 * C::kQBytes);
-      for (int c = 0; c < C::kChunks; ++c) {
-        tma_load_3d(q_smem + c * kM * 128, &tm_q, &bars->qdo_full, c * 64, h, row0);
-        tma_load_3d(do_smem + c * kM * 128, &tm_do, &bars->qdo_full, c * 64, h, row0);
-      }
-      for (int j = 0; j < n; ++j) {
-        const int st = j % kStages;
-        const uint32_t ph = (j / kStages) & 1;
-        const int kv_row = seq0 + __ldg(list + j) * B;
-        mbar_wait(&bars->k_empty[st], ph ^ 1);
-        mbar_expect_tx(&bars->k_full[st], C::kKVBytes);
-        for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(k_smem + st * C::kKVBytes + c * B * 128, &tm_k, &bars->k_full[st], c * 64, hk, kv_row);
-        mbar_wait(&bars->v_empty[st], ph ^ 1);
-        mbar_expect_tx(&bars->v_full[st], C::kKVBytes);
-        for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(v_smem + st * C::kKVBytes + c * B * 128, &tm_v, &bars->v_full[st], c * 64, hk, kv_row);
+      int g = 0, q = 0;
+      for (int k = 0;; ++k) {
+        const int it = sched::snake_item(order, n_items, grid, cta, k);
+        if (it < 0) break;
+        const QItem w = decode_q(it);
+        if (w.n <= 0) continue;
+        const int hk = w.h / (hq / hkv);
+        const int qb = q & 1;
+        const int row0 = w.seq0 + w.i * B;
+        mbar_wait(&bars->qdo_empty[qb], ((q >> 1) & 1) ^ 1);
+        mbar_expect_tx(&bars->qdo_full[qb], 2 * C::kQBytes);
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_3d(q_smem + qb * C::kQBytes + c * kM * 128, &tm_q, &bars->qdo_full[qb], c * 64, w.h, row0);
+          tma_load_3d(do_smem + qb * C::kQBytes + c * kM * 128, &tm_do, &bars->qdo_full[qb], c * 64, w.h, row0);
+        }
+        for (int j = 0; j < w.n; ++j, ++g) {
+          const int kv_row = w.seq0 + __ldg(w.list + j) * B;
+          const int st = g % kStages;
+          mbar_wait(&bars->k_empty[st], ((g / kStages) & 1) ^ 1);
+          mbar_expect_tx(&bars->k_full[st], C::kKVBytes);
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_3d(k_smem + st * C::kKVBytes + c * B * 128, &tm_k, &bars->k_full[st], c * 64, hk, kv_row);
+          const int vst = g % kVS;
+          mbar_wait(&bars->v_empty[vst], ((g / kVS) & 1) ^ 1);
+          mbar_expect_tx(&bars->v_full[vst], C::kKVBytes);
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_3d(v_smem + vst * C::kKVBytes + c * B * 128, &tm_v, &bars->v_full[vst], c * 64, hk, kv_row);
+        }
+        ++q;
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && n > 0) {
+    // Global block stream g over all items: S_0, dP_0 | S_{g+1} (other S buffer) overlaps the
+    // math of g | [dS_g] dQ_g, dP_{g+1} | ...  The next item's S / dP follow without a gap.
+    if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kM, B, false, false);
       constexpr uint32_t idesc_dq = idesc_bf16_f32(kM, D, false, true);
-      const uint32_t q_addr = smem_u32(q_smem), do_addr = smem_u32(do_smem);
       const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
-      mbar_wait(&bars->qdo_full, 0);
-      auto issue_dq = [&](int jj) {
-        const int st = jj % kStages;
-        mbar_wait(&bars->ds_full, jj & 1);
+      auto s_col = [](int gg) { return (gg & 1) ? C::kS1 : C::kS0; };
+      auto issue_s = [&](int gg, int qb) {
+        const int st = gg % kStages;
+        mbar_wait(&bars->k_full[st], (gg / kStages) & 1);
         tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < B / 16; ++kk)
-          mma_ts(tmem + C::kDQ, tmem + C::kS + kk * 8, desc_sw128(k_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024),
-                 idesc_dq, (jj > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(&bars->k_empty[st]);
-      };
-      for (int j = 0; j < n; ++j) {
-        const int st = j % kStages;
-        mbar_wait(&bars->k_full[st], (j / kStages) & 1);
-        mbar_wait(&bars->v_full[st], (j / kStages) & 1);
-        tc_fence_after();
-        if (j > 0) issue_dq(j - 1);  // frees S (dS alias) before S_j overwrites it (in-order pipe)
+        const uint32_t q_addr = smem_u32(q_smem + qb * C::kQBytes);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
           const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
-          mma_ss(tmem + C::kS, desc_sw128(q_addr + off_m, 16, 1024),
+          mma_ss(tmem + s_col(gg), desc_sw128(q_addr + off_m, 16, 1024),
                  desc_sw128(k_addr + st * C::kKVBytes + off_n, 16, 1024), idesc_s, kk > 0);
-          mma_ss(tmem + C::kDP, desc_sw128(do_addr + off_m, 16, 1024),
-                 desc_sw128(v_addr + st * C::kKVBytes + off_n, 16, 1024), idesc_s, kk > 0);
         }
-        tc_commit(&bars->v_empty[st]);
-        tc_commit(&bars->s_full);
+        tc_commit(&bars->s_full[gg & 1]);
+      };
+      auto issue_dp = [&](int gg, int qb, bool last_of_item) {
+        const int vst = gg % kVS;
+        mbar_wait(&bars->v_full[vst], (gg / kVS) & 1);
+        tc_fence_after();
+        const uint32_t do_addr = smem_u32(do_smem + qb * C::kQBytes);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
+          const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
+          mma_ss(tmem + C::kDP, desc_sw128(do_addr + off_m, 16, 1024),
+                 desc_sw128(v_addr + vst * C::kKVBytes + off_n, 16, 1024), idesc_s, kk > 0);
+        }
+        tc_commit(&bars->dp_full);
+        tc_commit(&bars->v_empty[vst]);
+        if (last_of_item) tc_commit(&bars->qdo_empty[qb]);  // last S (earlier) and dP of the item
+      };
+      // Flattened stream: for each block g know (item q, local j, item length n).
+      int g = 0, q = 0;
+      int cur_k = 0;
+      QItem cur;
+      auto next_item = [&](int& kk_, QItem& w) -> bool {
+        for (;; ++kk_) {
+          const int it = sched::snake_item(order, n_items, grid, cta, kk_);
+          if (it < 0) return false;
+          w = decode_q(it);
+          if (w.n > 0) {
+            ++kk_;
+            return true;
+          }
+        }
+      };
+      bool have = next_item(cur_k, cur);
+      if (have) {
+        mbar_wait(&bars->qdo_full[0], 0);
+        issue_s(0, 0);
+        issue_dp(0, 0, cur.n == 1);
       }
-      issue_dq(n - 1);
-      tc_commit(&bars->done);
+      while (have) {
+        const int qb = q & 1;
+        const int n = cur.n;
+        QItem pending = cur;
+        int pending_k = cur_k;
+        bool pending_have = false;
+        for (int j = 0; j < n; ++j, ++g) {
+          // Look ahead: the next block of the stream (same item, or the first of the next one).
+          const bool last = j + 1 == n;
+          QItem nxt;
+          int nk = cur_k;
+          bool have_next = false;
+          if (!last) {
+            issue_s(g + 1, qb);
+          } else {
+            have_next = next_item(nk, nxt);
+            if (have_next) {
+              mbar_wait(&bars->qdo_full[qb ^ 1], ((q + 1) >> 1) & 1);
+              issue_s(g + 1, qb ^ 1);
+            }
+          }
+          mbar_wait(&bars->ds_full, g & 1);
+          tc_fence_after();
+          if (j == 0) mbar_wait(&bars->dq_free, (q & 1) ^ 1);  // previous item's dQ read out
+          const int st = g % kStages;
+#pragma unroll
+          for (int kk = 0; kk < B / 16; ++kk)
+            mma_ts(tmem + C::kDQ, tmem + s_col(g) + kk * 8,
+                   desc_sw128(k_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024), idesc_dq,
+                   (j > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&bars->k_empty[st]);
+          if (last) tc_commit(&bars->dq_done);
+          if (!last) {
+            issue_dp(g + 1, qb, j + 2 == n);
+          } else if (have_next) {
+            issue_dp(g + 1, qb ^ 1, nxt.n == 1);
+          }
+          if (last) {
+            pending = nxt;
+            pending_k = nk;
+            pending_have = have_next;
+          }
+        }
+        cur = pending;
+        cur_k = pending_k;
+        have = pending_have;
+        ++q;
+      }
     }
   } else {
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lf = static_cast<uint32_t>(quarter * 32) << 16;
-    const bool valid = r < nrows;
-    const float l2 = valid ? __ldg(lse2 + static_cast<size_t>(h) * tp + row0 + r) : 0.f;
-    const float dd = valid ? __ldg(dvec + static_cast<size_t>(h) * tp + row0 + r) : 0.f;
-    for (int j = 0; j < n; ++j) {
-      const int jb = __ldg(list + j);
-      const int key_lim = min(B, seq_len - jb * B);
-      const int lim = valid ? min(key_lim, jb == i ? r + 1 : B) : 0;
-      mbar_wait(&bars->s_full, j & 1);
-      tc_fence_after();
+    int g = 0, q = 0;
+    for (int k = 0;; ++k) {
+      const int it = sched::snake_item(order, n_items, grid, cta, k);
+      if (it < 0) break;
+      const QItem w = decode_q(it);
+      const int row0 = w.seq0 + w.i * B;
+      const int nrows = min(B, w.seq_len - w.i * B);
+      const bool valid = r < nrows;
+      uint16_t* dq_row = dq + (static_cast<size_t>(row0 + r) * hq + w.h) * D;
+      if (w.n <= 0) {
+        if (valid)
+          for (int e = 0; e < D / 8; ++e) reinterpret_cast<uint4*>(dq_row)[e] = make_uint4(0, 0, 0, 0);
+        continue;
+      }
+      const float l2 = valid ? __ldg(lse2 + static_cast<size_t>(w.h) * tp + row0 + r) : 0.f;
+      const float dd = valid ? __ldg(dvec + static_cast<size_t>(w.h) * tp + row0 + r) : 0.f;
+      for (int j = 0; j < w.n; ++j, ++g) {
+        const int jb = __ldg(w.list + j);
+        const int key_lim = min(B, w.seq_len - jb * B);
+        const int lim = valid ? min(key_lim, jb == w.i ? r + 1 : B) : 0;
+        const uint32_t s_col = (g & 1) ? C::kS1 : C::kS0;
+        mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
+        tc_fence_after();
+        float p[B];
+        {
+          uint32_t sv[B / 32][32];
 #pragma unroll
-      for (int c2 = 0; c2 < B / 32; ++c2) {
-        uint32_t sv[32], pv[32];
-        tmem_ld32(tmem + lf + C::kS + c2 * 32, sv);
-        tmem_ld32(tmem + lf + C::kDP + c2 * 32, pv);
-        tmem_wait_ld();
-        uint32_t dsp[16];
+          for (int c2 = 0; c2 < B / 32; ++c2) tmem_ld32(tmem + lf + s_col + c2 * 32, sv[c2]);
+          tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float ds[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int col = c2 * 32 + e + u;
-            const float p = col < lim ? exp2f(__uint_as_float(sv[e + u]) * scale_log2 - l2) : 0.f;
-            ds[u] = p * (__uint_as_float(pv[e + u]) - dd);
+          for (int c = 0; c < B; ++c) {
+            const float e = ex2_mixed(fmaf(__uint_as_float(sv[c / 32][c % 32]), scale_log2, -l2), c);
+            p[c] = c < lim ? e : 0.f;
           }
-          dsp[e / 2] = pack_bf16x2(ds[0], ds[1]);
         }
-        tmem_st16(tmem + lf + C::kS + c2 * 16, dsp);
+        mbar_wait(&bars->dp_full, g & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c2 = 0; c2 < B / 32; ++c2) {
+          uint32_t pv[32];
+          tmem_ld32(tmem + lf + C::kDP + c2 * 32, pv);
+          tmem_wait_ld();
+          uint32_t dsp[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int c = c2 * 32 + e;
+            dsp[e / 2] = pack_bf16x2(p[c] * (__uint_as_float(pv[e]) - dd), p[c + 1] * (__uint_as_float(pv[e + 1]) - dd));
+          }
+          tmem_st16(tmem + lf + s_col + c2 * 16, dsp);  // dS over S (already in registers)
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->ds_full);
       }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&bars->ds_full);
-    }
-    if (n > 0) {
-      mbar_wait(&bars->done, 0);
+      mbar_wait(&bars->dq_done, q & 1);
       tc_fence_after();
-    }
-    uint16_t* row = dq + (static_cast<size_t>(row0 + r) * hq + h) * D;
+      uint32_t v[D / 32][32];
 #pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t v[32];
-      if (n > 0) {
-        tmem_ld32(tmem + lf + C::kDQ + cc * 32, v);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = 0u;
-      }
+      for (int cc = 0; cc < D / 32; ++cc) tmem_ld32(tmem + lf + C::kDQ + cc * 32, v[cc]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars->dq_free);
       if (valid) {
-        uint4* dst = reinterpret_cast<uint4*>(row + cc * 32);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          uint4 q4;
-          q4.x = pack_bf16x2(__uint_as_float(v[8 * e + 0]) * scale, __uint_as_float(v[8 * e + 1]) * scale);
-          q4.y = pack_bf16x2(__uint_as_float(v[8 * e + 2]) * scale, __uint_as_float(v[8 * e + 3]) * scale);
-          q4.z = pack_bf16x2(__uint_as_float(v[8 * e + 4]) * scale, __uint_as_float(v[8 * e + 5]) * scale);
-          q4.w = pack_bf16x2(__uint_as_float(v[8 * e + 6]) * scale, __uint_as_float(v[8 * e + 7]) * scale);
-          dst[e] = q4;
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint4* dst = reinterpret_cast<uint4*>(dq_row + cc * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint4 q4;
+            q4.x = pack_bf16x2(__uint_as_float(v[cc][8 * e + 0]) * scale, __uint_as_float(v[cc][8 * e + 1]) * scale);
+            q4.y = pack_bf16x2(__uint_as_float(v[cc][8 * e + 2]) * scale, __uint_as_float(v[cc][8 * e + 3]) * scale);
+            q4.z = pack_bf16x2(__uint_as_float(v[cc][8 * e + 4]) * scale, __uint_as_float(v[cc][8 * e + 5]) * scale);
+            q4.w = pack_bf16x2(__uint_as_float(v[cc][8 * e + 6]) * scale, __uint_as_float(v[cc][8 * e + 7]) * scale);
+            dst[e] = q4;
+          }
         }
       }
+      ++q;
     }
   }
   tc_fence_before();
@@ -581,8 +800,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
 }
 
 // ------------------------------------------------------------------------------------ host
+constexpr int kMaxKvCost = 4096;
+
 struct BwdWorkspace {
-  size_t lse2, dvec, tr_cnt, tr_off, tr_ent, total;
+  size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, total;
   int tp;
 };
 
@@ -602,6 +823,10 @@ BwdWorkspace bwd_layout(int total, int nb_total, int hq, int hkv, int hsel, int 
   off = align256(off + (static_cast<size_t>(hkv) * nb_total + 1) * 4);
   w.tr_ent = off;
   off = align256(off + static_cast<size_t>(hsel) * nb_total * k_max * 4);
+  w.order_q = off;
+  off = align256(off + sched::order_workspace_bytes(hq * nb_total, hq * (k_max + 1)));
+  w.order_kv = off;
+  off = align256(off + sched::order_workspace_bytes(hkv * nb_total, hkv * (kMaxKvCost + 1)));
   w.total = off;
   return w;
 }
@@ -618,19 +843,25 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   int32_t* tr_off = reinterpret_cast<int32_t*>(ws + w.tr_off);
   int32_t* tr_ent = reinterpret_cast<int32_t*>(ws + w.tr_ent);
   const float scale_log2 = scale * kLog2e;
+  const int sms = sched::num_sms();
 
-  bwd_prep_kernel<<<592, 256, 0, st>>>(o, d_o, lse, total, hq, D, w.tp, lse2, dvec);
+  bwd_prep_kernel<<<sms * 8, 256, 0, st>>>(o, d_o, lse, total, hq, D, w.tp, lse2, dvec);
   launched("sb_sparse_attn_bwd/prep");
-  const int warps = hkv * nb_total;
+  const int kv_items = hkv * nb_total;
   const int rows_per_kv = hsel / hkv;
-  transpose_sel_kernel<<<(warps + 3) / 4, 128, 0, st>>>(idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 0, tr_cnt,
-                                                         nullptr, nullptr);
+  transpose_sel_kernel<<<(kv_items + 3) / 4, 128, 0, st>>>(idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 0,
+                                                            tr_cnt, nullptr, nullptr);
   launched("sb_sparse_attn_bwd/transpose_count");
-  scan_kernel<<<1, 1024, 0, st>>>(tr_cnt, warps, tr_off);
+  scan_kernel<<<1, 1024, 0, st>>>(tr_cnt, kv_items, tr_off);
   launched("sb_sparse_attn_bwd/scan");
-  transpose_sel_kernel<<<(warps + 3) / 4, 128, 0, st>>>(idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 1, tr_cnt,
-                                                         tr_off, tr_ent);
+  transpose_sel_kernel<<<(kv_items + 3) / 4, 128, 0, st>>>(idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 1,
+                                                            tr_cnt, tr_off, tr_ent);
   launched("sb_sparse_attn_bwd/transpose_fill");
+  const int32_t* order_kv = sched::build_order(sched::CostFromLists{tr_off, hq / hsel, kMaxKvCost, nb_total, hkv},
+                                               kv_items, ws + w.order_kv, st, "sb_sparse_attn_bwd/order_kv");
+  const int q_items = hq * nb_total;
+  const int32_t* order_q = sched::build_order(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, q_items,
+                                              ws + w.order_q, st, "sb_sparse_attn_bwd/order_q");
 
   // dK / dV: key tiles are 128 rows (UMMA M); query tiles are B rows (UMMA N).
   {
@@ -642,9 +873,9 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
     auto kern = attn_bwd_dkv_kernel<D, B>;
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes),
                "sb_sparse_attn_bwd: smem attribute (dkv)");
-    kern<<<dim3(nb_total, hkv), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, cu, blk_off, nseq, hq, hkv, hsel,
-                                                               tr_off, tr_ent, lse2, dvec, w.tp, scale, scale_log2,
-                                                               dk, dv);
+    kern<<<std::min(kv_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, cu, blk_off, nseq, hq, hkv, hsel,
+                                                                   tr_off, tr_ent, lse2, dvec, w.tp, scale,
+                                                                   scale_log2, dk, dv, order_kv, kv_items);
     launched("sb_sparse_attn_bwd/dkv");
   }
   {
@@ -656,8 +887,9 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
     auto kern = attn_bwd_dq_kernel<D, B>;
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes),
                "sb_sparse_attn_bwd: smem attribute (dq)");
-    kern<<<dim3(nb_total, hq), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, cu, blk_off, nseq, hq, hkv, idx, cnt,
-                                                              hsel, k_max, lse2, dvec, w.tp, scale, scale_log2, dq);
+    kern<<<std::min(q_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, cu, blk_off, nseq, hq, hkv, idx,
+                                                                  cnt, hsel, k_max, lse2, dvec, w.tp, scale,
+                                                                  scale_log2, dq, order_q, q_items);
     launched("sb_sparse_attn_bwd/dq");
   }
 }

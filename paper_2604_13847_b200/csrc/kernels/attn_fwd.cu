@@ -1,21 +1,28 @@
 // K5: varlen block-sparse attention forward on tcgen05 / TMEM (Eq. 2).
 //
-// One CTA owns one (q block, q head) work item: a 128-row Q tile (B=128: the block; B=64:
-// the block plus 64 rows that are computed and discarded) and the list of selected key
-// blocks of its selection row. Warp roles:
-//   warp 0      TMA producer: Q once, then K_j / V_j of every selected block j into a
-//               2-stage ring (each selected block is a contiguous B x D slab -> plain
-//               tensor-map boxes, no element gather).
-//   warp 1      TMEM allocator + single-thread UMMA issuer:
-//                 S_j = Q K_j^T   (SS, M=128 N=B K=D)         -> TMEM S[j % 2]
-//                 O  += P_j V_j   (TS, A = P_j from TMEM, B = V_j MN-major smem)
-//               issue order QK_0, QK_1, PV_0, QK_2, PV_1, ... so QK_{j+1} overlaps softmax_j.
-//   warps 2..5  softmax: one TMEM lane (= query row) per thread; online softmax in the
-//               log2 domain with lazy O rescaling (only when the row max grows by > 8),
-//               P_j written back into TMEM as packed bf16 over S_j, final O / l and LSE.
+// Persistent kernel: one CTA per SM walks a longest-first list of work items (one item = one
+// q block x q head: a 128-row Q tile -- for B=64 the block plus 64 rows computed and
+// discarded -- and the selected key blocks of its selection row). Warp roles:
+//   warp 0      TMA producer: Q of each item (2 buffers, so the next item's Q arrives while
+//               the current one runs) and K_j / V_j of every selected block into a 2-stage
+//               ring (each selected block is a contiguous B x D slab -> plain tensor-map
+//               boxes, no element gather).
+//   warp 1      TMEM allocator + single-thread UMMA issuer over the CTA's global block
+//               stream g (all items back to back):
+//                 S_g = Q K_g^T   (SS, M=128 N=B K=D)          -> TMEM S[g % 2]
+//                 O  += P_g V_g   (TS, A = P_g from TMEM, B = V_g MN-major in smem)
+//               issue order QK_0, QK_1, PV_0, QK_2, PV_1, ... across item boundaries, so the
+//               next item's first QK overlaps the last softmax and epilogue of the previous.
+//               O is double-buffered per item (TMEM: S0 | S1 | O0 | O1).
+//   warps 2..5  softmax: one TMEM lane (= query row) per thread; online softmax in the log2
+//               domain with lazy O rescaling (only when the row max grows by > 8); 3/8 of the
+//               exponentials on the FMA pipe (fastmath.cuh); P written back into TMEM as packed
+//               bf16 over S; epilogue O / l -> bf16 rows and LSE.
 // Masking: keys past the sequence end and the causal upper triangle of the diagonal block.
 #include "common.cuh"
+#include "fastmath.cuh"
 #include "sb_kernels.h"
+#include "sched.cuh"
 #include "sm100.cuh"
 #include "tmap.cuh"
 
@@ -24,71 +31,84 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kM = 128;            // UMMA M / Q tile rows
-constexpr int kStages = 2;         // K and V ring depth
-constexpr int kThreads = 192;      // 6 warps
+constexpr int kM = 128;                 // UMMA M / Q tile rows
+constexpr int kStages = 2;              // K and V ring depth
+constexpr int kThreads = 192;           // 6 warps
 constexpr float kRescaleThresh = 8.0f;  // log2 units: lazily rescale O only on a 256x max jump
 
 template <int D, int B>
 struct FwdCfg {
-  static constexpr int kChunks = D / 64;                 // 128-byte swizzle atoms along D
-  static constexpr int kQBytes = kChunks * kM * 128;     // Q tile
-  static constexpr int kKVBytes = kChunks * B * 128;     // one K or V block
-  static constexpr int kSmemTiles = kQBytes + 2 * kStages * kKVBytes;
-  static constexpr int kTmemS0 = 0, kTmemS1 = B, kTmemO = 2 * B;
-  static constexpr uint32_t kTmemCols = (2 * B + D) <= 256 ? 256 : 512;
+  static constexpr int kChunks = D / 64;              // 128-byte swizzle atoms along D
+  static constexpr int kQBytes = kChunks * kM * 128;  // one Q tile
+  static constexpr int kKVBytes = kChunks * B * 128;  // one K or V block
+  static constexpr int kSmemTiles = 2 * kQBytes + 2 * kStages * kKVBytes;
+  static constexpr int kTmemS0 = 0, kTmemS1 = B, kTmemO0 = 2 * B, kTmemO1 = 2 * B + D;
+  static constexpr uint32_t kTmemCols = (2 * B + 2 * D) <= 256 ? 256 : 512;
   static constexpr int kSmemBytes = kSmemTiles + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
 struct FwdBars {
-  uint64_t q_full;
+  uint64_t q_full[2], q_empty[2];
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
   uint64_t s_full[2], p_full[2];
-  uint64_t o_done;
+  uint64_t o_done, o_free[2];
   uint32_t tmem_base;
 };
+
+struct Item {
+  int h, gi, s, i, seq0, seq_len, n;
+  const int32_t* list;
+};
+
+__device__ __forceinline__ Item decode(int it, const int32_t* cu, const int32_t* blk_off, int nseq, int nbt, int hq,
+                                       int hsel, const int32_t* idx, const int32_t* cnt, int k_max) {
+  Item w;
+  w.h = it / nbt;
+  w.gi = it - w.h * nbt;
+  w.s = seq_of_block(blk_off, nseq, w.gi);
+  w.i = w.gi - blk_off[w.s];
+  w.seq0 = cu[w.s];
+  w.seq_len = cu[w.s + 1] - w.seq0;
+  const int srow = w.h / (hq / hsel);
+  w.list = idx + (static_cast<size_t>(srow) * nbt + w.gi) * k_max;
+  w.n = cnt[static_cast<size_t>(srow) * nbt + w.gi];
+  return w;
+}
 
 template <int D, int B>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
     const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off,
     int nseq, int total_tokens, int hq, int hkv, const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt,
-    int hsel, int k_max, float scale_log2, uint16_t* __restrict__ out, float* __restrict__ lse) {
+    int hsel, int k_max, float scale_log2, uint16_t* __restrict__ out, float* __restrict__ lse,
+    const int32_t* __restrict__ order, int n_items) {
   using C = FwdCfg<D, B>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-  uint8_t* q_smem = smem;
-  uint8_t* k_smem = smem + C::kQBytes;
-  uint8_t* v_smem = k_smem + kStages * C::kKVBytes;
+  uint8_t* q_smem = smem;                                // [2]
+  uint8_t* k_smem = smem + 2 * C::kQBytes;               // [kStages]
+  uint8_t* v_smem = k_smem + kStages * C::kKVBytes;      // [kStages]
   FwdBars* bars = reinterpret_cast<FwdBars*>(smem + C::kSmemTiles);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gi = blockIdx.x, h = blockIdx.y;
   const int nbt = blk_off[nseq];
-  const int s = seq_of_block(blk_off, nseq, gi);
-  const int i = gi - blk_off[s];
-  const int seq0 = cu[s];
-  const int seq_len = cu[s + 1] - seq0;
-  const int row0 = seq0 + i * B;
-  const int nrows = min(B, seq_len - i * B);
-  const int hk = h / (hq / hkv);
-  const int srow = h / (hq / hsel);
-  const int32_t* list = idx + (static_cast<size_t>(srow) * nbt + gi) * k_max;
-  const int n = cnt[static_cast<size_t>(srow) * nbt + gi];
+  const int grid = gridDim.x, cta = blockIdx.x;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars->q_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars->q_full[b], 1);
+      mbar_init(&bars->q_empty[b], 1);
+      mbar_init(&bars->s_full[b], 1);
+      mbar_init(&bars->p_full[b], 128);
+      mbar_init(&bars->o_free[b], 128);
+    }
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&bars->k_full[st], 1);
       mbar_init(&bars->k_empty[st], 1);
       mbar_init(&bars->v_full[st], 1);
       mbar_init(&bars->v_empty[st], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bars->s_full[b], 1);
-      mbar_init(&bars->p_full[b], 128);
     }
     mbar_init(&bars->o_done, 1);
     fence_barrier_init();
@@ -101,40 +121,78 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && n > 0) {
+    if (lane == 0) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
       tma_prefetch(&tm_v);
-      mbar_expect_tx(&bars->q_full, C::kQBytes);
-      for (int c = 0; c < C::kChunks; ++c) tma_load_3d(q_smem + c * kM * 128, &tm_q, &bars->q_full, c * 64, h, row0);
-      for (int j = 0; j < n; ++j) {
-        const int st = j % kStages;
-        const uint32_t ph = (j / kStages) & 1;
-        const int kv_row = seq0 + __ldg(list + j) * B;
-        mbar_wait(&bars->k_empty[st], ph ^ 1);
-        mbar_expect_tx(&bars->k_full[st], C::kKVBytes);
+      int g = 0, q = 0;
+      for (int k = 0;; ++k) {
+        const int it = sched::snake_item(order, n_items, grid, cta, k);
+        if (it < 0) break;
+        const Item w = decode(it, cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
+        if (w.n <= 0) continue;
+        const int hk = w.h / (hq / hkv);
+        const int qb = q & 1;
+        mbar_wait(&bars->q_empty[qb], ((q >> 1) & 1) ^ 1);
+        mbar_expect_tx(&bars->q_full[qb], C::kQBytes);
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(k_smem + st * C::kKVBytes + c * B * 128, &tm_k, &bars->k_full[st], c * 64, hk, kv_row);
-        mbar_wait(&bars->v_empty[st], ph ^ 1);
-        mbar_expect_tx(&bars->v_full[st], C::kKVBytes);
-        for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(v_smem + st * C::kKVBytes + c * B * 128, &tm_v, &bars->v_full[st], c * 64, hk, kv_row);
+          tma_load_3d(q_smem + qb * C::kQBytes + c * kM * 128, &tm_q, &bars->q_full[qb], c * 64, w.h,
+                      w.seq0 + w.i * B);
+        for (int j = 0; j < w.n; ++j, ++g) {
+          const int st = g % kStages;
+          const uint32_t ph = (g / kStages) & 1;
+          const int kv_row = w.seq0 + __ldg(w.list + j) * B;
+          mbar_wait(&bars->k_empty[st], ph ^ 1);
+          mbar_expect_tx(&bars->k_full[st], C::kKVBytes);
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_3d(k_smem + st * C::kKVBytes + c * B * 128, &tm_k, &bars->k_full[st], c * 64, hk, kv_row);
+          mbar_wait(&bars->v_empty[st], ph ^ 1);
+          mbar_expect_tx(&bars->v_full[st], C::kKVBytes);
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_3d(v_smem + st * C::kKVBytes + c * B * 128, &tm_v, &bars->v_full[st], c * 64, hk, kv_row);
+        }
+        ++q;
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ UMMA issuer
-    if (lane == 0 && n > 0) {
+    if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(kM, B, false, false);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(kM, D, false, true);
-      const uint32_t q_addr = smem_u32(q_smem), k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
-      mbar_wait(&bars->q_full, 0);
-      tc_fence_after();
-      for (int j = 0; j <= n; ++j) {
-        if (j < n) {
-          const int st = j % kStages;
-          mbar_wait(&bars->k_full[st], (j / kStages) & 1);
+      const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
+      // Pending PV (the previous global block), issued after the next QK.
+      int pv_g = -1, pv_j = 0, pv_q = 0;
+      auto issue_pv = [&]() {
+        const int st = pv_g % kStages;
+        const int ob = pv_q & 1;
+        mbar_wait(&bars->v_full[st], (pv_g / kStages) & 1);
+        mbar_wait(&bars->p_full[pv_g & 1], (pv_g >> 1) & 1);
+        if (pv_j == 0) mbar_wait(&bars->o_free[ob], ((pv_q >> 1) & 1) ^ 1);  // epilogue of item q-2 done
+        tc_fence_after();
+        const uint32_t p_tmem = tmem + ((pv_g & 1) ? C::kTmemS1 : C::kTmemS0);
+        const uint32_t o_tmem = tmem + (ob ? C::kTmemO1 : C::kTmemO0);
+#pragma unroll
+        for (int kk = 0; kk < B / 16; ++kk) {
+          const uint64_t b = desc_sw128(v_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024);
+          mma_ts(o_tmem, p_tmem + kk * 8, b, idesc_pv, (pv_j > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(&bars->v_empty[st]);
+        tc_commit(&bars->o_done);
+      };
+      int g = 0, q = 0;
+      for (int k = 0;; ++k) {
+        const int it = sched::snake_item(order, n_items, grid, cta, k);
+        if (it < 0) break;
+        const Item w = decode(it, cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
+        if (w.n <= 0) continue;
+        const int qb = q & 1;
+        const uint32_t q_addr = smem_u32(q_smem + qb * C::kQBytes);
+        mbar_wait(&bars->q_full[qb], (q >> 1) & 1);
+        for (int j = 0; j < w.n; ++j, ++g) {
+          const int st = g % kStages;
+          mbar_wait(&bars->k_full[st], (g / kStages) & 1);
           tc_fence_after();
-          const uint32_t d_s = tmem + ((j & 1) ? C::kTmemS1 : C::kTmemS0);
+          const uint32_t d_s = tmem + ((g & 1) ? C::kTmemS1 : C::kTmemS0);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t koff = (kk & 3) * 32;  // 16 bf16 = 32 B inside the swizzle atom
@@ -142,130 +200,137 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
             const uint64_t b = desc_sw128(k_addr + st * C::kKVBytes + (kk >> 2) * (B * 128) + koff, 16, 1024);
             mma_ss(d_s, a, b, idesc_qk, kk > 0 ? 1u : 0u);
           }
-          tc_commit(&bars->s_full[j & 1]);
+          tc_commit(&bars->s_full[g & 1]);
           tc_commit(&bars->k_empty[st]);
+          if (j == w.n - 1) tc_commit(&bars->q_empty[qb]);
+          if (pv_g >= 0) issue_pv();
+          pv_g = g;
+          pv_j = j;
+          pv_q = q;
         }
-        if (j >= 1) {
-          const int jj = j - 1;
-          const int st = jj % kStages;
-          mbar_wait(&bars->v_full[st], (jj / kStages) & 1);
-          mbar_wait(&bars->p_full[jj & 1], (jj >> 1) & 1);
-          tc_fence_after();
-          const uint32_t p_tmem = tmem + ((jj & 1) ? C::kTmemS1 : C::kTmemS0);
-#pragma unroll
-          for (int kk = 0; kk < B / 16; ++kk) {
-            const uint64_t b = desc_sw128(v_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024);
-            mma_ts(tmem + C::kTmemO, p_tmem + kk * 8, b, idesc_pv, (jj > 0 || kk > 0) ? 1u : 0u);
-          }
-          tc_commit(&bars->v_empty[st]);
-          tc_commit(&bars->o_done);
-        }
+        ++q;
       }
+      if (pv_g >= 0) issue_pv();
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     const uint32_t lane_field = static_cast<uint32_t>(quarter * 32) << 16;
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < n; ++j) {
-      const int b = j & 1;
-      const uint32_t t_s = tmem + lane_field + (b ? C::kTmemS1 : C::kTmemS0);
-      const int jb = __ldg(list + j);
-      mbar_wait(&bars->s_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      float x[B];
-#pragma unroll
-      for (int c = 0; c < B / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_s + c * 32, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) x[c * 32 + e] = __uint_as_float(v[e]);
-      }
-      // Valid keys: inside the sequence, and causal on the diagonal block.
-      const int key_lim = min(B, seq_len - jb * B);
-      const int causal_lim = (jb == i) ? r + 1 : B;
-      const int lim = min(key_lim, causal_lim);
-      float mblk = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < B; ++c) {
-        x[c] = (c < lim) ? x[c] * scale_log2 : -INFINITY;
-        mblk = fmaxf(mblk, x[c]);
-      }
-      const float m_new = fmaxf(m_run, mblk);
-      const bool rescale = m_new > m_run + kRescaleThresh;
-      const float m_use = rescale ? m_new : m_run;
-      const float alpha = rescale ? exp2f(m_run - m_use) : 1.0f;
-      float sum = 0.f;
-#pragma unroll
-      for (int c = 0; c < B / 64; ++c) {
-        uint32_t w[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float p0 = exp2f(x[c * 64 + 2 * e] - m_use), p1 = exp2f(x[c * 64 + 2 * e + 1] - m_use);
-          sum += p0 + p1;
-          w[e] = pack_bf16x2(p0, p1);
+    int g = 0, q = 0;
+    for (int k = 0;; ++k) {
+      const int it = sched::snake_item(order, n_items, grid, cta, k);
+      if (it < 0) break;
+      const Item w = decode(it, cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
+      const int row0 = w.seq0 + w.i * B;
+      const int nrows = min(B, w.seq_len - w.i * B);
+      const bool store = r < nrows;
+      if (w.n <= 0) {  // nothing selected: zero output, LSE = -inf
+        if (store) {
+          uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<size_t>(row0 + r) * hq + w.h) * D);
+          for (int e = 0; e < D / 8; ++e) dst[e] = make_uint4(0, 0, 0, 0);
+          lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = -INFINITY;
         }
-        tmem_st32(t_s + c * 32, w);  // P_j (packed bf16) over the first B/2 columns of S_j
+        continue;
       }
-      l_run = l_run * alpha + sum;
-      tmem_wait_st();
-      if (j > 0) {
-        mbar_wait(&bars->o_done, (j - 1) & 1);  // PV_{j-1} finished writing O
+      const int ob = q & 1;
+      const uint32_t t_o = tmem + lane_field + (ob ? C::kTmemO1 : C::kTmemO0);
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < w.n; ++j, ++g) {
+        const int b = g & 1;
+        const uint32_t t_s = tmem + lane_field + (b ? C::kTmemS1 : C::kTmemS0);
+        const int jb = __ldg(w.list + j);
+        mbar_wait(&bars->s_full[b], (g >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, rescale)) {
-          const uint32_t t_o = tmem + lane_field + C::kTmemO;
+        uint32_t sv[B / 32][32];
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld32(t_o + c * 32, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-            tmem_st32(t_o + c * 32, v);
-          }
-          tmem_wait_st();
-        }
-      }
-      m_run = m_use;
-      tc_fence_before();
-      mbar_arrive(&bars->p_full[b]);
-    }
-    // Epilogue: O / l -> bf16 rows; LSE (natural log).
-    if (n > 0) {
-      mbar_wait(&bars->o_done, (n - 1) & 1);
-      tc_fence_after();
-    }
-    const float inv_l = (n > 0 && l_run > 0.f) ? 1.0f / l_run : 0.f;
-    const bool store = r < nrows;
-    uint16_t* orow = out + (static_cast<size_t>(row0 + r) * hq + h) * D;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t v[32];
-      if (n > 0) {
-        tmem_ld32(tmem + lane_field + C::kTmemO + c * 32, v);
+        for (int c = 0; c < B / 32; ++c) tmem_ld32(t_s + c * 32, sv[c]);
         tmem_wait_ld();
-      } else {
+        // Keys of off-diagonal blocks are all valid (earlier blocks of a sequence are full);
+        // the diagonal block masks the causal upper triangle and keys past the sequence end.
+        const bool diag = jb == w.i;
+        const int lim = diag ? min(min(B, w.seq_len - jb * B), r + 1) : B;
+        float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = 0u;
-      }
-      if (store) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(v[8 * e + 0]) * inv_l, __uint_as_float(v[8 * e + 1]) * inv_l);
-          w.y = pack_bf16x2(__uint_as_float(v[8 * e + 2]) * inv_l, __uint_as_float(v[8 * e + 3]) * inv_l);
-          w.z = pack_bf16x2(__uint_as_float(v[8 * e + 4]) * inv_l, __uint_as_float(v[8 * e + 5]) * inv_l);
-          w.w = pack_bf16x2(__uint_as_float(v[8 * e + 6]) * inv_l, __uint_as_float(v[8 * e + 7]) * inv_l);
-          dst[e] = w;
+        for (int c = 0; c < B; c += 2) {
+          const float a = __uint_as_float(sv[c / 32][c % 32]), b2 = __uint_as_float(sv[c / 32][c % 32 + 1]);
+          mx0 = fmaxf(mx0, (!diag || c < lim) ? a : -INFINITY);
+          mx1 = fmaxf(mx1, (!diag || c + 1 < lim) ? b2 : -INFINITY);
         }
+        const float m_new = fmaxf(m_run, fmaxf(mx0, mx1) * scale_log2);
+        const bool rescale = m_new > m_run + kRescaleThresh;
+        const float m_use = rescale ? m_new : m_run;
+        const float alpha = rescale ? ex2_sfu(m_run - m_use) : 1.0f;
+        float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < B / 64; ++c) {
+          uint32_t pw[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int c0 = c * 64 + 2 * e;
+            float p0 = ex2_mixed(fmaf(__uint_as_float(sv[c0 / 32][c0 % 32]), scale_log2, -m_use), c0);
+            float p1 = ex2_mixed(fmaf(__uint_as_float(sv[c0 / 32][c0 % 32 + 1]), scale_log2, -m_use), c0 + 1);
+            if (diag) {
+              p0 = c0 < lim ? p0 : 0.f;
+              p1 = c0 + 1 < lim ? p1 : 0.f;
+            }
+            sum0 += p0;
+            sum1 += p1;
+            pw[e] = pack_bf16x2(p0, p1);
+          }
+          tmem_st32(t_s + c * 32, pw);  // P (packed bf16) over the first B/2 columns of S
+        }
+        l_run = l_run * alpha + (sum0 + sum1);
+        tmem_wait_st();
+        if (j > 0) {
+          mbar_wait(&bars->o_done, (g - 1) & 1);  // PV_{g-1} (same item) finished writing O
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t v[32];
+              tmem_ld32(t_o + c * 32, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+              tmem_st32(t_o + c * 32, v);
+            }
+            tmem_wait_st();
+          }
+        }
+        m_run = m_use;
+        tc_fence_before();
+        mbar_arrive(&bars->p_full[b]);
       }
+      // Epilogue: wait for the item's last PV, O / l -> bf16 rows; LSE (natural log).
+      mbar_wait(&bars->o_done, (g - 1) & 1);
+      tc_fence_after();
+      const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
+      uint16_t* orow = out + (static_cast<size_t>(row0 + r) * hq + w.h) * D;
+      uint32_t v[D / 32][32];
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) tmem_ld32(t_o + c * 32, v[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars->o_free[ob]);  // O buffer may be overwritten by item q + 2
+      if (store) {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint4 o4;
+            o4.x = pack_bf16x2(__uint_as_float(v[c][8 * e + 0]) * inv_l, __uint_as_float(v[c][8 * e + 1]) * inv_l);
+            o4.y = pack_bf16x2(__uint_as_float(v[c][8 * e + 2]) * inv_l, __uint_as_float(v[c][8 * e + 3]) * inv_l);
+            o4.z = pack_bf16x2(__uint_as_float(v[c][8 * e + 4]) * inv_l, __uint_as_float(v[c][8 * e + 5]) * inv_l);
+            o4.w = pack_bf16x2(__uint_as_float(v[c][8 * e + 6]) * inv_l, __uint_as_float(v[c][8 * e + 7]) * inv_l);
+            dst[e] = o4;
+          }
+        }
+        lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = (m_run + log2f(l_run)) * 0.69314718055994531f;
+      }
+      ++q;
     }
-    if (store)
-      lse[static_cast<size_t>(h) * total_tokens + row0 + r] =
-          (n > 0) ? (m_run + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
   }
   tc_fence_before();
   __syncthreads();
@@ -278,50 +343,49 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
 template <int D, int B>
 void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* cu, const int32_t* blk_off,
                 int nseq, int total, int nb_total, int hq, int hkv, const int32_t* idx, const int32_t* cnt, int hsel,
-                int k_max, float scale, uint16_t* o, float* lse, cudaStream_t st) {
+                int k_max, float scale, uint16_t* o, float* lse, void* ws, cudaStream_t st) {
   using C = FwdCfg<D, B>;
+  const int n_items = hq * nb_total;
+  const int32_t* order = sched::build_order(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, n_items, ws, st,
+                                            "sb_sparse_attn_fwd/order");
   const CUtensorMap tq = make_thd_map(q, total, hq, D, kM);
   const CUtensorMap tk = make_thd_map(k, total, hkv, D, B);
   const CUtensorMap tv = make_thd_map(v, total, hkv, D, B);
   auto kern = attn_fwd_kernel<D, B>;
   cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes),
              "sb_sparse_attn_fwd: smem attribute");
-  dim3 grid(nb_total, hq);
+  const int grid = std::min(n_items, sched::num_sms());
   kern<<<grid, kThreads, C::kSmemBytes, st>>>(tq, tk, tv, cu, blk_off, nseq, total, hq, hkv, idx, cnt, hsel, k_max,
-                                              scale * 1.4426950408889634f, o, lse);
+                                              scale * 1.4426950408889634f, o, lse, order, n_items);
   launched("sb_sparse_attn_fwd");
 }
 
 }  // namespace
 }  // namespace sbk
 
-SB_API size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq) {
-  (void)nb_total;
-  (void)hq;
-  return 0;
+SB_API size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq, int k_max) {
+  return sbk::sched::order_workspace_bytes(nb_total * hq, hq * (k_max + 1));
 }
 
 SB_API int sb_sparse_attn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* cu_seqlens,
                               const int32_t* blk_off, int nseq, int total_tokens, int nb_total, int hq, int hkv,
                               int head_dim, int block_size, const int32_t* idx, const int32_t* cnt, int hsel,
                               int k_max, float scale, uint16_t* o, float* lse, void* workspace, void* stream) {
-  (void)workspace;
   return sbk::abi_call([&] {
     sbk::require(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128");
     sbk::require(block_size == 64 || block_size == 128, "block_size must be 64 or 128");
     sbk::require(hq >= 1 && hkv >= 1 && hq % hkv == 0, "hq must be a positive multiple of hkv");
     sbk::require(hsel >= 1 && hq % hsel == 0, "hsel must divide hq");
     sbk::require(k_max >= 1, "k_max must be >= 1");
-    sbk::require(hq <= 65535, "hq too large");
     if (nseq == 0 || nb_total == 0 || total_tokens == 0) return;
-    sbk::require(q && k && v && cu_seqlens && blk_off && idx && cnt && o && lse, "null pointer");
+    sbk::require(q && k && v && cu_seqlens && blk_off && idx && cnt && o && lse && workspace, "null pointer");
     sbk::require((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) % 16 == 0,
                  "q/k/v must be 16-byte aligned");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define SB_FWD_CASE(DD, BB)                                                                                      \
   if (head_dim == DD && block_size == BB)                                                                        \
     return sbk::launch_fwd<DD, BB>(q, k, v, cu_seqlens, blk_off, nseq, total_tokens, nb_total, hq, hkv, idx, cnt, \
-                                   hsel, k_max, scale, o, lse, st);
+                                   hsel, k_max, scale, o, lse, workspace, st);
     SB_FWD_CASE(128, 128)
     SB_FWD_CASE(128, 64)
     SB_FWD_CASE(64, 128)

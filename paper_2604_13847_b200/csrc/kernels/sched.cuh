@@ -1,0 +1,140 @@
+// Work order for the persistent attention kernels: head-major, longest-first within a head.
+//
+// Work items (one q block x head, or one key block x kv head) have very different costs in a
+// varlen batch with per-sequence keep counts (1 .. k_max selected blocks). Items are sorted by
+// the key (head, cost descending): keeping one head's items together makes the ~148 resident
+// CTAs share that head's K/V (or Q/dO) slabs in L2 (16 MB per head at 32K tokens, d=128),
+// while longest-first inside the head and across the whole list keeps the tail short. CTAs
+// walk the list in snake order (c, 2G-1-c, 2G+c, ...) with no device-side atomics in the hot
+// kernels. The sort is a counting sort on the device (histogram, scan, scatter).
+#pragma once
+
+#include "common.cuh"
+
+namespace sbk {
+namespace sched {
+namespace {  // internal linkage: included by several translation units
+
+// Sort keys in [0, bins): key = head * (max_cost + 1) + (max_cost - min(cost, max_cost)).
+struct CostFromCnt {  // fwd / dq: item = h * NB + gi, cost = cnt[srow(h)][gi]
+  const int32_t* cnt;
+  int max_cost;
+  int hq, hsel, nb_total;
+  __device__ int operator()(int item) const {
+    const int h = item / nb_total, gi = item - h * nb_total;
+    const int c = cnt[static_cast<size_t>(h / (hq / hsel)) * nb_total + gi];
+    return h * (max_cost + 1) + (max_cost - min(c, max_cost));
+  }
+  int bins() const { return hq * (max_cost + 1); }
+};
+
+struct CostFromLists {  // dkv: item = hk * NB + gj, cost = (#selection rows listing it) * heads per row
+  const int32_t* tr_off;
+  int per_entry;
+  int max_cost;
+  int nb_total, hkv;
+  __device__ int operator()(int item) const {
+    const int hk = item / nb_total;
+    const int c = (tr_off[item + 1] - tr_off[item]) * per_entry;
+    return hk * (max_cost + 1) + (max_cost - min(c, max_cost));
+  }
+  int bins() const { return hkv * (max_cost + 1); }
+};
+
+template <typename Key>
+__global__ void key_hist_kernel(Key key, int n_items, int32_t* __restrict__ hist) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += gridDim.x * blockDim.x)
+    atomicAdd(hist + key(i), 1);
+}
+
+// start[b] = number of items with key < b (exclusive scan, one CTA of 1024); resets the
+// histogram so it can serve as the scatter cursor.
+__global__ void __launch_bounds__(1024) key_start_kernel(int32_t* __restrict__ hist, int bins,
+                                                         int32_t* __restrict__ start) {
+  __shared__ int warp_sum[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base < bins; base += 1024) {
+    const int b = base + threadIdx.x;
+    const int v = b < bins ? hist[b] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int ws = warp_sum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, ws, o);
+        if (lane >= o) ws += y;
+      }
+      warp_sum[lane] = ws;
+    }
+    __syncthreads();
+    const int excl = carry + (warp ? warp_sum[warp - 1] : 0) + x - v;
+    if (b < bins) {
+      start[b] = excl;
+      hist[b] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+}
+
+template <typename Key>
+__global__ void scatter_kernel(Key key, int n_items, const int32_t* __restrict__ start,
+                               int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += gridDim.x * blockDim.x) {
+    const int b = key(i);
+    order[start[b] + atomicAdd(cursor + b, 1)] = i;
+  }
+}
+
+inline size_t order_workspace_bytes(int n_items, int bins) {
+  return (static_cast<size_t>(n_items) + 2 * static_cast<size_t>(bins) + 64) * sizeof(int32_t);
+}
+
+// Writes order[0..n_items) (ascending key) into ws. Returns the order pointer.
+template <typename Key>
+int32_t* build_order(Key key, int n_items, void* ws, cudaStream_t st, const char* who) {
+  const int bins = key.bins();
+  int32_t* order = static_cast<int32_t*>(ws);
+  int32_t* hist = order + n_items;
+  int32_t* start = hist + bins;
+  cuda_check(cudaMemsetAsync(hist, 0, sizeof(int32_t) * bins, st), who);
+  const int blocks = min(1184, (n_items + 255) / 256);
+  key_hist_kernel<<<blocks, 256, 0, st>>>(key, n_items, hist);
+  launched(who);
+  key_start_kernel<<<1, 1024, 0, st>>>(hist, bins, start);
+  launched(who);
+  scatter_kernel<<<blocks, 256, 0, st>>>(key, n_items, start, hist, order);
+  launched(who);
+  return order;
+}
+
+// Item handled by CTA `cta` of `grid` in round k of the snake order (or -1 when exhausted).
+__device__ __forceinline__ int snake_item(const int32_t* __restrict__ order, int n_items, int grid, int cta, int k) {
+  const int pos = k * grid + ((k & 1) ? (grid - 1 - cta) : cta);
+  return pos < n_items ? __ldg(order + pos) : -1;
+}
+
+inline int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "SM count");
+  }
+  return n;
+}
+
+}  // namespace
+}  // namespace sched
+}  // namespace sbk

@@ -219,20 +219,31 @@ __global__ void row_sorted_mass_kernel(const float* __restrict__ scores, const i
   for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = buf[j];
 }
 
-__global__ void profile_reduce_kernel(const float* __restrict__ sorted, const int32_t* __restrict__ blk_off,
-                                      const int64_t* __restrict__ tri_off, int nseq, int nb_max, int hs,
-                                      double* __restrict__ profile) {
-  const int s = blockIdx.y;
+// Partial sums per (sequence, rank r, head h) over the rows i >= r of that head, then a fixed
+// order sum over heads: deterministic and parallel over (s, r, h).
+__global__ void profile_partial_kernel(const float* __restrict__ sorted, const int32_t* __restrict__ blk_off,
+                                       const int64_t* __restrict__ tri_off, int nseq, int nb_max,
+                                       double* __restrict__ partial) {
+  const int s = blockIdx.y, h = blockIdx.z;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nb_max) return;
   const int nb = blk_off[s + 1] - blk_off[s];
   const int64_t tri = tri_off[nseq];
   double acc = 0.0;
+  const float* base = sorted + static_cast<size_t>(h) * tri + tri_off[s];
+  for (int i = r; i < nb; ++i) acc = __dadd_rn(acc, static_cast<double>(base[static_cast<int64_t>(i) * (i + 1) / 2 + r]));
+  partial[(static_cast<size_t>(h) * nseq + s) * nb_max + r] = acc;
+}
+
+__global__ void profile_reduce_kernel(const double* __restrict__ partial, const int32_t* __restrict__ blk_off,
+                                      int nseq, int nb_max, int hs, double* __restrict__ profile) {
+  const int s = blockIdx.y;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nb_max) return;
+  const int nb = blk_off[s + 1] - blk_off[s];
+  double acc = 0.0;
   if (r < nb) {
-    for (int h = 0; h < hs; ++h) {
-      const float* base = sorted + static_cast<size_t>(h) * tri + tri_off[s];
-      for (int i = r; i < nb; ++i) acc = __dadd_rn(acc, static_cast<double>(base[static_cast<int64_t>(i) * (i + 1) / 2 + r]));
-    }
+    for (int h = 0; h < hs; ++h) acc = __dadd_rn(acc, partial[(static_cast<size_t>(h) * nseq + s) * nb_max + r]);
     acc = acc / (static_cast<double>(hs) * static_cast<double>(nb));
   }
   profile[static_cast<size_t>(s) * nb_max + r] = acc;
@@ -276,15 +287,17 @@ SB_API int sb_topk_select(const float* scores, const int32_t* blk_off, const int
   });
 }
 
-SB_API size_t sb_coverage_profile_workspace_size(int64_t tri_total, int hs) {
-  return static_cast<size_t>(tri_total) * static_cast<size_t>(hs) * sizeof(float);
+SB_API size_t sb_coverage_profile_workspace_size(int64_t tri_total, int hs, int nseq, int nb_max) {
+  const size_t sorted = (static_cast<size_t>(tri_total) * static_cast<size_t>(hs) * sizeof(float) + 255) & ~size_t(255);
+  return sorted + static_cast<size_t>(hs) * static_cast<size_t>(nseq) * static_cast<size_t>(nb_max) * sizeof(double);
 }
 
 SB_API int sb_coverage_profile(const float* scores, const int32_t* blk_off, const int64_t* tri_off, int nseq,
-                               int nb_total, int nb_max, int hs, void* workspace, double* profile,
-                               void* stream) {
+                               int nb_total, int64_t tri_total_host, int nb_max, int hs, void* workspace,
+                               double* profile, void* stream) {
   return sbk::abi_call([&] {
     sbk::require(hs >= 1 && hs <= 65535, "hs must be in [1, 65535]");
+    sbk::require(tri_total_host >= 0, "tri_total must be >= 0");
     sbk::require(nb_max <= sbk::kMaxRow, "rows longer than 4096 blocks are not supported");
     if (nseq == 0 || nb_max == 0) return;
     sbk::require(scores && blk_off && tri_off && workspace && profile, "null pointer");
@@ -298,8 +311,13 @@ SB_API int sb_coverage_profile(const float* scores, const int32_t* blk_off, cons
                                                                         sorted);
       sbk::launched("sb_coverage_profile/sort");
     }
+    const size_t sorted_bytes = (static_cast<size_t>(tri_total_host) * hs * sizeof(float) + 255) & ~size_t(255);
+    double* partial = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + sorted_bytes);
+    dim3 g1((nb_max + 127) / 128, nseq, hs);
+    sbk::profile_partial_kernel<<<g1, 128, 0, st>>>(sorted, blk_off, tri_off, nseq, nb_max, partial);
+    sbk::launched("sb_coverage_profile/partial");
     dim3 g2((nb_max + 127) / 128, nseq);
-    sbk::profile_reduce_kernel<<<g2, 128, 0, st>>>(sorted, blk_off, tri_off, nseq, nb_max, hs, profile);
+    sbk::profile_reduce_kernel<<<g2, 128, 0, st>>>(partial, blk_off, nseq, nb_max, hs, profile);
     sbk::launched("sb_coverage_profile/reduce");
   });
 }

@@ -34,10 +34,10 @@ def _lib():
             "sb_block_pool": (i, [_vp, _vp, _vp, i, i, i, i, i, _vp, _vp]),
             "sb_block_scores": (i, [_vp, _vp, _vp, _vp, i, i, i, i, i, f, _vp, _vp]),
             "sb_topk_select": (i, [_vp, _vp, _vp, i, i, i, i, i, _vp, i, i, _vp, _vp, _vp]),
-            "sb_coverage_profile_workspace_size": (sz, [i64, i]),
-            "sb_coverage_profile": (i, [_vp, _vp, _vp, i, i, i, i, _vp, _vp, _vp]),
+            "sb_coverage_profile_workspace_size": (sz, [i64, i, i, i]),
+            "sb_coverage_profile": (i, [_vp, _vp, _vp, i, i, i64, i, i, _vp, _vp, _vp]),
             "sb_coverage_at_grid": (i, [_vp, _vp, i, i, _vp, i, _vp, _vp]),
-            "sb_sparse_attn_fwd_workspace_size": (sz, [i, i]),
+            "sb_sparse_attn_fwd_workspace_size": (sz, [i, i, i]),
             "sb_sparse_attn_fwd": (i, [_vp, _vp, _vp, _vp, _vp, i, i, i, i, i, i, i, _vp, _vp, i, i, f, _vp, _vp,
                                        _vp, _vp]),
             "sb_sparse_attn_bwd_workspace_size": (sz, [i, i, i, i, i, i, i]),
@@ -167,11 +167,11 @@ def coverage_profile(scores: torch.Tensor, lay: VarlenLayout) -> torch.Tensor:
     """K4a: per-sequence routing profile [nseq, nb_max] fp64 (zero padded)."""
     _need_cuda(scores)
     Hs = scores.shape[0]
-    ws = torch.empty(max(1, int(_lib().sb_coverage_profile_workspace_size(lay.tri_total, Hs))), dtype=torch.uint8,
-                     device=scores.device)
+    ws = torch.empty(max(1, int(_lib().sb_coverage_profile_workspace_size(lay.tri_total, Hs, lay.nseq, lay.nb_max))),
+                     dtype=torch.uint8, device=scores.device)
     prof = torch.empty((lay.nseq, max(1, lay.nb_max)), dtype=torch.float64, device=scores.device)
     _call("sb_coverage_profile", _ptr(scores), _ptr(lay.blk_off), _ptr(lay.tri_off), lay.nseq, lay.nb_total,
-          lay.nb_max, Hs, _ptr(ws), _ptr(prof), _stream())
+          lay.tri_total, lay.nb_max, Hs, _ptr(ws), _ptr(prof), _stream())
     return prof
 
 
@@ -197,9 +197,11 @@ def sparse_attn_fwd(q, k, v, lay: VarlenLayout, idx, cnt, scale: float | None = 
     scale = 1.0 / math.sqrt(D) if scale is None else scale
     o = torch.empty_like(q)
     lse = torch.empty((Hq, T), dtype=torch.float32, device=q.device)
+    ws = torch.empty(max(16, int(_lib().sb_sparse_attn_fwd_workspace_size(lay.nb_total, Hq, k_max))),
+                     dtype=torch.uint8, device=q.device)
     _call("sb_sparse_attn_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(lay.cu_seqlens), _ptr(lay.blk_off), lay.nseq, T,
           lay.nb_total, Hq, Hkv, D, lay.block_size, _ptr(idx), _ptr(cnt), hsel, k_max, C.c_float(scale), _ptr(o),
-          _ptr(lse), None, _stream())
+          _ptr(lse), _ptr(ws), _stream())
     return o, lse
 
 

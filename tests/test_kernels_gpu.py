@@ -150,6 +150,7 @@ ATTN_CASES = [
     ([0, 77, 700, 2000], 2, 1, 128, 64, "head", 0.4),
     ([0, 33, 1500], 2, 2, 64, 128, "head", 1.0),        # dense
     ([0, 128 * 20], 2, 2, 128, 128, "head", 0.05),      # k = 1: diagonal only
+    ([0, 8192, 9000, 12288], 8, 2, 64, 128, "head", 0.3),  # > 1 work item per persistent CTA
 ]
 
 
@@ -179,6 +180,8 @@ BWD_CASES = [
     ([0, 77, 700, 2000], 2, 1, 128, 64, "head", 0.4),
     ([0, 33, 1500], 2, 2, 64, 128, "head", 1.0),
     ([0, 2048], 4, 4, 64, 64, "head", 0.25),
+    ([0, 8192, 9000, 12288], 8, 2, 64, 128, "head", 0.3),   # > 1 work item per persistent CTA
+    ([0, 6000, 6100, 9000], 4, 4, 128, 128, "head", 0.5),
 ]
 
 
