@@ -258,12 +258,19 @@ def main():
     torch.cuda.synchronize()
     launches0 = ops.launch_count()
     with ClockSampler(local_rank) as clk:
+        time.sleep(0.3)  # let nvidia-smi start sampling
         t0.record(stream)
         for s in range(args.steps):
             step(evs[s])
         t1.record(stream)
         torch.cuda.synchronize()
-    launches = ops.launch_count() - launches0
+        launches = ops.launch_count() - launches0
+        # Keep the GPU under the same load (untimed) so the sampler sees >= ~1 s of it.
+        t_load = time.perf_counter()
+        while time.perf_counter() - t_load < 1.2:
+            for _ in range(args.steps):
+                step()
+            torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1) / args.steps

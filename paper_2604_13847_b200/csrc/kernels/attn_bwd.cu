@@ -150,6 +150,49 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
   if (threadIdx.x == 0) out[n] = carry;
 }
 
+// P^T row of one key row (this thread): p[r] = 2^(S^T[r] * scale_log2 - lse2[r]) over the B query
+// columns, packed FFMA2 with the per-column -lse2 from shared memory; kMasked zeroes columns
+// outside [r_lo, nq) (causal diagonal / sequence end).
+template <int B, bool kMasked>
+__device__ __forceinline__ void dkv_p(const uint32_t (&sv)[B / 32][32], const float* vs, float scale_log2, int r_lo,
+                                      int nq, float (&p)[B]) {
+  const f2 sc = mk2(scale_log2, scale_log2);
+#pragma unroll
+  for (int pe = 0; pe < B / 2; ++pe) {
+    const int r = 2 * pe;
+    const float2 nl = *reinterpret_cast<const float2*>(vs + r);
+    f2 e = ex2_pair(ffma2(mk2(__uint_as_float(sv[r / 32][r % 32]), __uint_as_float(sv[r / 32][r % 32 + 1])), sc,
+                          mk2(nl.x, nl.y)),
+                    pe);
+    if (kMasked) {
+      e.x = (r < nq && r >= r_lo) ? e.x : 0.f;
+      e.y = (r + 1 < nq && r + 1 >= r_lo) ? e.y : 0.f;
+    }
+    p[r] = e.x;
+    p[r + 1] = e.y;
+  }
+}
+
+// P row of one query row: p[c] = 2^(S[c] * scale_log2 - lse2) (row constant), kMasked zeroes
+// columns >= lim.
+template <int B, bool kMasked>
+__device__ __forceinline__ void dq_p(const uint32_t (&sv)[B / 32][32], float neg_l2, float scale_log2, int lim,
+                                     float (&p)[B]) {
+  const f2 sc = mk2(scale_log2, scale_log2), nl = mk2(neg_l2, neg_l2);
+#pragma unroll
+  for (int pe = 0; pe < B / 2; ++pe) {
+    const int c = 2 * pe;
+    f2 e = ex2_pair(ffma2(mk2(__uint_as_float(sv[c / 32][c % 32]), __uint_as_float(sv[c / 32][c % 32 + 1])), sc, nl),
+                    pe);
+    if (kMasked) {
+      e.x = c < lim ? e.x : 0.f;
+      e.y = c + 1 < lim ? e.y : 0.f;
+    }
+    p[c] = e.x;
+    p[c + 1] = e.y;
+  }
+}
+
 // ------------------------------------------------------------------------------------ dkv
 // Persistent: one CTA per SM walks key-block items (hk, gj) longest-first. Per item the CTA
 // holds K / V (128 key rows) and streams every (q head, q block) that selected the block
@@ -287,8 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         float* vs = vec_smem + st * 2 * B;
         for (int r = lane; r < B; r += 32) {
           const bool ok = r < nq;
-          vs[r] = ok ? __ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
-          vs[B + r] = ok ? __ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+          vs[r] = ok ? -__ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+          vs[B + r] = ok ? -__ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->q_full[st]);
@@ -391,10 +434,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
 #pragma unroll
           for (int c2 = 0; c2 < B / 32; ++c2) tmem_ld32(tmem + lf + C::kSt + c2 * 32, sv[c2]);
           tmem_wait_ld();
-#pragma unroll
-          for (int r = 0; r < B; ++r) {
-            const float e = ex2_mixed(fmaf(__uint_as_float(sv[r / 32][r % 32]), scale_log2, -vs[r]), r);
-            p[r] = (r < nq && r >= r_lo) ? e : 0.f;
+          // vs[0..B) holds -lse2 of the item's query rows (producer negates).
+          if (r_lo == 0 && nq == B) {
+            dkv_p<B, false>(sv, vs, scale_log2, 0, B, p);
+          } else {
+            dkv_p<B, true>(sv, vs, scale_log2, r_lo, nq, p);
           }
         }
 #pragma unroll
@@ -418,8 +462,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             const int r = c2 * 32 + e;
-            dd[e / 2] = pack_bf16x2(p[r] * (__uint_as_float(pv[e]) - vs[B + r]),
-                                    p[r + 1] * (__uint_as_float(pv[e + 1]) - vs[B + r + 1]));
+            const float2 nd = *reinterpret_cast<const float2*>(vs + B + r);  // -D
+            const f2 ds = fmul2(mk2(p[r], p[r + 1]),
+                                fadd2(mk2(__uint_as_float(pv[e]), __uint_as_float(pv[e + 1])), mk2(nd.x, nd.y)));
+            dd[e / 2] = pack_bf16x2(ds.x, ds.y);
           }
           tmem_st16(tmem + lf + C::kDPt + c2 * 16, dd);
         }
@@ -740,10 +786,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
 #pragma unroll
           for (int c2 = 0; c2 < B / 32; ++c2) tmem_ld32(tmem + lf + s_col + c2 * 32, sv[c2]);
           tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < B; ++c) {
-            const float e = ex2_mixed(fmaf(__uint_as_float(sv[c / 32][c % 32]), scale_log2, -l2), c);
-            p[c] = c < lim ? e : 0.f;
+          if (__all_sync(0xffffffffu, lim == B)) {
+            dq_p<B, false>(sv, -l2, scale_log2, B, p);
+          } else {
+            dq_p<B, true>(sv, -l2, scale_log2, lim, p);
           }
         }
         mbar_wait(&bars->dp_full, g & 1);
@@ -757,7 +803,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             const int c = c2 * 32 + e;
-            dsp[e / 2] = pack_bf16x2(p[c] * (__uint_as_float(pv[e]) - dd), p[c + 1] * (__uint_as_float(pv[e + 1]) - dd));
+            const f2 ds = fmul2(mk2(p[c], p[c + 1]),
+                                fadd2(mk2(__uint_as_float(pv[e]), __uint_as_float(pv[e + 1])), mk2(-dd, -dd)));
+            dsp[e / 2] = pack_bf16x2(ds.x, ds.y);
           }
           tmem_st16(tmem + lf + s_col + c2 * 16, dsp);  // dS over S (already in registers)
         }

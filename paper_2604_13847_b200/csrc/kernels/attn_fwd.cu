@@ -76,6 +76,52 @@ __device__ __forceinline__ Item decode(int it, const int32_t* cu, const int32_t*
   return w;
 }
 
+// One key block of one query row (this thread's TMEM lane): row max (FMNMX3), lazy rescale
+// decision, P = 2^(S*scale_log2 - m) with packed FFMA2 / FADD2 and the SFU/FMA exp2 split,
+// packed bf16 P written back over the first B/2 columns of S. kMasked handles the diagonal
+// block (causal + sequence end: columns >= lim are masked).
+template <int B, bool kMasked>
+__device__ __forceinline__ void softmax_block(const uint32_t (&sv)[B / 32][32], int lim, float scale_log2,
+                                              float m_run, uint32_t t_s, float& m_use, float& alpha, float& sum,
+                                              bool& rescale) {
+  float xs[B];
+#pragma unroll
+  for (int c = 0; c < B; ++c) {
+    xs[c] = __uint_as_float(sv[c / 32][c % 32]);
+    if (kMasked) xs[c] = c < lim ? xs[c] : -INFINITY;
+  }
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < B; c += 4) {
+    m0 = fmax3(m0, xs[c], xs[c + 1]);
+    m1 = fmax3(m1, xs[c + 2], xs[c + 3]);
+  }
+  const float m_new = fmaxf(m_run, fmaxf(m0, m1) * scale_log2);
+  rescale = m_new > m_run + kRescaleThresh;
+  m_use = rescale ? m_new : m_run;
+  alpha = rescale ? ex2_sfu(m_run - m_use) : 1.0f;
+  const f2 sc = mk2(scale_log2, scale_log2), nm = mk2(-m_use, -m_use);
+  f2 acc0 = mk2(0.f, 0.f), acc1 = mk2(0.f, 0.f);
+#pragma unroll
+  for (int c2 = 0; c2 < B / 64; ++c2) {
+    uint32_t pw[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const int pe = c2 * 32 + e;  // column pair (2pe, 2pe+1)
+      f2 p = ex2_pair(ffma2(mk2(xs[2 * pe], xs[2 * pe + 1]), sc, nm), pe);
+      if (kMasked) {
+        p.x = 2 * pe < lim ? p.x : 0.f;
+        p.y = 2 * pe + 1 < lim ? p.y : 0.f;
+      }
+      if (e & 1) acc1 = fadd2(acc1, p); else acc0 = fadd2(acc0, p);
+      pw[e] = pack_bf16x2(p.x, p.y);
+    }
+    tmem_st32(t_s + c2 * 32, pw);  // P (packed bf16) over the first B/2 columns of S
+  }
+  const f2 acc = fadd2(acc0, acc1);
+  sum = acc.x + acc.y;
+}
+
 template <int D, int B>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -250,36 +296,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         // the diagonal block masks the causal upper triangle and keys past the sequence end.
         const bool diag = jb == w.i;
         const int lim = diag ? min(min(B, w.seq_len - jb * B), r + 1) : B;
-        float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < B; c += 2) {
-          const float a = __uint_as_float(sv[c / 32][c % 32]), b2 = __uint_as_float(sv[c / 32][c % 32 + 1]);
-          mx0 = fmaxf(mx0, (!diag || c < lim) ? a : -INFINITY);
-          mx1 = fmaxf(mx1, (!diag || c + 1 < lim) ? b2 : -INFINITY);
+        float m_use, alpha, sum;
+        bool rescale;
+        if (diag) {
+          softmax_block<B, true>(sv, lim, scale_log2, m_run, t_s, m_use, alpha, sum, rescale);
+        } else {
+          softmax_block<B, false>(sv, lim, scale_log2, m_run, t_s, m_use, alpha, sum, rescale);
         }
-        const float m_new = fmaxf(m_run, fmaxf(mx0, mx1) * scale_log2);
-        const bool rescale = m_new > m_run + kRescaleThresh;
-        const float m_use = rescale ? m_new : m_run;
-        const float alpha = rescale ? ex2_sfu(m_run - m_use) : 1.0f;
-        float sum0 = 0.f, sum1 = 0.f;
-#pragma unroll
-        for (int c = 0; c < B / 64; ++c) {
-          uint32_t pw[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int c0 = c * 64 + 2 * e;
-            float p0 = ex2_mixed(fmaf(__uint_as_float(sv[c0 / 32][c0 % 32]), scale_log2, -m_use), c0);
-            float p1 = ex2_mixed(fmaf(__uint_as_float(sv[c0 / 32][c0 % 32 + 1]), scale_log2, -m_use), c0 + 1);
-            if (diag) {
-              p0 = c0 < lim ? p0 : 0.f;
-              p1 = c0 + 1 < lim ? p1 : 0.f;
-            }
-            sum0 += p0;
-            sum1 += p1;
-            pw[e] = pack_bf16x2(p0, p1);
-          }
-          tmem_st32(t_s + c * 32, pw);  // P (packed bf16) over the first B/2 columns of S
-        }
+        const float sum0 = sum, sum1 = 0.f;
         l_run = l_run * alpha + (sum0 + sum1);
         tmem_wait_st();
         if (j > 0) {

@@ -1,12 +1,58 @@
-// exp2 for the softmax stages, split between the MUFU (SFU) pipe and the FMA pipe.
+// Elementwise math for the softmax stages, written for the sm_100 issue budget.
 //
-// On B200 the SFU retires 16 ex2/clk/SM, so exponentiating a 128x128 score tile costs exactly
-// as many cycles as the two 128x128x128 UMMAs it sits between. Evaluating a fraction of the
-// exponentials with a Cody-Waite + degree-3 polynomial on the FMA pipe (max relative error
-// 2.1e-4, far below the bf16 rounding of P) takes the SFU off the critical path.
+// The softmax warps are issue-bound (one warp per SM sub-partition streams 128 columns per
+// key block), so the hot loops use the packed fp32x2 FMA-pipe instructions (FFMA2 / FADD2 /
+// FMUL2), the 3-input FMNMX3 for row maxima, and split the exponentials between the SFU
+// (MUFU.EX2, 16/clk/SM on B200 -- exactly the UMMA time of a 128x128 tile) and a
+// Cody-Waite + degree-3 polynomial on the FMA pipe (max relative error 2.1e-4, far below the
+// bf16 rounding of P).
 #pragma once
 
+#include <stdint.h>
+
 namespace sbk {
+
+struct f2 {
+  float x, y;
+};
+
+__device__ __forceinline__ f2 mk2(float a, float b) { return f2{a, b}; }
+
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+  f2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+__device__ __forceinline__ f2 fmul2(f2 a, f2 b) {
+  f2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 
 __device__ __forceinline__ float ex2_sfu(float x) {
   float y;
@@ -14,24 +60,34 @@ __device__ __forceinline__ float ex2_sfu(float x) {
   return y;
 }
 
-// 2^x for x in [-125, 64]: x = j + f with j = rint(x) (via the 1.5*2^23 magic-number add) and
-// f in [-0.5, 0.5]; 2^f by a degree-3 polynomial; j folded into the exponent field with one
-// shift + add (the low mantissa bits of x + magic hold j in two's complement).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.0f);  // keeps the result a normal float (2^-125 ~ 0 for softmax)
-  const float magic = 12582912.0f;
-  const float t = x + magic;
-  const float f = x - (t - magic);
-  float p = fmaf(0.054848f, f, 0.24180661f);
-  p = fmaf(p, f, 0.6932482f);
-  p = fmaf(p, f, 0.99998866f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+// 2^x for a pair: x = j + f, j = rint(x) via the 1.5*2^23 magic-number add (the low mantissa
+// bits of x + magic hold j in two's complement), f in [-0.5, 0.5], 2^f by a degree-3
+// polynomial, j folded into the exponent field with one shift + add. x is clamped to >= -127
+// first so the exponent never wraps (2^-127 ~ 0 for softmax).
+__device__ __forceinline__ f2 ex2_poly2(f2 x) {
+  x.x = fmaxf(x.x, -127.0f);
+  x.y = fmaxf(x.y, -127.0f);
+  const f2 t = fadd2(x, mk2(12582912.0f, 12582912.0f));
+  const f2 jf = fadd2(t, mk2(-12582912.0f, -12582912.0f));
+  const f2 f = ffma2(jf, mk2(-1.0f, -1.0f), x);
+  f2 p = ffma2(mk2(0.054848f, 0.054848f), f, mk2(0.24180661f, 0.24180661f));
+  p = ffma2(p, f, mk2(0.6932482f, 0.6932482f));
+  p = ffma2(p, f, mk2(0.99998866f, 0.99998866f));
+  return mk2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+             __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-// Column-interleaved split: 3 of every 8 columns on the FMA pipe. `col` must be a
+// Pair e of a row (columns 2e, 2e+1): 3 of every 8 pairs on the FMA pipe. `e` must be a
 // compile-time constant after unrolling so the branch disappears.
+__device__ __forceinline__ f2 ex2_pair(f2 x, int e) {
+  if ((e & 7) >= 5) return ex2_poly2(x);
+  return mk2(ex2_sfu(x.x), ex2_sfu(x.y));
+}
+
+// Scalar variant used by the (rare) masked paths.
 __device__ __forceinline__ float ex2_mixed(float x, int col) {
-  return ((col & 7) >= 5) ? ex2_poly(x) : ex2_sfu(x);
+  if (((col >> 1) & 7) >= 5) return ex2_poly2(mk2(x, x)).x;
+  return ex2_sfu(x);
 }
 
 }  // namespace sbk
