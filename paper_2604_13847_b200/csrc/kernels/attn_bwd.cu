@@ -453,21 +453,27 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         mbar_arrive(&bars->pt_full);
         mbar_wait(&bars->dpt_full, g & 1);
         tc_fence_after();
-#pragma unroll
-        for (int c2 = 0; c2 < B / 32; ++c2) {
-          uint32_t pv[32];
-          tmem_ld32(tmem + lf + C::kDPt + c2 * 32, pv);
+        {
+          // dP^T chunks software-pipelined: chunk c2+1 is in flight while c2 is processed.
+          uint32_t pv[2][32];
+          tmem_ld32(tmem + lf + C::kDPt, pv[0]);
           tmem_wait_ld();
-          uint32_t dd[16];
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const int r = c2 * 32 + e;
-            const float2 nd = *reinterpret_cast<const float2*>(vs + B + r);  // -D
-            const f2 ds = fmul2(mk2(p[r], p[r + 1]),
-                                fadd2(mk2(__uint_as_float(pv[e]), __uint_as_float(pv[e + 1])), mk2(nd.x, nd.y)));
-            dd[e / 2] = pack_bf16x2(ds.x, ds.y);
+          for (int c2 = 0; c2 < B / 32; ++c2) {
+            if (c2 + 1 < B / 32) tmem_ld32(tmem + lf + C::kDPt + (c2 + 1) * 32, pv[(c2 + 1) & 1]);
+            uint32_t dd[16];
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const int r = c2 * 32 + e;
+              const float2 nd = *reinterpret_cast<const float2*>(vs + B + r);  // -D
+              const f2 ds = fmul2(mk2(p[r], p[r + 1]), fadd2(mk2(__uint_as_float(pv[c2 & 1][e]),
+                                                                  __uint_as_float(pv[c2 & 1][e + 1])),
+                                                              mk2(nd.x, nd.y)));
+              dd[e / 2] = pack_bf16x2(ds.x, ds.y);
+            }
+            tmem_st16(tmem + lf + C::kDPt + c2 * 16, dd);  // over columns already read
+            tmem_wait_ld();
           }
-          tmem_st16(tmem + lf + C::kDPt + c2 * 16, dd);
         }
         tmem_wait_st();
         tc_fence_before();
@@ -794,20 +800,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         }
         mbar_wait(&bars->dp_full, g & 1);
         tc_fence_after();
-#pragma unroll
-        for (int c2 = 0; c2 < B / 32; ++c2) {
-          uint32_t pv[32];
-          tmem_ld32(tmem + lf + C::kDP + c2 * 32, pv);
+        {
+          uint32_t pv[2][32];
+          tmem_ld32(tmem + lf + C::kDP, pv[0]);
           tmem_wait_ld();
-          uint32_t dsp[16];
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const int c = c2 * 32 + e;
-            const f2 ds = fmul2(mk2(p[c], p[c + 1]),
-                                fadd2(mk2(__uint_as_float(pv[e]), __uint_as_float(pv[e + 1])), mk2(-dd, -dd)));
-            dsp[e / 2] = pack_bf16x2(ds.x, ds.y);
+          for (int c2 = 0; c2 < B / 32; ++c2) {
+            if (c2 + 1 < B / 32) tmem_ld32(tmem + lf + C::kDP + (c2 + 1) * 32, pv[(c2 + 1) & 1]);
+            uint32_t dsp[16];
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const int c = c2 * 32 + e;
+              const f2 ds = fmul2(mk2(p[c], p[c + 1]), fadd2(mk2(__uint_as_float(pv[c2 & 1][e]),
+                                                                  __uint_as_float(pv[c2 & 1][e + 1])),
+                                                              mk2(-dd, -dd)));
+              dsp[e / 2] = pack_bf16x2(ds.x, ds.y);
+            }
+            tmem_st16(tmem + lf + s_col + c2 * 16, dsp);  // dS over S (already in registers)
+            tmem_wait_ld();
           }
-          tmem_st16(tmem + lf + s_col + c2 * 16, dsp);  // dS over S (already in registers)
         }
         tmem_wait_st();
         tc_fence_before();

@@ -90,18 +90,20 @@ __device__ __forceinline__ void softmax_block(const uint32_t (&sv)[B / 32][32], 
     xs[c] = __uint_as_float(sv[c / 32][c % 32]);
     if (kMasked) xs[c] = c < lim ? xs[c] : -INFINITY;
   }
-  float m0 = -INFINITY, m1 = -INFINITY;
+  float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
-  for (int c = 0; c < B; c += 4) {
+  for (int c = 0; c < B; c += 8) {
     m0 = fmax3(m0, xs[c], xs[c + 1]);
     m1 = fmax3(m1, xs[c + 2], xs[c + 3]);
+    m2 = fmax3(m2, xs[c + 4], xs[c + 5]);
+    m3 = fmax3(m3, xs[c + 6], xs[c + 7]);
   }
-  const float m_new = fmaxf(m_run, fmaxf(m0, m1) * scale_log2);
+  const float m_new = fmaxf(m_run, fmax3(m0, m1, fmaxf(m2, m3)) * scale_log2);
   rescale = m_new > m_run + kRescaleThresh;
   m_use = rescale ? m_new : m_run;
   alpha = rescale ? ex2_sfu(m_run - m_use) : 1.0f;
   const f2 sc = mk2(scale_log2, scale_log2), nm = mk2(-m_use, -m_use);
-  f2 acc0 = mk2(0.f, 0.f), acc1 = mk2(0.f, 0.f);
+  f2 acc[4] = {mk2(0.f, 0.f), mk2(0.f, 0.f), mk2(0.f, 0.f), mk2(0.f, 0.f)};
 #pragma unroll
   for (int c2 = 0; c2 < B / 64; ++c2) {
     uint32_t pw[32];
@@ -113,13 +115,13 @@ __device__ __forceinline__ void softmax_block(const uint32_t (&sv)[B / 32][32], 
         p.x = 2 * pe < lim ? p.x : 0.f;
         p.y = 2 * pe + 1 < lim ? p.y : 0.f;
       }
-      if (e & 1) acc1 = fadd2(acc1, p); else acc0 = fadd2(acc0, p);
+      acc[e & 3] = fadd2(acc[e & 3], p);
       pw[e] = pack_bf16x2(p.x, p.y);
     }
     tmem_st32(t_s + c2 * 32, pw);  // P (packed bf16) over the first B/2 columns of S
   }
-  const f2 acc = fadd2(acc0, acc1);
-  sum = acc.x + acc.y;
+  const f2 a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+  sum = a01.x + a01.y;
 }
 
 template <int D, int B>
