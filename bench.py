@@ -57,29 +57,24 @@ def workload(rank: int):
 
 
 def useful_flops(cu, B, idx, cnt, d):
-    """(fwd, bwd) useful FLOPs: 4*d*sum(e_ij) and 10*d*sum(e_ij) over q heads."""
-    cu = np.asarray(cu)
+    """(fwd, bwd) useful FLOPs: 4*d*sum(e_ij) and 10*d*sum(e_ij) over q heads, where e_ij is the
+    number of unmasked score entries of pair (i, j): r_i * c_j off the diagonal and
+    r_i (r_i + 1) / 2 on the causal diagonal."""
+    cu = np.asarray(cu, np.int64)
     nb = (np.diff(cu) + B - 1) // B
     blk = np.concatenate([[0], np.cumsum(nb)])
-    rows = np.zeros(int(blk[-1]), np.int64)  # valid rows per block (global block index)
-    local = np.zeros(int(blk[-1]), np.int64)
-    for s in range(len(nb)):
-        L = cu[s + 1] - cu[s]
-        for i in range(nb[s]):
-            rows[blk[s] + i] = min(B, L - i * B)
-            local[blk[s] + i] = i
     seq_of = np.repeat(np.arange(len(nb)), nb)
-    e = 0
-    hsel = idx.shape[0]
-    for g in range(hsel):
-        n = cnt[g]
-        for gi in range(idx.shape[1]):
-            sel = idx[g, gi, :n[gi]]
-            r = rows[gi]
-            kv_rows = rows[blk[seq_of[gi]] + sel]
-            diag = sel == local[gi]
-            e += int(np.sum(np.where(diag, r * (r + 1) // 2, r * kv_rows)))
-    return 4.0 * d * e, 10.0 * d * e
+    local = np.arange(int(blk[-1])) - blk[seq_of]
+    lens = np.diff(cu)[seq_of]
+    rows = np.minimum(B, lens - local * B)
+    k_max = idx.shape[2]
+    valid = np.arange(k_max)[None, None, :] < cnt[:, :, None]
+    sel = np.where(valid, idx, 0).astype(np.int64)
+    kv_rows = rows[blk[seq_of][None, :, None] + sel]
+    r = rows[None, :, None]
+    diag = sel == local[None, :, None]
+    e = np.where(valid, np.where(diag, r * (r + 1) // 2, r * kv_rows), 0).sum(dtype=np.int64)
+    return 4.0 * d * float(e), 10.0 * d * float(e)
 
 
 class ClockSampler:
@@ -139,7 +134,17 @@ def run_reference_arm(args, rank, world):
         return
     from oracle import device as orc
 
-    cu, k_seq = workload(0)
+    if world > 1 or args.workload == "c3":
+        from paper_2604_13847_b200 import dp
+        from paper_2604_13847_b200.host import api
+
+        lengths_all = c3_global_batch(world, CFG["seed"])
+        bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=api().synthesize_table(block_size=CFG["block"]))
+        mine = [int(lengths_all[i]) for i in bins[0][0]]
+        cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
+        k_seq = np.maximum(1, (np.diff(cu) + CFG["block"] - 1) // CFG["block"] // 8).astype(np.int32)
+    else:
+        cu, k_seq = workload(0)
     T, D, B = int(cu[-1]), CFG["head_dim"], CFG["block"]
     rng = np.random.default_rng(1)
 
@@ -167,7 +172,8 @@ def run_reference_arm(args, rank, world):
             times.append(dt)
     ms = 1e3 * statistics.mean(times)
     value = flops / (ms * 1e-3) / 1e12
-    sample = f"q head 0 of 32 of rank 0's 32K-token micro-batch ({len(cu) - 1} seqs), fwd+bwd + scorer/selector"
+    sample = (f"q head 0 of 32, one layer, of rank 0's {T}-token micro-batch ({len(cu) - 1} seqs): "
+              "scorer, profile, selector, fwd, bwd")
     line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
@@ -178,12 +184,47 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+class Marker:
+    """Records CUDA events at tagged phase boundaries inside a step (on the launching stream)."""
+
+    def __init__(self, torch, stream):
+        self.torch, self.stream = torch, stream
+        self.marks = []
+
+    def __call__(self, tag):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        self.marks.append((tag, e))
+
+    def durations(self):
+        """ms per tag: time from the previous mark to this one, summed per tag."""
+        out = {}
+        for (_, a), (tag, b) in zip(self.marks, self.marks[1:]):
+            out[tag] = out.get(tag, 0.0) + a.elapsed_time(b)
+        return out
+
+
+def c3_global_batch(world: int, seed: int):
+    """C3: the reference workload generator's 40% 32K / 60% 2K bimodal mix
+    (distribution={bimodal, short_weight 0.6, ln 2048 / ln 32768, sigma 0}), gbs = 5 * dp."""
+    from paper_2604_13847_b200.host import api
+
+    dist_spec = dict(short_weight=0.6, short_log_mean=float(np.log(2048)), short_log_sigma=0.0,
+                     long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
+    lengths, _ = api().generate_samples(5 * world, 1, CFG["block"], seed=seed, dist=dist_spec)
+    return np.asarray(lengths)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, choices=["c2", "c3"],
+                    help="c2 (default at 1 GPU): 32K packed, per-sequence keeps; c3 (default at >1 GPU): 40/60 "
+                         "32K/2K global batch, SAB plan + per-layer DST across ranks")
+    ap.add_argument("--layers", type=int, default=36, help="c3: layers per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="2 plain steps then exit (for ncu)")
     args = ap.parse_args()
@@ -192,66 +233,93 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    workload_kind = args.workload or ("c2" if world == 1 else "c3")
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
 
     import torch
     import torch.distributed as dist
 
-    from paper_2604_13847_b200 import ops
+    from paper_2604_13847_b200 import dp, ops
+    from paper_2604_13847_b200.host import api
 
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
     H, D, B = CFG["heads"], CFG["head_dim"], CFG["block"]
-    cu, k_seq = workload(rank)
+    stream = torch.cuda.current_stream()
+
+    if workload_kind == "c2":
+        cu, k_seq = workload(rank)
+        config = {"workload": "C2: 32K-token packed varlen micro-batch per rank ([12288, 8192, 4096, 2048x4], SURVEY "
+                              "8d), 32 heads MHA, d128, B128, per-sequence keep U[0.05,0.5], "
+                              "scorer+profile+selector+fwd+bwd", "seqs_rank0": int(len(cu) - 1)}
+    else:
+        lengths_all = c3_global_batch(world, CFG["seed"])
+        table = api().synthesize_table(block_size=B)
+        bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=table)
+        mine = [int(lengths_all[i]) for i in bins[rank][0]]
+        cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
+        k_seq = None
+        config = {"workload": f"C3: 40% 32K / 60% 2K global batch (reference generator, seed 42, gbs={5 * world}), "
+                              f"SAB plan mbs=5 (one packed micro-batch per rank), {args.layers} layers, per-layer DST "
+                              "(Mean anchor, p=0.1, global scope, coverage base) from GPU-measured profiles, 32 heads "
+                              "MHA, d128, B128, scorer+profile+allgather+DST+selector+fwd+bwd",
+                  "tokens_per_rank": [int(x) for x in np.array([sum(int(lengths_all[i]) for i in b[0]) for b in bins])]}
     T = int(cu[-1])
     lay = ops.VarlenLayout.build(cu, B, device=dev)
     g = torch.Generator(device=dev).manual_seed(CFG["seed"] + rank)
     q, k, v, do = (torch.randn((T, H, D), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
-    kseq_d = torch.from_numpy(k_seq).to(dev)
-    k_max = int(k_seq.max())
-    grid = torch.tensor([1, 2, 3, 4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 56, 64], dtype=torch.int32, device=dev)
     scale = 1.0 / math.sqrt(D)
-    est = torch.zeros(3 * max(1, world), dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream()
 
-    def step(ev=None):
-        if ev:
-            ev[0].record(stream)
-        S = ops.block_scores(q, k, lay, scale)
-        prof = ops.coverage_profile(S, lay)
-        ops.coverage_at_grid(prof, lay, grid)
-        idx, cnt = ops.topk_select(S, lay, kseq_d, k_max)
-        if ev:
-            ev[1].record(stream)
-        o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
-        if ev:
-            ev[2].record(stream)
-        dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
-        if ev:
-            ev[3].record(stream)
-        if world > 1:  # workload-estimate allgather for the tuner (x, k_base, T_base)
-            mine = torch.tensor([float(T), float(k_max), 0.0], dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(est, mine)
-        return idx, cnt, o, dq, dk, dv
+    if workload_kind == "c2":
+        kseq_d = torch.from_numpy(k_seq).to(dev)
+        k_max = int(k_seq.max())
+        grid = torch.tensor([1, 2, 3, 4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 56, 64], dtype=torch.int32,
+                            device=dev)
 
-    idx, cnt, *_ = step()
+        def step(mark=None):
+            S = ops.block_scores(q, k, lay, scale)
+            prof = ops.coverage_profile(S, lay)
+            ops.coverage_at_grid(prof, lay, grid)
+            idx, cnt = ops.topk_select(S, lay, kseq_d, k_max)
+            if mark:
+                mark("decided")
+            o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+            if mark:
+                mark("fwd")
+            dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+            if mark:
+                mark("bwd")
+            return [(idx, cnt, o, (dq, dk, dv))]
+    else:
+        rng = np.random.default_rng(CFG["seed"])
+        layer_scales = np.exp(rng.uniform(-0.5, 1.0, size=args.layers))  # per-layer softmax temperature
+        runner = dp.DPStep(dp.RankBatch(np.diff(cu), list(bins[rank][0]), lay), q, k, v, do, layer_scales, table,
+                           dp.DstSettings(), rank=rank, world=world, width=int(np.ceil(32768 / B)))
+
+        def step(mark=None):
+            return runner.run(backward=True, mark=mark)
+
+    outs = step()
     torch.cuda.synchronize()
+    f_fwd = f_bwd = 0.0
+    for idx, cnt, *_ in outs:
+        a, b_ = useful_flops(cu, B, idx.cpu().numpy(), cnt.cpu().numpy(), D)
+        f_fwd, f_bwd = f_fwd + a, f_bwd + b_
+    f_step = f_fwd + f_bwd
     if args.profile_only:
         step()
         torch.cuda.synchronize()
         print("profile-only: 2 steps done")
         return
-    f_fwd, f_bwd = useful_flops(cu, B, idx.cpu().numpy(), cnt.cpu().numpy(), D)
-    f_step = f_fwd + f_bwd
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
-    # ---- device-timed region: inputs resident in HBM
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    # ---- device-timed region: inputs resident in HBM (each >= 256 MB, larger than L2)
+    markers = [Marker(torch, stream) for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -260,23 +328,25 @@ def main():
     with ClockSampler(local_rank) as clk:
         time.sleep(0.3)  # let nvidia-smi start sampling
         t0.record(stream)
-        for s in range(args.steps):
-            step(evs[s])
+        for s_ in range(args.steps):
+            markers[s_]("start")
+            step(markers[s_])
         t1.record(stream)
         torch.cuda.synchronize()
         launches = ops.launch_count() - launches0
         # Keep the GPU under the same load (untimed) so the sampler sees >= ~1 s of it.
         t_load = time.perf_counter()
         while time.perf_counter() - t_load < 1.2:
-            for _ in range(args.steps):
-                step()
+            step()
             torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1) / args.steps
-    sel_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-    fwd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
-    bwd_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    phase = {}
+    for m in markers:
+        for k_, v_ in m.durations().items():
+            phase[k_] = phase.get(k_, 0.0) + v_ / args.steps
+    sel_ms, fwd_ms, bwd_ms = phase.get("decided", 0.0), phase.get("fwd", 0.0), phase.get("bwd", 0.0)
 
     # ---- end-to-end region: host (pinned) inputs in, results out, every step
     hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, do))
@@ -292,7 +362,8 @@ def main():
         k.copy_(hk, non_blocking=True)
         v.copy_(hv, non_blocking=True)
         do.copy_(hdo, non_blocking=True)
-        _, _, o, dq, dk, dv = step()
+        res = step()
+        _, _, o, (dq, dk, dv) = res[-1]
         ho.copy_(o, non_blocking=True)
         hdq.copy_(dq, non_blocking=True)
         hdk.copy_(dk, non_blocking=True)
@@ -304,22 +375,22 @@ def main():
     nbytes = 4 * T * H * D * 2
 
     # ---- max over ranks, whole-job aggregates
-    vals = torch.tensor([ms, e2e_ms, f_step, fwd_ms, bwd_ms, sel_ms], dtype=torch.float64, device=dev)
+    vals = torch.tensor([ms, e2e_ms, f_step], dtype=torch.float64, device=dev)
     if world > 1:
         mx = vals.clone()
-        dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         tot = vals.clone()
-        dist.all_reduce(tot[2:3], op=dist.ReduceOp.SUM)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         ms_max, e2e_max, flops_all = float(mx[0]), float(mx[1]), float(tot[2])
-        per_rank_ms = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(world)]
-        dist.all_gather(per_rank_ms, vals[0:1])
-        per_rank_ms = [float(x) for x in per_rank_ms]
+        per_rank = [torch.zeros(3, dtype=torch.float64, device=dev) for _ in range(world)]
+        dist.all_gather(per_rank, vals)
+        per_rank_ms = [float(x[0]) for x in per_rank]
+        per_rank_tflop = [float(x[2]) / 1e12 for x in per_rank]
     else:
-        ms_max, e2e_max, flops_all, per_rank_ms = ms, e2e_ms, f_step, [ms]
+        ms_max, e2e_max, flops_all, per_rank_ms, per_rank_tflop = ms, e2e_ms, f_step, [ms], [f_step / 1e12]
 
     if rank == 0:
         bf16_peak, hbm_peak, peak_kind = peaks()
-        # Dominant kernel: whichever of fwd / bwd takes longer inside the step.
         if bwd_ms >= fwd_ms:
             dom, dom_ms, dom_flops = "sb_sparse_attn_bwd (dkv+dq passes)", bwd_ms, f_bwd
         else:
@@ -329,31 +400,31 @@ def main():
         prof_path = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
         if os.path.exists(prof_path):
             try:
-                traffic = json.load(open(prof_path)).get("dominant_traffic_bytes")
+                traffic = json.load(open(prof_path)).get(workload_kind, {}).get("dominant_traffic_bytes")
             except Exception:
                 traffic = None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(cu, k_seq)
+            cpu = cpu_baseline(cu, k_seq if k_seq is not None else np.maximum(1, (np.diff(cu) + B - 1) // B // 8))
         value = flops_all / (ms_max * 1e-3) / 1e12
+        config.update({"tokens_per_rank" if workload_kind == "c2" else "tokens_rank0": T,
+                       "l2": "inputs 256 MB+ each > L2, no flush", "parallelism": f"dp{world}"})
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C2: 32K-token packed varlen micro-batch per rank ([12288, 8192, 4096, 2048x4], "
-                                   "SURVEY 8d), 32 heads MHA, d128, B128, per-sequence keep "
-                                   "U[0.05,0.5], scorer+profile+selector+fwd+bwd",
-                       "seqs_rank0": int(len(cu) - 1), "tokens_per_rank": T, "l2": "inputs 256 MB each > L2, no flush",
-                       "parallelism": f"dp{world}"},
-            "breakdown_ms": {"scorer_profile_selector": sel_ms, "fwd": fwd_ms, "bwd": bwd_ms},
-            "per_rank_ms": per_rank_ms, "max_over_mean": ms_max / statistics.mean(per_rank_ms),
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": config,
+            "breakdown_ms_rank0": {"scorer_profile_exchange_dst_selector": sel_ms, "fwd": fwd_ms, "bwd": bwd_ms},
+            "per_rank_ms": per_rank_ms, "per_rank_useful_tflop": per_rank_tflop,
+            "max_over_mean": ms_max / statistics.mean(per_rank_ms),
             "useful_tflop_per_step": flops_all / 1e12,
-            "fwd_tflops": f_fwd / (fwd_ms * 1e-3) / 1e12, "bwd_tflops": f_bwd / (bwd_ms * 1e-3) / 1e12,
+            "fwd_tflops_rank0": f_fwd / (fwd_ms * 1e-3) / 1e12 if fwd_ms else None,
+            "bwd_tflops_rank0": f_bwd / (bwd_ms * 1e-3) / 1e12 if bwd_ms else None,
             "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16_peak,
                          "unit": "TFLOP/s", "frac": achieved / bf16_peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} bf16 dense (burst)"},
             "e2e": {"value": flops_all / (e2e_max * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_max,
-                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
+                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                    "note": "pinned H2D of Q,K,V,dO + D2H of O,dQ,dK,dV (last layer) every step"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -1,0 +1,212 @@
+"""Data-parallel SparseBalance step driver: one process per GPU, NCCL for the plumbing.
+
+Re-hosts the reference step driver's decision path (proj/core/src/sim.cpp:277-432) on real
+kernels. Per optimizer step:
+
+  1. SAB plan (host, deterministic on every rank, no collective): the global batch's lengths ->
+     rank -> micro-batch assignment (plan_batching / plan_lbb / plan_sequential, sab.cpp:224-310).
+  2. Per rank, per layer: block scorer (K1+K2) + coverage profile (K4) on this rank's packed
+     micro-batch -> one RoutingProfile per (sequence, layer), copied to the host.
+  3. ONE all-gather of every rank's workload estimate: its micro-batch length descriptor and
+     its per-layer member profiles (a few KB). Concatenating rank-major reproduces the
+     reference's pooled order (sim.cpp:357-369).
+  4. Every rank runs the identical host DST over the pooled micro-batches (make_micro_batch
+     merge, coverage-mode intrinsic_budget, tune_global_batch per layer): bit-identical
+     k_final on all ranks with no broadcast.
+  5. Per layer: top-k selection with k_final clamped per sequence, sparse attention fwd + bwd.
+
+There is no KV or sequence exchange between ranks (no CP / ring / Ulysses): the only
+collectives are the step-3 all-gather and the caller's gradient all-reduce.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Sequence
+
+import numpy as np
+import torch
+
+from . import ops
+from .host import DEFAULT_BUDGET_GRID, ProfileTable, api
+
+
+@dataclass
+class DstSettings:
+    threshold_p: float = 0.1
+    anchor: str = "mean"           # paper default; the reference defaults to min
+    base_mode: str = "coverage"    # or "fixed"
+    base_budget: int = 32          # fixed mode
+    coverage_target: float = 0.9
+    budget_grid: Sequence[int] = field(default_factory=lambda: list(DEFAULT_BUDGET_GRID))
+
+
+@dataclass
+class RankBatch:
+    """This rank's packed micro-batch (one micro-batch per rank per step)."""
+
+    lengths: np.ndarray      # member sequence lengths
+    sample_ids: List[int]
+    layout: ops.VarlenLayout
+
+    @property
+    def length_descriptor(self) -> int:
+        return int(self.lengths.sum())
+
+
+def assign_rank_batches(global_lengths: Sequence[int], dp: int, mbs: int, strategy: str = "lbb", est=None,
+                        table: ProfileTable | None = None):
+    """SAB / LBB / sequential plan of the global batch (reference plan_batching / plan_lbb /
+    plan_sequential, sab.cpp:224-310) -> per rank the list of micro-batches (sample ids)."""
+    h = api()
+    n = len(global_lengths)
+    bins, _ = h.plan_batching(strategy, np.arange(n), np.asarray(global_lengths), n, mbs, dp, est, table)
+    return bins
+
+
+def profiles_to_host(prof: torch.Tensor, lay: ops.VarlenLayout) -> List[np.ndarray]:
+    """[nseq, nb_max] fp64 device profiles -> per-sequence numpy vectors of nb_s entries."""
+    p = prof.cpu().numpy()
+    return [p[s, :nb].copy() for s, nb in enumerate(lay.nb_per_seq)]
+
+
+def pack_estimate(lengths: np.ndarray, layer_profiles: List[List[np.ndarray]], width: int) -> torch.Tensor:
+    """Flatten one rank's workload estimate into a fixed-size fp64 vector for the all-gather:
+    [nseq, lengths..., then for every layer and member the nb entries zero-padded to width]."""
+    L = len(layer_profiles)
+    nseq = len(lengths)
+    out = np.zeros(1 + nseq + L * nseq * width, np.float64)
+    out[0] = nseq
+    out[1:1 + nseq] = lengths
+    pos = 1 + nseq
+    for l in range(L):
+        for s in range(nseq):
+            v = layer_profiles[l][s]
+            out[pos:pos + len(v)] = v
+            pos += width
+    return torch.from_numpy(out)
+
+
+def unpack_estimate(vec: np.ndarray, num_layers: int, width: int, block: int):
+    nseq = int(vec[0])
+    lengths = vec[1:1 + nseq].astype(np.int64)
+    pos = 1 + nseq
+    prof = []  # [seq][layer]
+    nbs = (lengths + block - 1) // block
+    per_layer = []
+    for l in range(num_layers):
+        row = []
+        for s in range(nseq):
+            row.append(vec[pos:pos + nbs[s]].copy())
+            pos += width
+        per_layer.append(row)
+    for s in range(nseq):
+        prof.append([per_layer[l][s] for l in range(num_layers)])
+    return lengths, prof
+
+
+def decide_budgets(pooled, table: ProfileTable, cfg: DstSettings, num_layers: int):
+    """Host DST over the pooled micro-batches (rank-major): returns k_final[rank][layer] and the
+    decisions. pooled = list over ranks of (lengths, per-member per-layer profiles)."""
+    h = api()
+    grid = np.asarray(cfg.budget_grid, np.int32)
+    xs, merged, k_base = [], [], []
+    for lengths, prof in pooled:
+        ld, mp = h.make_micro_batch(lengths, prof)  # reference make_micro_batch merge (workload.cpp:64-99)
+        xs.append(ld)
+        merged.append(mp)
+        if cfg.base_mode == "coverage":
+            k_base.append(h.intrinsic_budget(mp, grid, cfg.coverage_target))
+        else:
+            k_base.append(cfg.base_budget)
+    k_final = np.zeros((len(pooled), num_layers), np.int32)
+    decisions = []
+    for l in range(num_layers):
+        ds = h.tune_global_batch(table, xs, k_base, [m[l] for m in merged], layer=l, threshold_p=cfg.threshold_p,
+                                 anchor=cfg.anchor, budget_grid=grid)
+        for d in ds:
+            k_final[d.micro_batch_id, l] = d.k_final
+        decisions.extend(ds)
+    return k_final, decisions, np.asarray(k_base), np.asarray(xs)
+
+
+class DPStep:
+    """One rank's hot-path step over its micro-batch for `num_layers` layers.
+
+    Layers share the synthetic Q/K/V/dO tensors but each layer uses its own softmax
+    temperature (scale_l / sqrt(d)), so per-layer routing profiles -- and the tuner's per-layer
+    budgets -- differ as they do across real layers."""
+
+    def __init__(self, batch: RankBatch, q, k, v, do, layer_scales, table: ProfileTable, cfg: DstSettings,
+                 rank: int = 0, world: int = 1, group=None, width: int | None = None):
+        self.batch, self.q, self.k, self.v, self.do = batch, q, k, v, do
+        self.layer_scales = list(layer_scales)
+        self.table, self.cfg = table, cfg
+        self.rank, self.world, self.group = rank, world, group
+        self.d = q.shape[2]
+        self.block = batch.layout.block_size
+        self.width = width if width is not None else int(batch.layout.nb_max)
+        self.last = {}
+
+    def scorer_pass(self):
+        """K1 + K2 + K4 for every layer (the scorer pre-pass coverage-mode budgets need)."""
+        lay = self.batch.layout
+        qbar, kbar = ops.block_pool(self.q, lay), ops.block_pool(self.k, lay)
+        profs, scores = [], []
+        for s_l in self.layer_scales:
+            S = ops.block_scores(self.q, self.k, lay, s_l / math.sqrt(self.d), qbar=qbar, kbar=kbar)
+            scores.append(S)
+            profs.append(ops.coverage_profile(S, lay))
+        return qbar, kbar, profs, scores
+
+    def exchange(self, profs):
+        lay = self.batch.layout
+        layer_profiles = [profiles_to_host(p, lay) for p in profs]
+        return exchange_estimates(self.batch.lengths, layer_profiles, self.width, self.block, self.world, self.group,
+                                  self.q.device)
+
+    def run(self, backward: bool = True, mark=None):
+        """mark(tag) (optional) is called at phase boundaries: 'decided' after the scorer
+        pre-pass + exchange + DST, then 'fwd' / 'bwd' after each layer's kernels."""
+        lay = self.batch.layout
+        qbar, kbar, profs, scores = self.scorer_pass()
+        pooled = self.exchange(profs)
+        k_final, decisions, k_base, xs = decide_budgets(pooled, self.table, self.cfg, len(self.layer_scales))
+        self.last = dict(k_final=k_final, decisions=decisions, k_base=k_base, xs=xs)
+        if mark:
+            mark("decided")
+        nb = lay.nb_per_seq
+        outs = []
+        for l, s_l in enumerate(self.layer_scales):
+            k_seq = np.minimum(int(k_final[self.rank, l]), nb).astype(np.int32)
+            k_max = int(max(1, k_seq.max()))
+            scale = s_l / math.sqrt(self.d)
+            idx, cnt = ops.topk_select(scores[l], lay, torch.from_numpy(k_seq).to(self.q.device), k_max)
+            o, lse = ops.sparse_attn_fwd(self.q, self.k, self.v, lay, idx, cnt, scale)
+            if mark:
+                mark("fwd")
+            grads = ops.sparse_attn_bwd(self.q, self.k, self.v, o, self.do, lse, lay, idx, cnt, scale) if backward else None
+            if mark:
+                mark("bwd")
+            outs.append((idx, cnt, o, grads))
+        return outs
+
+
+def exchange_estimates(lengths, layer_profiles, width: int, block: int, world: int, group=None, device="cpu"):
+    """All-gather every rank's workload estimate (micro-batch member lengths + per-layer member
+    profiles, a few KB) -> the pooled list, rank-major. NCCL on GPU tensors; gloo on CPU."""
+    import torch.distributed as dist
+
+    num_layers = len(layer_profiles)
+    mine = pack_estimate(np.asarray(lengths), layer_profiles, width)
+    if world == 1:
+        return [unpack_estimate(mine.numpy(), num_layers, width, block)]
+    size = torch.tensor([mine.numel()], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(size) for _ in range(world)]
+    dist.all_gather(sizes, size, group=group)
+    n = int(max(int(x) for x in sizes))
+    buf = torch.zeros(n, dtype=torch.float64, device=device)
+    buf[:mine.numel()] = mine.to(device)
+    outs = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf, group=group)
+    return [unpack_estimate(o.cpu().numpy(), num_layers, width, block) for o in outs]
