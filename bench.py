@@ -138,7 +138,7 @@ def run_reference_arm(args, rank, world):
         from paper_2604_13847_b200 import dp
         from paper_2604_13847_b200.host import api
 
-        lengths_all = c3_global_batch(world, CFG["seed"])
+        lengths_all, _ = c3_global_batch(world, CFG["seed"], args.layers)
         bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=api().synthesize_table(block_size=CFG["block"]))
         mine = [int(lengths_all[i]) for i in bins[0][0]]
         cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
@@ -204,15 +204,16 @@ class Marker:
         return out
 
 
-def c3_global_batch(world: int, seed: int):
+def c3_global_batch(world: int, seed: int, layers: int = 1):
     """C3: the reference workload generator's 40% 32K / 60% 2K bimodal mix
-    (distribution={bimodal, short_weight 0.6, ln 2048 / ln 32768, sigma 0}), gbs = 5 * dp."""
+    (distribution={bimodal, short_weight 0.6, ln 2048 / ln 32768, sigma 0}, default
+    concentration), gbs = 5 * dp -> (lengths, per-sample per-layer routing profiles)."""
     from paper_2604_13847_b200.host import api
 
     dist_spec = dict(short_weight=0.6, short_log_mean=float(np.log(2048)), short_log_sigma=0.0,
                      long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
-    lengths, _ = api().generate_samples(5 * world, 1, CFG["block"], seed=seed, dist=dist_spec)
-    return np.asarray(lengths)
+    lengths, profiles = api().generate_samples(5 * world, layers, CFG["block"], seed=seed, dist=dist_spec)
+    return np.asarray(lengths), profiles
 
 
 def main():
@@ -256,7 +257,7 @@ def main():
                               "8d), 32 heads MHA, d128, B128, per-sequence keep U[0.05,0.5], "
                               "scorer+profile+selector+fwd+bwd", "seqs_rank0": int(len(cu) - 1)}
     else:
-        lengths_all = c3_global_batch(world, CFG["seed"])
+        lengths_all, profiles_all = c3_global_batch(world, CFG["seed"], args.layers)
         table = api().synthesize_table(block_size=B)
         bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=table)
         mine = [int(lengths_all[i]) for i in bins[rank][0]]
@@ -264,8 +265,9 @@ def main():
         k_seq = None
         config = {"workload": f"C3: 40% 32K / 60% 2K global batch (reference generator, seed 42, gbs={5 * world}), "
                               f"SAB plan mbs=5 (one packed micro-batch per rank), {args.layers} layers, per-layer DST "
-                              "(Mean anchor, p=0.1, global scope, coverage base) from GPU-measured profiles, 32 heads "
-                              "MHA, d128, B128, scorer+profile+allgather+DST+selector+fwd+bwd",
+                              "(Mean anchor, p=0.1, global scope, coverage base) on the generator's routing profiles "
+                              "(all-gathered), GPU block scores for selection, 32 heads MHA, d128, B128, "
+                              "scorer+allgather+DST+selector+fwd+bwd",
                   "tokens_per_rank": [int(x) for x in np.array([sum(int(lengths_all[i]) for i in b[0]) for b in bins])]}
     T = int(cu[-1])
     lay = ops.VarlenLayout.build(cu, B, device=dev)
@@ -296,8 +298,10 @@ def main():
     else:
         rng = np.random.default_rng(CFG["seed"])
         layer_scales = np.exp(rng.uniform(-0.5, 1.0, size=args.layers))  # per-layer softmax temperature
+        routing = [[profiles_all[i][l] for i in bins[rank][0]] for l in range(args.layers)]
         runner = dp.DPStep(dp.RankBatch(np.diff(cu), list(bins[rank][0]), lay), q, k, v, do, layer_scales, table,
-                           dp.DstSettings(), rank=rank, world=world, width=int(np.ceil(32768 / B)))
+                           dp.DstSettings(), rank=rank, world=world, width=int(np.ceil(32768 / B)),
+                           routing_profiles=routing)
 
         def step(mark=None):
             return runner.run(backward=True, mark=mark)

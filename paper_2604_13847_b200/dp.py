@@ -138,7 +138,11 @@ class DPStep:
     budgets -- differ as they do across real layers."""
 
     def __init__(self, batch: RankBatch, q, k, v, do, layer_scales, table: ProfileTable, cfg: DstSettings,
-                 rank: int = 0, world: int = 1, group=None, width: int | None = None):
+                 rank: int = 0, world: int = 1, group=None, width: int | None = None, routing_profiles=None):
+        """routing_profiles (optional): per-layer, per-member RoutingProfiles to feed the tuner
+        instead of the GPU coverage profiles -- e.g. the reference workload generator's own
+        routing scores for these samples (workload.cpp:239-271), which carry the reference's
+        sparsity structure; synthetic N(0,1) activations give near-uniform block scores."""
         self.batch, self.q, self.k, self.v, self.do = batch, q, k, v, do
         self.layer_scales = list(layer_scales)
         self.table, self.cfg = table, cfg
@@ -146,6 +150,7 @@ class DPStep:
         self.d = q.shape[2]
         self.block = batch.layout.block_size
         self.width = width if width is not None else int(batch.layout.nb_max)
+        self.routing_profiles = routing_profiles
         self.last = {}
 
     def scorer_pass(self):
@@ -156,12 +161,16 @@ class DPStep:
         for s_l in self.layer_scales:
             S = ops.block_scores(self.q, self.k, lay, s_l / math.sqrt(self.d), qbar=qbar, kbar=kbar)
             scores.append(S)
-            profs.append(ops.coverage_profile(S, lay))
+            if self.routing_profiles is None:
+                profs.append(ops.coverage_profile(S, lay))
         return qbar, kbar, profs, scores
 
     def exchange(self, profs):
         lay = self.batch.layout
-        layer_profiles = [profiles_to_host(p, lay) for p in profs]
+        if self.routing_profiles is not None:
+            layer_profiles = self.routing_profiles
+        else:
+            layer_profiles = [profiles_to_host(p, lay) for p in profs]
         return exchange_estimates(self.batch.lengths, layer_profiles, self.width, self.block, self.world, self.group,
                                   self.q.device)
 
@@ -176,12 +185,16 @@ class DPStep:
         if mark:
             mark("decided")
         nb = lay.nb_per_seq
+        # All layers' per-sequence keep counts in one pinned, asynchronous H2D copy (a pageable
+        # copy would block the host behind the GPU once per layer).
+        k_all = np.minimum(k_final[self.rank][:, None], nb[None, :]).astype(np.int32)
+        self._k_host = torch.from_numpy(k_all).pin_memory()
+        k_dev = self._k_host.to(self.q.device, non_blocking=True)
         outs = []
         for l, s_l in enumerate(self.layer_scales):
-            k_seq = np.minimum(int(k_final[self.rank, l]), nb).astype(np.int32)
-            k_max = int(max(1, k_seq.max()))
+            k_max = int(max(1, k_all[l].max()))
             scale = s_l / math.sqrt(self.d)
-            idx, cnt = ops.topk_select(scores[l], lay, torch.from_numpy(k_seq).to(self.q.device), k_max)
+            idx, cnt = ops.topk_select(scores[l], lay, k_dev[l], k_max)
             o, lse = ops.sparse_attn_fwd(self.q, self.k, self.v, lay, idx, cnt, scale)
             if mark:
                 mark("fwd")
