@@ -27,7 +27,7 @@ using namespace sm100;
 
 constexpr int kM = 128;
 constexpr int kStages = 2;
-constexpr int kThreads = 192;
+constexpr int kThreads = 352;  // warp 0 TMA, warp 1 UMMA, warps 2..9 two column-split math warpgroups, warp 10 TMA (V)
 constexpr float kLog2e = 1.4426950408889634f;
 
 __host__ __device__ constexpr uint32_t pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
@@ -150,47 +150,54 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
   if (threadIdx.x == 0) out[n] = carry;
 }
 
-// P^T row of one key row (this thread): p[r] = 2^(S^T[r] * scale_log2 - lse2[r]) over the B query
-// columns, packed FFMA2 with the per-column -lse2 from shared memory; kMasked zeroes columns
-// outside [r_lo, nq) (causal diagonal / sequence end).
-template <int B, bool kMasked>
-__device__ __forceinline__ void dkv_p(const uint32_t (&sv)[B / 32][32], const float* vs, float scale_log2, int r_lo,
-                                      int nq, float (&p)[B]) {
+// P^T for one key row (this thread) over this warpgroup's NC query columns col0 .. col0+NC:
+// p[r] = 2^(S^T * scale_log2 - lse2[col0 + r]), packed FFMA2 with the per-column -lse2 from
+// shared memory; kMasked zeroes columns outside [r_lo, nq) (causal diagonal / sequence end).
+template <int NC, bool kMasked>
+__device__ __forceinline__ void dkv_p(const uint32_t (&sv)[NC / 32][32], const float* vs, float scale_log2, int col0,
+                                      int r_lo, int nq, float (&p)[NC]) {
   const f2 sc = mk2(scale_log2, scale_log2);
 #pragma unroll
-  for (int pe = 0; pe < B / 2; ++pe) {
+  for (int pe = 0; pe < NC / 2; ++pe) {
     const int r = 2 * pe;
-    const float2 nl = *reinterpret_cast<const float2*>(vs + r);
+    const float2 nl = *reinterpret_cast<const float2*>(vs + col0 + r);
     f2 e = ex2_pair(ffma2(mk2(__uint_as_float(sv[r / 32][r % 32]), __uint_as_float(sv[r / 32][r % 32 + 1])), sc,
                           mk2(nl.x, nl.y)),
                     pe);
     if (kMasked) {
-      e.x = (r < nq && r >= r_lo) ? e.x : 0.f;
-      e.y = (r + 1 < nq && r + 1 >= r_lo) ? e.y : 0.f;
+      e.x = (col0 + r < nq && col0 + r >= r_lo) ? e.x : 0.f;
+      e.y = (col0 + r + 1 < nq && col0 + r + 1 >= r_lo) ? e.y : 0.f;
     }
     p[r] = e.x;
     p[r + 1] = e.y;
   }
 }
 
-// P row of one query row: p[c] = 2^(S[c] * scale_log2 - lse2) (row constant), kMasked zeroes
-// columns >= lim.
-template <int B, bool kMasked>
-__device__ __forceinline__ void dq_p(const uint32_t (&sv)[B / 32][32], float neg_l2, float scale_log2, int lim,
-                                     float (&p)[B]) {
+// P for one query row over NC key columns col0 .. col0+NC: p[c] = 2^(S * scale_log2 - lse2)
+// (row constant); kMasked zeroes columns >= lim.
+template <int NC, bool kMasked>
+__device__ __forceinline__ void dq_p(const uint32_t (&sv)[NC / 32][32], float neg_l2, float scale_log2, int col0,
+                                     int lim, float (&p)[NC]) {
   const f2 sc = mk2(scale_log2, scale_log2), nl = mk2(neg_l2, neg_l2);
 #pragma unroll
-  for (int pe = 0; pe < B / 2; ++pe) {
+  for (int pe = 0; pe < NC / 2; ++pe) {
     const int c = 2 * pe;
     f2 e = ex2_pair(ffma2(mk2(__uint_as_float(sv[c / 32][c % 32]), __uint_as_float(sv[c / 32][c % 32 + 1])), sc, nl),
                     pe);
     if (kMasked) {
-      e.x = c < lim ? e.x : 0.f;
-      e.y = c + 1 < lim ? e.y : 0.f;
+      e.x = col0 + c < lim ? e.x : 0.f;
+      e.y = col0 + c + 1 < lim ? e.y : 0.f;
     }
     p[c] = e.x;
     p[c + 1] = e.y;
   }
+}
+
+// TMEM column of the packed-bf16 A operand for UMMA K-step kk when each column half h of the
+// B-wide score tile stores its packed values at the start of its own half (h * B / 2).
+template <int B>
+__device__ __forceinline__ uint32_t packed_col(int kk) {
+  return static_cast<uint32_t>((kk / (B / 32)) * (B / 2) + (kk % (B / 32)) * 8);
 }
 
 // ------------------------------------------------------------------------------------ dkv
@@ -269,8 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     }
     mbar_init(&bars->st_full, 1);
     mbar_init(&bars->dpt_full, 1);
-    mbar_init(&bars->pt_full, 128);
-    mbar_init(&bars->dst_full, 128);
+    mbar_init(&bars->pt_full, 256);
+    mbar_init(&bars->dst_full, 256);
     mbar_init(&bars->acc_done, 1);
     fence_barrier_init();
   }
@@ -386,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
-            mma_ts(tmem + C::kDV, tmem + C::kSt + kk * 8, desc_sw128(da(g) + kk * 2048, B * 128, 1024), idesc_acc,
+            mma_ts(tmem + C::kDV, tmem + C::kSt + packed_col<B>(kk), desc_sw128(da(g) + kk * 2048, B * 128, 1024), idesc_acc,
                    (m > 0 || kk > 0) ? 1u : 0u);
           if (m + 1 < items) issue_st(g + 1);
           else tc_commit(&bars->kv_empty);  // K (last S^T) and V (last dP^T) no longer read
@@ -394,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
-            mma_ts(tmem + C::kDK, tmem + C::kDPt + kk * 8, desc_sw128(qa(g) + kk * 2048, B * 128, 1024), idesc_acc,
+            mma_ts(tmem + C::kDK, tmem + C::kDPt + packed_col<B>(kk), desc_sw128(qa(g) + kk * 2048, B * 128, 1024), idesc_acc,
                    (m > 0 || kk > 0) ? 1u : 0u);
           tc_commit(&bars->q_empty[g % kStages]);
           if (m + 1 < items) issue_dpt(g + 1);
@@ -403,11 +410,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         ++t;
       }
     }
-  } else {
+  } else if (warp < 10) {
     // ------------------------------------------------------------ softmax-gradient + epilogue
+    // Two warpgroups split every key row's B query columns (and the D output columns of the
+    // epilogue) in halves; the math is column-independent, so they never synchronise.
+    constexpr int HB = B / 2;
     const int quarter = warp & 3;
+    const int hf = (warp - 2) >> 2;
     const int c = quarter * 32 + lane;  // key row
     const uint32_t lf = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t st_col = C::kSt + hf * HB, dpt_col = C::kDPt + hf * HB;
     int g = 0, t = 0;
     for (int k = 0;; ++k) {
       const int it = sched::snake_item(order, n_items, grid, cta, k);
@@ -428,25 +440,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         mbar_wait(&bars->q_full[st], (g / kStages) & 1);  // producer's plain smem writes of vs
         mbar_wait(&bars->st_full, g & 1);
         tc_fence_after();
-        float p[B];
+        float p[HB];
         {
-          uint32_t sv[B / 32][32];
+          uint32_t sv[HB / 32][32];
 #pragma unroll
-          for (int c2 = 0; c2 < B / 32; ++c2) tmem_ld32(tmem + lf + C::kSt + c2 * 32, sv[c2]);
+          for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(tmem + lf + st_col + c2 * 32, sv[c2]);
           tmem_wait_ld();
           // vs[0..B) holds -lse2 of the item's query rows (producer negates).
-          if (r_lo == 0 && nq == B) {
-            dkv_p<B, false>(sv, vs, scale_log2, 0, B, p);
+          if (r_lo <= hf * HB && nq == B) {
+            dkv_p<HB, false>(sv, vs, scale_log2, hf * HB, 0, B, p);
           } else {
-            dkv_p<B, true>(sv, vs, scale_log2, r_lo, nq, p);
+            dkv_p<HB, true>(sv, vs, scale_log2, hf * HB, r_lo, nq, p);
           }
         }
+        {
+          uint32_t pw[HB / 2];
 #pragma unroll
-        for (int c2 = 0; c2 < B / 64; ++c2) {
-          uint32_t pw[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) pw[e] = pack_bf16x2(p[c2 * 64 + 2 * e], p[c2 * 64 + 2 * e + 1]);
-          tmem_st32(tmem + lf + C::kSt + c2 * 32, pw);
+          for (int e = 0; e < HB / 2; ++e) pw[e] = pack_bf16x2(p[2 * e], p[2 * e + 1]);
+          if constexpr (HB == 64) {
+            tmem_st32(tmem + lf + st_col, pw);
+          } else {
+            tmem_st16(tmem + lf + st_col, pw);
+          }
         }
         tmem_wait_st();
         tc_fence_before();
@@ -456,22 +471,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         {
           // dP^T chunks software-pipelined: chunk c2+1 is in flight while c2 is processed.
           uint32_t pv[2][32];
-          tmem_ld32(tmem + lf + C::kDPt, pv[0]);
+          tmem_ld32(tmem + lf + dpt_col, pv[0]);
           tmem_wait_ld();
 #pragma unroll
-          for (int c2 = 0; c2 < B / 32; ++c2) {
-            if (c2 + 1 < B / 32) tmem_ld32(tmem + lf + C::kDPt + (c2 + 1) * 32, pv[(c2 + 1) & 1]);
+          for (int c2 = 0; c2 < HB / 32; ++c2) {
+            if (c2 + 1 < HB / 32) tmem_ld32(tmem + lf + dpt_col + (c2 + 1) * 32, pv[(c2 + 1) & 1]);
             uint32_t dd[16];
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
               const int r = c2 * 32 + e;
-              const float2 nd = *reinterpret_cast<const float2*>(vs + B + r);  // -D
+              const float2 nd = *reinterpret_cast<const float2*>(vs + B + hf * HB + r);  // -D
               const f2 ds = fmul2(mk2(p[r], p[r + 1]), fadd2(mk2(__uint_as_float(pv[c2 & 1][e]),
                                                                   __uint_as_float(pv[c2 & 1][e + 1])),
                                                               mk2(nd.x, nd.y)));
               dd[e / 2] = pack_bf16x2(ds.x, ds.y);
             }
-            tmem_st16(tmem + lf + C::kDPt + c2 * 16, dd);  // over columns already read
+            tmem_st16(tmem + lf + dpt_col + c2 * 16, dd);  // over columns already read
             tmem_wait_ld();
           }
         }
@@ -484,15 +499,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         tc_fence_after();
         ++t;
       }
-      // Epilogue: dV and dK * scale for the valid key rows (zeros if nobody selected the block).
+      // Epilogue: dV and dK * scale for the valid key rows (zeros if nobody selected the block);
+      // warpgroup hf writes output columns [hf * D/2, (hf + 1) * D/2).
       const bool store = c < nkv;
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
-        const uint32_t col = part == 0 ? C::kDV : C::kDK;
+        const uint32_t col = (part == 0 ? C::kDV : C::kDK) + hf * (D / 2);
         const float mul = part == 0 ? 1.0f : scale;
-        uint16_t* row = (part == 0 ? dv : dk) + (static_cast<size_t>(kv0 + c) * hkv + w.hk) * D;
+        uint16_t* row = (part == 0 ? dv : dk) + (static_cast<size_t>(kv0 + c) * hkv + w.hk) * D + hf * (D / 2);
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
+        for (int cc = 0; cc < D / 64; ++cc) {
           uint32_t v[32];
           if (items > 0) {
             tmem_ld32(tmem + lf + col + cc * 32, v);
@@ -585,9 +601,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
       mbar_init(&bars->v_empty[st], 1);
     }
     mbar_init(&bars->dp_full, 1);
-    mbar_init(&bars->ds_full, 128);
+    mbar_init(&bars->ds_full, 256);
     mbar_init(&bars->dq_done, 1);
-    mbar_init(&bars->dq_free, 128);
+    mbar_init(&bars->dq_free, 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kCols>(&bars->tmem_base);
@@ -614,12 +630,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
     return w;
   };
 
-  if (warp == 0) {
-    if (lane == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      tma_prefetch(&tm_do);
+  if (warp == 0 || warp == 10) {
+    // Warp 0 streams Q/dO + K, warp 10 streams V (independent rings in separate warps).
+    const int lane = (warp == 10) ? 1 : threadIdx.x & 31;  // role: 0 = Q/dO + K, 1 = V
+    if (lane < 2 && (threadIdx.x & 31) == 0) {
+      if (lane == 0) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_do);
+      } else {
+        tma_prefetch(&tm_v);
+      }
       int g = 0, q = 0;
       for (int k = 0;; ++k) {
         const int it = sched::snake_item(order, n_items, grid, cta, k);
@@ -627,26 +648,31 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         const QItem w = decode_q(it);
         if (w.n <= 0) continue;
         const int hk = w.h / (hq / hkv);
-        const int qb = q & 1;
-        const int row0 = w.seq0 + w.i * B;
-        mbar_wait(&bars->qdo_empty[qb], ((q >> 1) & 1) ^ 1);
-        mbar_expect_tx(&bars->qdo_full[qb], 2 * C::kQBytes);
-        for (int c = 0; c < C::kChunks; ++c) {
-          tma_load_3d(q_smem + qb * C::kQBytes + c * kM * 128, &tm_q, &bars->qdo_full[qb], c * 64, w.h, row0);
-          tma_load_3d(do_smem + qb * C::kQBytes + c * kM * 128, &tm_do, &bars->qdo_full[qb], c * 64, w.h, row0);
+        if (lane == 0) {
+          const int qb = q & 1;
+          const int row0 = w.seq0 + w.i * B;
+          mbar_wait(&bars->qdo_empty[qb], ((q >> 1) & 1) ^ 1);
+          mbar_expect_tx(&bars->qdo_full[qb], 2 * C::kQBytes);
+          for (int c = 0; c < C::kChunks; ++c) {
+            tma_load_3d(q_smem + qb * C::kQBytes + c * kM * 128, &tm_q, &bars->qdo_full[qb], c * 64, w.h, row0);
+            tma_load_3d(do_smem + qb * C::kQBytes + c * kM * 128, &tm_do, &bars->qdo_full[qb], c * 64, w.h, row0);
+          }
         }
         for (int j = 0; j < w.n; ++j, ++g) {
           const int kv_row = w.seq0 + __ldg(w.list + j) * B;
-          const int st = g % kStages;
-          mbar_wait(&bars->k_empty[st], ((g / kStages) & 1) ^ 1);
-          mbar_expect_tx(&bars->k_full[st], C::kKVBytes);
-          for (int c = 0; c < C::kChunks; ++c)
-            tma_load_3d(k_smem + st * C::kKVBytes + c * B * 128, &tm_k, &bars->k_full[st], c * 64, hk, kv_row);
-          const int vst = g % kVS;
-          mbar_wait(&bars->v_empty[vst], ((g / kVS) & 1) ^ 1);
-          mbar_expect_tx(&bars->v_full[vst], C::kKVBytes);
-          for (int c = 0; c < C::kChunks; ++c)
-            tma_load_3d(v_smem + vst * C::kKVBytes + c * B * 128, &tm_v, &bars->v_full[vst], c * 64, hk, kv_row);
+          if (lane == 0) {
+            const int st = g % kStages;
+            mbar_wait(&bars->k_empty[st], ((g / kStages) & 1) ^ 1);
+            mbar_expect_tx(&bars->k_full[st], C::kKVBytes);
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_load_3d(k_smem + st * C::kKVBytes + c * B * 128, &tm_k, &bars->k_full[st], c * 64, hk, kv_row);
+          } else {
+            const int vst = g % kVS;
+            mbar_wait(&bars->v_empty[vst], ((g / kVS) & 1) ^ 1);
+            mbar_expect_tx(&bars->v_full[vst], C::kKVBytes);
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_load_3d(v_smem + vst * C::kKVBytes + c * B * 128, &tm_v, &bars->v_full[vst], c * 64, hk, kv_row);
+          }
         }
         ++q;
       }
@@ -737,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
           const int st = g % kStages;
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
-            mma_ts(tmem + C::kDQ, tmem + s_col(g) + kk * 8,
+            mma_ts(tmem + C::kDQ, tmem + s_col(g) + packed_col<B>(kk),
                    desc_sw128(k_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024), idesc_dq,
                    (j > 0 || kk > 0) ? 1u : 0u);
           tc_commit(&bars->k_empty[st]);
@@ -759,8 +785,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         ++q;
       }
     }
-  } else {
+  } else if (warp < 10) {
+    // Two warpgroups split every query row's B key columns and the D output columns in halves.
+    constexpr int HB = B / 2;
     const int quarter = warp & 3;
+    const int hf = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;
     const uint32_t lf = static_cast<uint32_t>(quarter * 32) << 16;
     int g = 0, q = 0;
@@ -771,10 +800,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
       const int row0 = w.seq0 + w.i * B;
       const int nrows = min(B, w.seq_len - w.i * B);
       const bool valid = r < nrows;
-      uint16_t* dq_row = dq + (static_cast<size_t>(row0 + r) * hq + w.h) * D;
+      uint16_t* dq_row = dq + (static_cast<size_t>(row0 + r) * hq + w.h) * D + hf * (D / 2);
       if (w.n <= 0) {
         if (valid)
-          for (int e = 0; e < D / 8; ++e) reinterpret_cast<uint4*>(dq_row)[e] = make_uint4(0, 0, 0, 0);
+          for (int e = 0; e < D / 16; ++e) reinterpret_cast<uint4*>(dq_row)[e] = make_uint4(0, 0, 0, 0);
         continue;
       }
       const float l2 = valid ? __ldg(lse2 + static_cast<size_t>(w.h) * tp + row0 + r) : 0.f;
@@ -783,30 +812,31 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         const int jb = __ldg(w.list + j);
         const int key_lim = min(B, w.seq_len - jb * B);
         const int lim = valid ? min(key_lim, jb == w.i ? r + 1 : B) : 0;
-        const uint32_t s_col = (g & 1) ? C::kS1 : C::kS0;
+        const uint32_t s_col = ((g & 1) ? C::kS1 : C::kS0) + hf * HB;
         mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();
-        float p[B];
+        float p[HB];
         {
-          uint32_t sv[B / 32][32];
+          uint32_t sv[HB / 32][32];
 #pragma unroll
-          for (int c2 = 0; c2 < B / 32; ++c2) tmem_ld32(tmem + lf + s_col + c2 * 32, sv[c2]);
+          for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(tmem + lf + s_col + c2 * 32, sv[c2]);
           tmem_wait_ld();
-          if (__all_sync(0xffffffffu, lim == B)) {
-            dq_p<B, false>(sv, -l2, scale_log2, B, p);
+          if (__all_sync(0xffffffffu, lim >= (hf + 1) * HB)) {
+            dq_p<HB, false>(sv, -l2, scale_log2, hf * HB, B, p);
           } else {
-            dq_p<B, true>(sv, -l2, scale_log2, lim, p);
+            dq_p<HB, true>(sv, -l2, scale_log2, hf * HB, lim, p);
           }
         }
         mbar_wait(&bars->dp_full, g & 1);
         tc_fence_after();
         {
+          const uint32_t dp_col = C::kDP + hf * HB;
           uint32_t pv[2][32];
-          tmem_ld32(tmem + lf + C::kDP, pv[0]);
+          tmem_ld32(tmem + lf + dp_col, pv[0]);
           tmem_wait_ld();
 #pragma unroll
-          for (int c2 = 0; c2 < B / 32; ++c2) {
-            if (c2 + 1 < B / 32) tmem_ld32(tmem + lf + C::kDP + (c2 + 1) * 32, pv[(c2 + 1) & 1]);
+          for (int c2 = 0; c2 < HB / 32; ++c2) {
+            if (c2 + 1 < HB / 32) tmem_ld32(tmem + lf + dp_col + (c2 + 1) * 32, pv[(c2 + 1) & 1]);
             uint32_t dsp[16];
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
@@ -816,7 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
                                                               mk2(-dd, -dd)));
               dsp[e / 2] = pack_bf16x2(ds.x, ds.y);
             }
-            tmem_st16(tmem + lf + s_col + c2 * 16, dsp);  // dS over S (already in registers)
+            tmem_st16(tmem + lf + s_col + c2 * 16, dsp);  // dS over this half's S (already in registers)
             tmem_wait_ld();
           }
         }
@@ -826,15 +856,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
       }
       mbar_wait(&bars->dq_done, q & 1);
       tc_fence_after();
-      uint32_t v[D / 32][32];
+      uint32_t v[D / 64][32];
 #pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) tmem_ld32(tmem + lf + C::kDQ + cc * 32, v[cc]);
+      for (int cc = 0; cc < D / 64; ++cc) tmem_ld32(tmem + lf + C::kDQ + hf * (D / 2) + cc * 32, v[cc]);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bars->dq_free);
       if (valid) {
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
+        for (int cc = 0; cc < D / 64; ++cc) {
           uint4* dst = reinterpret_cast<uint4*>(dq_row + cc * 32);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {

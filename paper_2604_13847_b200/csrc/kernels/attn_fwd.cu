@@ -32,8 +32,9 @@ namespace {
 using namespace sm100;
 
 constexpr int kM = 128;                 // UMMA M / Q tile rows
-constexpr int kStages = 2;              // K and V ring depth
-constexpr int kThreads = 192;           // 6 warps
+constexpr int kStages = 2;              // K ring depth
+constexpr int kVStages = 3;             // V ring depth (V is consumed last: needs the longest prefetch)
+constexpr int kThreads = 224;           // 7 warps: Q/K producer, UMMA, 4 softmax, V producer
 constexpr float kRescaleThresh = 8.0f;  // log2 units: lazily rescale O only on a 256x max jump
 
 template <int D, int B>
@@ -41,7 +42,7 @@ struct FwdCfg {
   static constexpr int kChunks = D / 64;              // 128-byte swizzle atoms along D
   static constexpr int kQBytes = kChunks * kM * 128;  // one Q tile
   static constexpr int kKVBytes = kChunks * B * 128;  // one K or V block
-  static constexpr int kSmemTiles = 2 * kQBytes + 2 * kStages * kKVBytes;
+  static constexpr int kSmemTiles = 2 * kQBytes + (kStages + kVStages) * kKVBytes;
   static constexpr int kTmemS0 = 0, kTmemS1 = B, kTmemO0 = 2 * B, kTmemO1 = 2 * B + D;
   static constexpr uint32_t kTmemCols = (2 * B + 2 * D) <= 256 ? 256 : 512;
   static constexpr int kSmemBytes = kSmemTiles + 1024 /*align slack*/ + 256 /*barriers*/;
@@ -50,7 +51,7 @@ struct FwdCfg {
 struct FwdBars {
   uint64_t q_full[2], q_empty[2];
   uint64_t k_full[kStages], k_empty[kStages];
-  uint64_t v_full[kStages], v_empty[kStages];
+  uint64_t v_full[kVStages], v_empty[kVStages];
   uint64_t s_full[2], p_full[2];
   uint64_t o_done, o_free[2];
   uint32_t tmem_base;
@@ -130,8 +131,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
     const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off,
     int nseq, int total_tokens, int hq, int hkv, const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt,
     int hsel, int k_max, float scale_log2, uint16_t* __restrict__ out, float* __restrict__ lse,
-    const int32_t* __restrict__ order, int n_items) {
+    const int32_t* __restrict__ order, int n_items, unsigned long long* __restrict__ trace) {
   using C = FwdCfg<D, B>;
+  // Debug timeline (sb_debug_set_trace): CTA 0 records clock64 at phase boundaries.
+  auto tr = [&](int slot, int g) {
+    if (trace != nullptr && blockIdx.x == 0 && g < 256) trace[g * 8 + slot] = clock64();
+  };
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -155,6 +160,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&bars->k_full[st], 1);
       mbar_init(&bars->k_empty[st], 1);
+    }
+    for (int st = 0; st < kVStages; ++st) {
       mbar_init(&bars->v_full[st], 1);
       mbar_init(&bars->v_empty[st], 1);
     }
@@ -167,41 +174,55 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+  // TMA producer over the CTA's item stream: Q + K (v_stream = false) or V (v_stream = true).
+  auto produce = [&](bool v_stream) {
+    if (lane != 0) return;
+    if (v_stream) {
+      tma_prefetch(&tm_v);
+    } else {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      int g = 0, q = 0;
-      for (int k = 0;; ++k) {
-        const int it = sched::snake_item(order, n_items, grid, cta, k);
-        if (it < 0) break;
-        const Item w = decode(it, cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
-        if (w.n <= 0) continue;
-        const int hk = w.h / (hq / hkv);
+    }
+    int g = 0, q = 0;
+    for (int k = 0;; ++k) {
+      const int it = sched::snake_item(order, n_items, grid, cta, k);
+      if (it < 0) break;
+      const Item w = decode(it, cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
+      if (w.n <= 0) continue;
+      const int hk = w.h / (hq / hkv);
+      if (!v_stream) {
         const int qb = q & 1;
         mbar_wait(&bars->q_empty[qb], ((q >> 1) & 1) ^ 1);
         mbar_expect_tx(&bars->q_full[qb], C::kQBytes);
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_3d(q_smem + qb * C::kQBytes + c * kM * 128, &tm_q, &bars->q_full[qb], c * 64, w.h,
                       w.seq0 + w.i * B);
-        for (int j = 0; j < w.n; ++j, ++g) {
+      }
+      for (int j = 0; j < w.n; ++j, ++g) {
+        const int kv_row = w.seq0 + __ldg(w.list + j) * B;
+        if (!v_stream) {
           const int st = g % kStages;
-          const uint32_t ph = (g / kStages) & 1;
-          const int kv_row = w.seq0 + __ldg(w.list + j) * B;
-          mbar_wait(&bars->k_empty[st], ph ^ 1);
+          mbar_wait(&bars->k_empty[st], ((g / kStages) & 1) ^ 1);
           mbar_expect_tx(&bars->k_full[st], C::kKVBytes);
           for (int c = 0; c < C::kChunks; ++c)
             tma_load_3d(k_smem + st * C::kKVBytes + c * B * 128, &tm_k, &bars->k_full[st], c * 64, hk, kv_row);
-          mbar_wait(&bars->v_empty[st], ph ^ 1);
-          mbar_expect_tx(&bars->v_full[st], C::kKVBytes);
+        } else {
+          const int vs = g % kVStages;
+          mbar_wait(&bars->v_empty[vs], ((g / kVStages) & 1) ^ 1);
+          mbar_expect_tx(&bars->v_full[vs], C::kKVBytes);
           for (int c = 0; c < C::kChunks; ++c)
-            tma_load_3d(v_smem + st * C::kKVBytes + c * B * 128, &tm_v, &bars->v_full[st], c * 64, hk, kv_row);
+            tma_load_3d(v_smem + vs * C::kKVBytes + c * B * 128, &tm_v, &bars->v_full[vs], c * 64, hk, kv_row);
         }
-        ++q;
       }
+      ++q;
     }
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producers
+    // Warp 0 streams Q + K, warp 6 streams V: separate warps, so neither ring's wait blocks
+    // the other (divergent lanes of one warp would serialise on each other's sleeps).
+    produce(false);
   } else if (warp == 1) {
     // ------------------------------------------------------------ UMMA issuer
     if (lane == 0) {
@@ -211,10 +232,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
       // Pending PV (the previous global block), issued after the next QK.
       int pv_g = -1, pv_j = 0, pv_q = 0;
       auto issue_pv = [&]() {
-        const int st = pv_g % kStages;
+        const int st = pv_g % kVStages;
         const int ob = pv_q & 1;
-        mbar_wait(&bars->v_full[st], (pv_g / kStages) & 1);
+        mbar_wait(&bars->v_full[st], (pv_g / kVStages) & 1);
+        tr(2, pv_g);
         mbar_wait(&bars->p_full[pv_g & 1], (pv_g >> 1) & 1);
+        tr(3, pv_g);
         if (pv_j == 0) mbar_wait(&bars->o_free[ob], ((pv_q >> 1) & 1) ^ 1);  // epilogue of item q-2 done
         tc_fence_after();
         const uint32_t p_tmem = tmem + ((pv_g & 1) ? C::kTmemS1 : C::kTmemS0);
@@ -238,7 +261,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         mbar_wait(&bars->q_full[qb], (q >> 1) & 1);
         for (int j = 0; j < w.n; ++j, ++g) {
           const int st = g % kStages;
+          tr(0, g);
           mbar_wait(&bars->k_full[st], (g / kStages) & 1);
+          tr(1, g);
           tc_fence_after();
           const uint32_t d_s = tmem + ((g & 1) ? C::kTmemS1 : C::kTmemS0);
 #pragma unroll
@@ -260,6 +285,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
       }
       if (pv_g >= 0) issue_pv();
     }
+  } else if (warp == 6) {
+    produce(true);
   } else {
     // ------------------------------------------------------------ softmax / epilogue
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
@@ -289,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         const uint32_t t_s = tmem + lane_field + (b ? C::kTmemS1 : C::kTmemS0);
         const int jb = __ldg(w.list + j);
         mbar_wait(&bars->s_full[b], (g >> 1) & 1);
+        if (threadIdx.x == 64) tr(4, g);
         tc_fence_after();
         uint32_t sv[B / 32][32];
 #pragma unroll
@@ -308,8 +336,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         const float sum0 = sum, sum1 = 0.f;
         l_run = l_run * alpha + (sum0 + sum1);
         tmem_wait_st();
+        if (threadIdx.x == 64) tr(5, g);
         if (j > 0) {
           mbar_wait(&bars->o_done, (g - 1) & 1);  // PV_{g-1} (same item) finished writing O
+          if (threadIdx.x == 64) tr(6, g);
           tc_fence_after();
           if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll
@@ -366,6 +396,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
   }
 }
 
+unsigned long long* g_trace = nullptr;  // debug timeline buffer (sb_debug_set_trace)
+
 template <int D, int B>
 void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* cu, const int32_t* blk_off,
                 int nseq, int total, int nb_total, int hq, int hkv, const int32_t* idx, const int32_t* cnt, int hsel,
@@ -382,12 +414,15 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
              "sb_sparse_attn_fwd: smem attribute");
   const int grid = std::min(n_items, sched::num_sms());
   kern<<<grid, kThreads, C::kSmemBytes, st>>>(tq, tk, tv, cu, blk_off, nseq, total, hq, hkv, idx, cnt, hsel, k_max,
-                                              scale * 1.4426950408889634f, o, lse, order, n_items);
+                                              scale * 1.4426950408889634f, o, lse, order, n_items, g_trace);
   launched("sb_sparse_attn_fwd");
 }
 
 }  // namespace
 }  // namespace sbk
+
+// Debug only: device buffer of 256 x 8 uint64 for CTA 0's phase timeline (NULL disables).
+SB_API void sb_debug_set_trace(unsigned long long* buf) { sbk::g_trace = buf; }
 
 SB_API size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq, int k_max) {
   return sbk::sched::order_workspace_bytes(nb_total * hq, hq * (k_max + 1));

@@ -1,0 +1,38 @@
+"""Debug: phase timeline of CTA 0 of the forward kernel on the C2 workload (not product)."""
+import ctypes, math, sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2604_13847_b200 import ops
+import bench
+lib = ops._lib()
+lib.sb_debug_set_trace.argtypes = [ctypes.c_void_p]
+cu, k_seq = bench.workload(0)
+T = int(cu[-1]); H, D, B = 32, 128, 128
+lay = ops.VarlenLayout.build(cu, B)
+g = torch.Generator(device="cuda").manual_seed(0)
+q, k, v = (torch.randn((T, H, D), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+S = ops.block_scores(q, k, lay)
+idx, cnt = ops.topk_select(S, lay, torch.from_numpy(k_seq).cuda(), int(k_seq.max()))
+buf = torch.zeros(256 * 8, dtype=torch.int64, device="cuda")
+for it in range(3):
+    lib.sb_debug_set_trace(ctypes.c_void_p(buf.data_ptr() if it == 2 else 0))
+    ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)
+torch.cuda.synchronize()
+t = buf.cpu().numpy().reshape(256, 8).astype(np.int64)
+base = t[0, 0]
+names = ["mma:before k_full", "mma:k ready/QK issue", "mma:PV v ready", "mma:PV p_full seen", "smx:S ready", "smx:P done", "smx:o_done seen"]
+print("g  " + " | ".join(f"{n:>20s}" for n in names))
+for gg in range(0, 60):
+    row = t[gg]
+    print(f"{gg:3d} " + " | ".join(f"{(x - base) if x else -1:20d}" for x in row[:7]))
+d = np.diff(t[1:60, 1])
+print("median cycles between QK issues:", np.median(d))
+print("median softmax busy (P done - S ready):", np.median(t[1:60, 5] - t[1:60, 4]))
+print("median S ready -> next S ready:", np.median(np.diff(t[1:60, 4])))
+r = slice(2, 58)
+print("median k_full wait:", np.median(t[r, 1] - t[r, 0]))
+print("median QK issue -> v_full seen (prev PV):", np.median(t[r, 2] - t[r, 1]))
+print("median v_full -> p_full seen:", np.median(t[r, 3] - t[r, 2]))
+print("median p_full seen -> next before-k_full:", np.median(t[3:59, 0] - t[2:58, 3]))
+print("median S ready after QK issue:", np.median(t[r, 4] - t[r, 1]))
+print("median o_done wait (P done -> o_done seen):", np.median(t[r, 6] - t[r, 5]))
