@@ -158,18 +158,25 @@ __device__ __forceinline__ void dkv_p(const uint32_t (&sv)[NC / 32][32], const f
                                       int r_lo, int nq, float (&p)[NC]) {
   const f2 sc = mk2(scale_log2, scale_log2);
 #pragma unroll
-  for (int pe = 0; pe < NC / 2; ++pe) {
-    const int r = 2 * pe;
-    const float2 nl = *reinterpret_cast<const float2*>(vs + col0 + r);
-    f2 e = ex2_pair(ffma2(mk2(__uint_as_float(sv[r / 32][r % 32]), __uint_as_float(sv[r / 32][r % 32 + 1])), sc,
-                          mk2(nl.x, nl.y)),
-                    pe);
-    if (kMasked) {
-      e.x = (col0 + r < nq && col0 + r >= r_lo) ? e.x : 0.f;
-      e.y = (col0 + r + 1 < nq && col0 + r + 1 >= r_lo) ? e.y : 0.f;
+  for (int p4 = 0; p4 < NC / 4; ++p4) {
+    // One 16-byte broadcast load per 4 columns: the shared-memory crossbar is shared with the
+    // UMMA operand reads, which saturate it.
+    const float4 nl = *reinterpret_cast<const float4*>(vs + col0 + 4 * p4);
+#pragma unroll
+    for (int hp = 0; hp < 2; ++hp) {
+      const int pe = 2 * p4 + hp;
+      const int r = 2 * pe;
+      const f2 nl2 = hp == 0 ? mk2(nl.x, nl.y) : mk2(nl.z, nl.w);
+      f2 e = ex2_pair(ffma2(mk2(__uint_as_float(sv[r / 32][r % 32]), __uint_as_float(sv[r / 32][r % 32 + 1])), sc,
+                            nl2),
+                      pe);
+      if (kMasked) {
+        e.x = (col0 + r < nq && col0 + r >= r_lo) ? e.x : 0.f;
+        e.y = (col0 + r + 1 < nq && col0 + r + 1 >= r_lo) ? e.y : 0.f;
+      }
+      p[r] = e.x;
+      p[r + 1] = e.y;
     }
-    p[r] = e.x;
-    p[r + 1] = e.y;
   }
 }
 
@@ -250,8 +257,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off, int nseq, int hq, int hkv, int hsel,
     const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent, const float* __restrict__ lse2,
     const float* __restrict__ dvec, int tp, float scale, float scale_log2, uint16_t* __restrict__ dk,
-    uint16_t* __restrict__ dv, const int32_t* __restrict__ order, int n_items) {
+    uint16_t* __restrict__ dv, const int32_t* __restrict__ order, int n_items, unsigned long long* trace) {
   using C = DkvCfg<D, B>;
+  auto tr = [&](int slot, int g) {
+    if (trace != nullptr && blockIdx.x == 0 && g < 256) trace[g * 16 + slot] = clock64();
+  };
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -326,7 +336,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         pair_of(w, m, h, gi);
         const int q0 = w.seq0 + (gi - blk_off[w.s]) * B;
         const int nq = min(B, w.seq_len - (gi - blk_off[w.s]) * B);
+        // -lse2 / -D of the pair's query rows: all loads in flight before the ring-slot wait.
+        float nl[B / 32], nd[B / 32];
+#pragma unroll
+        for (int e = 0; e < B / 32; ++e) {
+          const int r = e * 32 + lane;
+          const bool ok = r < nq;
+          nl[e] = ok ? __ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+          nd[e] = ok ? __ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+        }
+        if (lane == 0) tr(11, g);
         mbar_wait(&bars->q_empty[st], ph ^ 1);
+        if (lane == 0) tr(12, g);
         if (lane == 0) {
           mbar_expect_tx(&bars->q_full[st], 2 * C::kQBytes);
           for (int c = 0; c < C::kChunks; ++c) {
@@ -335,12 +356,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
           }
         }
         float* vs = vec_smem + st * 2 * B;
-        for (int r = lane; r < B; r += 32) {
-          const bool ok = r < nq;
-          vs[r] = ok ? -__ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
-          vs[B + r] = ok ? -__ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+#pragma unroll
+        for (int e = 0; e < B / 32; ++e) {
+          vs[e * 32 + lane] = -nl[e];
+          vs[B + e * 32 + lane] = -nd[e];
         }
         __syncwarp();
+        if (lane == 0) tr(13, g);
         if (lane == 0) mbar_arrive(&bars->q_full[st]);
       }
       ++t;
@@ -357,7 +379,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
       auto qa = [&](int gg) { return smem_u32(q_smem + (gg % kStages) * C::kQBytes); };
       auto da = [&](int gg) { return smem_u32(do_smem + (gg % kStages) * C::kQBytes); };
       auto issue_st = [&](int gg) {
+        tr(8, gg);
         mbar_wait(&bars->q_full[gg % kStages], (gg / kStages) & 1);
+        tr(9, gg);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -389,7 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         issue_st(g);
         issue_dpt(g);
         for (int m = 0; m < items; ++m, ++g) {
+          tr(0, g);
           mbar_wait(&bars->pt_full, g & 1);
+          tr(1, g);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
@@ -397,13 +423,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
                    (m > 0 || kk > 0) ? 1u : 0u);
           if (m + 1 < items) issue_st(g + 1);
           else tc_commit(&bars->kv_empty);  // K (last S^T) and V (last dP^T) no longer read
+          tr(2, g);
           mbar_wait(&bars->dst_full, g & 1);
+          tr(3, g);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
             mma_ts(tmem + C::kDK, tmem + C::kDPt + packed_col<B>(kk), desc_sw128(qa(g) + kk * 2048, B * 128, 1024), idesc_acc,
                    (m > 0 || kk > 0) ? 1u : 0u);
           tc_commit(&bars->q_empty[g % kStages]);
+          tr(10, g);
           if (m + 1 < items) issue_dpt(g + 1);
         }
         tc_commit(&bars->acc_done);
@@ -439,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         const float* vs = vec_smem + st * 2 * B;
         mbar_wait(&bars->q_full[st], (g / kStages) & 1);  // producer's plain smem writes of vs
         mbar_wait(&bars->st_full, g & 1);
+        if (threadIdx.x == 64) tr(4, g);
         tc_fence_after();
         float p[HB];
         {
@@ -466,7 +496,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->pt_full);
+        if (threadIdx.x == 64) tr(5, g);
         mbar_wait(&bars->dpt_full, g & 1);
+        if (threadIdx.x == 64) tr(6, g);
         tc_fence_after();
         {
           // dP^T chunks software-pipelined: chunk c2+1 is in flight while c2 is processed.
@@ -478,13 +510,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
             if (c2 + 1 < HB / 32) tmem_ld32(tmem + lf + dpt_col + (c2 + 1) * 32, pv[(c2 + 1) & 1]);
             uint32_t dd[16];
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
+            for (int e = 0; e < 32; e += 4) {
               const int r = c2 * 32 + e;
-              const float2 nd = *reinterpret_cast<const float2*>(vs + B + hf * HB + r);  // -D
-              const f2 ds = fmul2(mk2(p[r], p[r + 1]), fadd2(mk2(__uint_as_float(pv[c2 & 1][e]),
-                                                                  __uint_as_float(pv[c2 & 1][e + 1])),
-                                                              mk2(nd.x, nd.y)));
-              dd[e / 2] = pack_bf16x2(ds.x, ds.y);
+              const float4 nd = *reinterpret_cast<const float4*>(vs + B + hf * HB + r);  // -D
+              const f2 ds0 = fmul2(mk2(p[r], p[r + 1]), fadd2(mk2(__uint_as_float(pv[c2 & 1][e]),
+                                                                   __uint_as_float(pv[c2 & 1][e + 1])),
+                                                               mk2(nd.x, nd.y)));
+              const f2 ds1 = fmul2(mk2(p[r + 2], p[r + 3]), fadd2(mk2(__uint_as_float(pv[c2 & 1][e + 2]),
+                                                                       __uint_as_float(pv[c2 & 1][e + 3])),
+                                                                   mk2(nd.z, nd.w)));
+              dd[e / 2] = pack_bf16x2(ds0.x, ds0.y);
+              dd[e / 2 + 1] = pack_bf16x2(ds1.x, ds1.y);
             }
             tmem_st16(tmem + lf + dpt_col + c2 * 16, dd);  // over columns already read
             tmem_wait_ld();
@@ -493,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->dst_full);
+        if (threadIdx.x == 64) tr(7, g);
       }
       if (items > 0) {
         mbar_wait(&bars->acc_done, t & 1);
@@ -890,6 +927,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
 
 // ------------------------------------------------------------------------------------ host
 constexpr int kMaxKvCost = 4096;
+unsigned long long* g_trace_bwd = nullptr;  // debug timeline buffer (sb_debug_set_trace_bwd)
 
 struct BwdWorkspace {
   size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, total;
@@ -964,7 +1002,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
                "sb_sparse_attn_bwd: smem attribute (dkv)");
     kern<<<std::min(kv_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, cu, blk_off, nseq, hq, hkv, hsel,
                                                                    tr_off, tr_ent, lse2, dvec, w.tp, scale,
-                                                                   scale_log2, dk, dv, order_kv, kv_items);
+                                                                   scale_log2, dk, dv, order_kv, kv_items, g_trace_bwd);
     launched("sb_sparse_attn_bwd/dkv");
   }
   {
@@ -985,6 +1023,9 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
 
 }  // namespace
 }  // namespace sbk
+
+// Debug only: device buffer of 256 x 16 uint64 for CTA 0 of the dK/dV pass (NULL disables).
+SB_API void sb_debug_set_trace_bwd(unsigned long long* buf) { sbk::g_trace_bwd = buf; }
 
 SB_API size_t sb_sparse_attn_bwd_workspace_size(int total_tokens, int nb_total, int hq, int hkv, int head_dim, int hsel,
                                                 int k_max) {
