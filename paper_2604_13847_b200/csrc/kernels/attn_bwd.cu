@@ -151,32 +151,23 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
 }
 
 // P^T for one key row (this thread) over this warpgroup's NC query columns col0 .. col0+NC:
-// p[r] = 2^(S^T * scale_log2 - lse2[col0 + r]), packed FFMA2 with the per-column -lse2 from
-// shared memory; kMasked zeroes columns outside [r_lo, nq) (causal diagonal / sequence end).
+// p[r] = 2^(S'^T * scale_log2). The UMMA already subtracted lse2[col] / scale_log2 from S^T
+// through the augmented K step (see DkvCfg), so no per-column operand is read here; kMasked
+// zeroes columns outside [r_lo, nq) (causal diagonal / sequence end).
 template <int NC, bool kMasked>
-__device__ __forceinline__ void dkv_p(const uint32_t (&sv)[NC / 32][32], const float* vs, float scale_log2, int col0,
-                                      int r_lo, int nq, float (&p)[NC]) {
+__device__ __forceinline__ void dkv_p(const uint32_t (&sv)[NC / 32][32], float scale_log2, int col0, int r_lo, int nq,
+                                      float (&p)[NC]) {
   const f2 sc = mk2(scale_log2, scale_log2);
 #pragma unroll
-  for (int p4 = 0; p4 < NC / 4; ++p4) {
-    // One 16-byte broadcast load per 4 columns: the shared-memory crossbar is shared with the
-    // UMMA operand reads, which saturate it.
-    const float4 nl = *reinterpret_cast<const float4*>(vs + col0 + 4 * p4);
-#pragma unroll
-    for (int hp = 0; hp < 2; ++hp) {
-      const int pe = 2 * p4 + hp;
-      const int r = 2 * pe;
-      const f2 nl2 = hp == 0 ? mk2(nl.x, nl.y) : mk2(nl.z, nl.w);
-      f2 e = ex2_pair(ffma2(mk2(__uint_as_float(sv[r / 32][r % 32]), __uint_as_float(sv[r / 32][r % 32 + 1])), sc,
-                            nl2),
-                      pe);
-      if (kMasked) {
-        e.x = (col0 + r < nq && col0 + r >= r_lo) ? e.x : 0.f;
-        e.y = (col0 + r + 1 < nq && col0 + r + 1 >= r_lo) ? e.y : 0.f;
-      }
-      p[r] = e.x;
-      p[r + 1] = e.y;
+  for (int pe = 0; pe < NC / 2; ++pe) {
+    const int r = 2 * pe;
+    f2 e = ex2_pair(fmul2(mk2(__uint_as_float(sv[r / 32][r % 32]), __uint_as_float(sv[r / 32][r % 32 + 1])), sc), pe);
+    if (kMasked) {
+      e.x = (col0 + r < nq && col0 + r >= r_lo) ? e.x : 0.f;
+      e.y = (col0 + r + 1 < nq && col0 + r + 1 >= r_lo) ? e.y : 0.f;
     }
+    p[r] = e.x;
+    p[r + 1] = e.y;
   }
 }
 
@@ -216,21 +207,65 @@ struct DkvCfg {
   static constexpr int kChunks = D / 64;
   static constexpr int kTileBytes = kChunks * kM * 128;  // K or V (128 key rows)
   static constexpr int kQBytes = kChunks * B * 128;      // Q_i or dO_i (B query rows)
-  static constexpr int kVecBytes = 2 * B * 4;            // lse2 + D for B rows
-  static constexpr int kSmemTiles = 2 * kTileBytes + kStages * (2 * kQBytes) + kStages * kVecBytes;
+  // Augmented K step (one extra UMMA K = 16 slice, SWIZZLE_NONE K-major: core matrix (8 rows x
+  // 16 B) (rg, kc) at rg * 256 + kc * 128). The key side holds (1, 1, 1, 0 ...) per key row, the
+  // query side the three-term bf16 split of -lse2 / scale_log2 (for S^T) or -D (for dP^T) per
+  // query row, so the UMMA produces S^T - lse2 / scale_log2 and dP^T - D directly and the
+  // math warps read no per-column vectors from shared memory (whose crossbar the SS UMMA
+  // operand reads saturate).
+  static constexpr int kAugOnesBytes = kM * 32;
+  static constexpr int kAugBytes = B * 32;
+  static constexpr int kSmemTiles = 2 * kTileBytes + kStages * (2 * kQBytes) + kAugOnesBytes + kStages * 2 * kAugBytes;
   static constexpr int kSt = 0, kDPt = B, kDV = 2 * B, kDK = 2 * B + D;
   static constexpr uint32_t kCols = pow2_cols(2 * B + 2 * D);
   static constexpr int kSmemBytes = kSmemTiles + 1024 + 256;
 };
 
+__device__ __forceinline__ uint64_t desc_aug(uint32_t saddr) {  // SWIZZLE_NONE, LBO 128, SBO 256
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(128u >> 4) << 16;
+  d |= static_cast<uint64_t>(256u >> 4) << 32;
+  d |= 1ull << 46;
+  return d;
+}
+
+// Byte offset of (row, k = 0) in an augmented slice; k = 0..3 are the 8 bytes from there.
+__device__ __forceinline__ int aug_off(int row) { return (row >> 3) * 256 + (row & 7) * 16; }
+
+// x -> three bf16 terms whose fp32 sum reproduces x to ~2^-24 relative, packed with a zero.
+__device__ __forceinline__ uint2 split3_bf16(float x) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(h);
+  const __nv_bfloat16 m = __float2bfloat16_rn(r1);
+  const __nv_bfloat16 l = __float2bfloat16_rn(r1 - __bfloat162float(m));
+  uint2 u;
+  u.x = static_cast<uint32_t>(__bfloat16_as_ushort(h)) | (static_cast<uint32_t>(__bfloat16_as_ushort(m)) << 16);
+  u.y = static_cast<uint32_t>(__bfloat16_as_ushort(l));
+  return u;
+}
+
 struct DkvBars {
   uint64_t kv_full, kv_empty;
-  uint64_t q_full[kStages], q_empty[kStages];
-  uint64_t st_full, dpt_full;  // UMMA -> softmax: S^T / dP^T in TMEM
-  uint64_t pt_full, dst_full;  // softmax -> UMMA: P^T / dS^T (bf16) in TMEM
+  uint64_t q_full[kStages], q_empty[kStages];    // Q_i (+ its augmented slice) ring
+  uint64_t do_full[kStages], do_empty[kStages];  // dO_i (+ its augmented slice) ring
+  uint64_t st_full, dpt_full;  // UMMA -> math: S^T / dP^T in TMEM
+  uint64_t st_free;            // math -> UMMA: S^T read into registers (the next S^T may overwrite)
+  uint64_t pds_full;           // math -> UMMA: P^T and dS^T (bf16) packed over dP^T's columns
   uint64_t acc_done;           // UMMA -> epilogue: the item's dV / dK are final
   uint32_t tmem_base;
 };
+
+// TMEM column (relative to dP^T) of the packed-bf16 P^T (dS^T: + 16) for UMMA K step kk.
+// Warpgroup hf owns query columns [hf * B/2, (hf + 1) * B/2) of dP^T; it writes chunk c2 (32
+// query columns) as P^T packed into columns c2 * 32 + [0, 16) and dS^T into c2 * 32 + [16, 32)
+// of its own range, i.e. over dP^T values it has already read.
+template <int B>
+__device__ __forceinline__ uint32_t pds_col(int kk) {
+  constexpr int kPerWg = B / 32;  // K steps (16 query columns) per warpgroup
+  const int hf = kk / kPerWg, r = kk % kPerWg;
+  return static_cast<uint32_t>(hf * (B / 2) + (r >> 1) * 32 + (r & 1) * 8);
+}
 
 struct KvItem {
   int hk, gj, s, jl, seq0, seq_len, e0, ne;
@@ -260,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     uint16_t* __restrict__ dv, const int32_t* __restrict__ order, int n_items, unsigned long long* trace) {
   using C = DkvCfg<D, B>;
   auto tr = [&](int slot, int g) {
-    if (trace != nullptr && blockIdx.x == 0 && g < 256) trace[g * 16 + slot] = clock64();
+    if (trace != nullptr && blockIdx.x == 0 && g < 256 && (threadIdx.x & 31) == 0) trace[g * 16 + slot] = clock64();
   };
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -269,29 +304,44 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
   uint8_t* v_smem = smem + C::kTileBytes;
   uint8_t* q_smem = smem + 2 * C::kTileBytes;            // [stage]
   uint8_t* do_smem = q_smem + kStages * C::kQBytes;      // [stage]
-  float* vec_smem = reinterpret_cast<float*>(do_smem + kStages * C::kQBytes);  // [stage][2][B]
+  uint8_t* ones_smem = do_smem + kStages * C::kQBytes;                  // augmented key side
+  uint8_t* qaug_smem = ones_smem + C::kAugOnesBytes;                    // [stage] -lse2 / scale_log2
+  uint8_t* daug_smem = qaug_smem + kStages * C::kAugBytes;              // [stage] -D
   DkvBars* bars = reinterpret_cast<DkvBars*>(smem + C::kSmemTiles);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbt = blk_off[nseq];
   const int grid = gridDim.x, cta = blockIdx.x;
   const int sg = hq / hsel;  // q heads per selection row
+  const float inv_scale_log2 = 1.0f / scale_log2;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->kv_full, 1);
     mbar_init(&bars->kv_empty, 1);
     for (int st = 0; st < kStages; ++st) {
-      mbar_init(&bars->q_full[st], 2);  // TMA expect_tx arrive + vector-copy arrive
+      mbar_init(&bars->q_full[st], 2);  // TMA expect_tx arrive + augmented-slice arrive
       mbar_init(&bars->q_empty[st], 1);
+      mbar_init(&bars->do_full[st], 2);
+      mbar_init(&bars->do_empty[st], 1);
     }
     mbar_init(&bars->st_full, 1);
     mbar_init(&bars->dpt_full, 1);
-    mbar_init(&bars->pt_full, 256);
-    mbar_init(&bars->dst_full, 256);
+    mbar_init(&bars->st_free, 256);
+    mbar_init(&bars->pds_full, 256);
     mbar_init(&bars->acc_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kCols>(&bars->tmem_base);
+  {
+    // Augmented slices: zero everything, then (1, 1, 1) in k = 0..2 of every key row.
+    uint4* z = reinterpret_cast<uint4*>(ones_smem);
+    for (int i = threadIdx.x; i < (C::kAugOnesBytes + kStages * 2 * C::kAugBytes) / 16; i += blockDim.x)
+      z[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    for (int r = threadIdx.x; r < kM; r += blockDim.x)
+      *reinterpret_cast<uint2*>(ones_smem + aug_off(r)) = make_uint2(0x3F803F80u, 0x00003F80u);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -334,9 +384,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         const uint32_t ph = (g / kStages) & 1;
         int h, gi;
         pair_of(w, m, h, gi);
+#ifdef SB_DKV_SAMEQ  // timing experiment only: every pair streams the same (L2-hot) Q / dO tile
+        h = 0;
+        gi = blk_off[w.s];
+#endif
         const int q0 = w.seq0 + (gi - blk_off[w.s]) * B;
         const int nq = min(B, w.seq_len - (gi - blk_off[w.s]) * B);
-        // -lse2 / -D of the pair's query rows: all loads in flight before the ring-slot wait.
+        // lse2 / D of the pair's query rows: all loads in flight before the ring-slot wait.
         float nl[B / 32], nd[B / 32];
 #pragma unroll
         for (int e = 0; e < B / 32; ++e) {
@@ -345,40 +399,62 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
           nl[e] = ok ? __ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
           nd[e] = ok ? __ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
         }
+        // Q and dO are separate rings: the UMMA releases Q_i after dK_i and dO_i after dV_i.
         if (lane == 0) tr(11, g);
         mbar_wait(&bars->q_empty[st], ph ^ 1);
         if (lane == 0) tr(12, g);
         if (lane == 0) {
-          mbar_expect_tx(&bars->q_full[st], 2 * C::kQBytes);
-          for (int c = 0; c < C::kChunks; ++c) {
+          mbar_expect_tx(&bars->q_full[st], C::kQBytes);
+          for (int c = 0; c < C::kChunks; ++c)
             tma_load_3d(q_smem + st * C::kQBytes + c * B * 128, &tm_q, &bars->q_full[st], c * 64, h, q0);
-            tma_load_3d(do_smem + st * C::kQBytes + c * B * 128, &tm_do, &bars->q_full[st], c * 64, h, q0);
-          }
         }
-        float* vs = vec_smem + st * 2 * B;
+        uint8_t* qa = qaug_smem + st * C::kAugBytes;
 #pragma unroll
-        for (int e = 0; e < B / 32; ++e) {
-          vs[e * 32 + lane] = -nl[e];
-          vs[B + e * 32 + lane] = -nd[e];
-        }
+        for (int e = 0; e < B / 32; ++e)
+          *reinterpret_cast<uint2*>(qa + aug_off(e * 32 + lane)) = split3_bf16(-nl[e] * inv_scale_log2);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> UMMA operand reads
         __syncwarp();
         if (lane == 0) tr(13, g);
         if (lane == 0) mbar_arrive(&bars->q_full[st]);
+        if (trace != nullptr && blockIdx.x == 0) {  // debug timeline only: Q tile landing time
+          mbar_wait(&bars->q_full[st], ph);
+          if (lane == 0) tr(14, g);
+        }
+        mbar_wait(&bars->do_empty[st], ph ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(&bars->do_full[st], C::kQBytes);
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_3d(do_smem + st * C::kQBytes + c * B * 128, &tm_do, &bars->do_full[st], c * 64, h, q0);
+        }
+        uint8_t* da = daug_smem + st * C::kAugBytes;
+#pragma unroll
+        for (int e = 0; e < B / 32; ++e)
+          *reinterpret_cast<uint2*>(da + aug_off(e * 32 + lane)) = split3_bf16(-nd[e]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->do_full[st]);
       }
       ++t;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ UMMA issuer
-    // Per pair m of an item (P^T / dS^T are in the softmax warps' registers before they are
-    // written back, so the next S^T / dP^T overwrite TMEM while the math of m proceeds):
-    //   St_m, dPt_m | [P^T_m] dV_m, St_{m+1} | [dS^T_m] dK_m, dPt_{m+1} | ...
-    if (lane == 0) {
+    // Flat pair stream g over all items. S^T_{g+1} is issued as soon as the math warps have
+    // read S^T_g (st_free), so it runs while they compute P_g / dS_g; P^T_g and dS^T_g come back
+    // packed over dP^T_g's columns:
+    //   St_g, dPt_g | [st_free_g] St_{g+1} | [pds_g] dV_g, dK_g, dPt_{g+1} | [st_free_{g+1}] ...
+    // The pipe then only waits on the short dS tail of the math, never on P.
+    {  // whole warp, converged; `leader` issues
+      const uint32_t leader = elect_one();
       constexpr uint32_t idesc_t = idesc_bf16_f32(kM, B, false, false);
       constexpr uint32_t idesc_acc = idesc_bf16_f32(kM, D, false, true);
       const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
       auto qa = [&](int gg) { return smem_u32(q_smem + (gg % kStages) * C::kQBytes); };
       auto da = [&](int gg) { return smem_u32(do_smem + (gg % kStages) * C::kQBytes); };
+      const uint32_t ones_addr = smem_u32(ones_smem);
+      auto qaug = [&](int gg) { return smem_u32(qaug_smem + (gg % kStages) * C::kAugBytes); };
+      auto daug = [&](int gg) { return smem_u32(daug_smem + (gg % kStages) * C::kAugBytes); };
       auto issue_st = [&](int gg) {
+        if (gg > 0) mbar_wait(&bars->st_free, (gg - 1) & 1);  // S^T_{gg-1} read out of TMEM
         tr(8, gg);
         mbar_wait(&bars->q_full[gg % kStages], (gg / kStages) & 1);
         tr(9, gg);
@@ -388,19 +464,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
           const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
           const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
           mma_ss(tmem + C::kSt, desc_sw128(k_addr + off_m, 16, 1024), desc_sw128(qa(gg) + off_n, 16, 1024), idesc_t,
-                 kk > 0);
+                 kk > 0, leader);
         }
-        tc_commit(&bars->st_full);
+        mma_ss(tmem + C::kSt, desc_aug(ones_addr), desc_aug(qaug(gg)), idesc_t, 1u, leader);  // - lse2 / scale_log2
+        tc_commit(&bars->st_full, leader);
       };
-      auto issue_dpt = [&](int gg) {  // q_full of gg already observed by issue_st(gg)
+      auto issue_dpt = [&](int gg) {
+        mbar_wait(&bars->do_full[gg % kStages], (gg / kStages) & 1);
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
           const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
           mma_ss(tmem + C::kDPt, desc_sw128(v_addr + off_m, 16, 1024), desc_sw128(da(gg) + off_n, 16, 1024), idesc_t,
-                 kk > 0);
+                 kk > 0, leader);
         }
-        tc_commit(&bars->dpt_full);
+        mma_ss(tmem + C::kDPt, desc_aug(ones_addr), desc_aug(daug(gg)), idesc_t, 1u, leader);  // - D
+        tc_commit(&bars->dpt_full, leader);
       };
       int g = 0, t = 0;
       for (int k = 0;; ++k) {
@@ -412,30 +492,30 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         mbar_wait(&bars->kv_full, t & 1);
         issue_st(g);
         issue_dpt(g);
+        if (items == 1) tc_commit(&bars->kv_empty, leader);  // last S^T / dP^T of the item issued
         for (int m = 0; m < items; ++m, ++g) {
+          if (m + 1 < items) issue_st(g + 1);
           tr(0, g);
-          mbar_wait(&bars->pt_full, g & 1);
+          mbar_wait(&bars->pds_full, g & 1);
           tr(1, g);
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < B / 16; ++kk)
-            mma_ts(tmem + C::kDV, tmem + C::kSt + packed_col<B>(kk), desc_sw128(da(g) + kk * 2048, B * 128, 1024), idesc_acc,
-                   (m > 0 || kk > 0) ? 1u : 0u);
-          if (m + 1 < items) issue_st(g + 1);
-          else tc_commit(&bars->kv_empty);  // K (last S^T) and V (last dP^T) no longer read
-          tr(2, g);
-          mbar_wait(&bars->dst_full, g & 1);
-          tr(3, g);
-          tc_fence_after();
+          for (int kk = 0; kk < B / 16; ++kk)  // dK first: Q_i is the ring the next S^T waits on
+            mma_ts(tmem + C::kDK, tmem + C::kDPt + pds_col<B>(kk) + 16, desc_sw128(qa(g) + kk * 2048, B * 128, 1024),
+                   idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
+          tc_commit(&bars->q_empty[g % kStages], leader);
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
-            mma_ts(tmem + C::kDK, tmem + C::kDPt + packed_col<B>(kk), desc_sw128(qa(g) + kk * 2048, B * 128, 1024), idesc_acc,
-                   (m > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(&bars->q_empty[g % kStages]);
+            mma_ts(tmem + C::kDV, tmem + C::kDPt + pds_col<B>(kk), desc_sw128(da(g) + kk * 2048, B * 128, 1024),
+                   idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
+          tc_commit(&bars->do_empty[g % kStages], leader);
           tr(10, g);
-          if (m + 1 < items) issue_dpt(g + 1);
+          if (m + 1 < items) {
+            issue_dpt(g + 1);
+            if (m + 2 == items) tc_commit(&bars->kv_empty, leader);  // K (last S^T) and V (last dP^T) no longer read
+          }
         }
-        tc_commit(&bars->acc_done);
+        tc_commit(&bars->acc_done, leader);
         ++t;
       }
     }
@@ -465,70 +545,60 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         const int nq = min(B, w.seq_len - il * B);
         // Valid query columns r: inside the sequence, and causal (key row c <= r) on the diagonal.
         const int r_lo = il == w.jl ? c : 0;
-        const float* vs = vec_smem + st * 2 * B;
-        mbar_wait(&bars->q_full[st], (g / kStages) & 1);  // producer's plain smem writes of vs
         mbar_wait(&bars->st_full, g & 1);
         if (threadIdx.x == 64) tr(4, g);
         tc_fence_after();
+#ifdef SB_DKV_NOMATH  // timing experiment only: UMMA stream without the math
+        mbar_arrive(&bars->st_free);
+        mbar_wait(&bars->dpt_full, g & 1);
+        mbar_arrive(&bars->pds_full);
+        continue;
+#endif
         float p[HB];
         {
           uint32_t sv[HB / 32][32];
 #pragma unroll
           for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(tmem + lf + st_col + c2 * 32, sv[c2]);
           tmem_wait_ld();
-          // vs[0..B) holds -lse2 of the item's query rows (producer negates).
+          tc_fence_before();
+          mbar_arrive(&bars->st_free);  // S^T_g is in registers: S^T_{g+1} may overwrite it
           if (r_lo <= hf * HB && nq == B) {
-            dkv_p<HB, false>(sv, vs, scale_log2, hf * HB, 0, B, p);
+            dkv_p<HB, false>(sv, scale_log2, hf * HB, 0, B, p);
           } else {
-            dkv_p<HB, true>(sv, vs, scale_log2, hf * HB, r_lo, nq, p);
+            dkv_p<HB, true>(sv, scale_log2, hf * HB, r_lo, nq, p);
           }
         }
-        {
-          uint32_t pw[HB / 2];
-#pragma unroll
-          for (int e = 0; e < HB / 2; ++e) pw[e] = pack_bf16x2(p[2 * e], p[2 * e + 1]);
-          if constexpr (HB == 64) {
-            tmem_st32(tmem + lf + st_col, pw);
-          } else {
-            tmem_st16(tmem + lf + st_col, pw);
-          }
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&bars->pt_full);
         if (threadIdx.x == 64) tr(5, g);
         mbar_wait(&bars->dpt_full, g & 1);
         if (threadIdx.x == 64) tr(6, g);
         tc_fence_after();
         {
-          // dP^T chunks software-pipelined: chunk c2+1 is in flight while c2 is processed.
+          // dP^T chunks software-pipelined: chunk c2+1 is in flight while c2 is processed; P^T and
+          // dS^T of chunk c2 are packed over chunk c2's own (already read) columns.
           uint32_t pv[2][32];
           tmem_ld32(tmem + lf + dpt_col, pv[0]);
           tmem_wait_ld();
 #pragma unroll
           for (int c2 = 0; c2 < HB / 32; ++c2) {
             if (c2 + 1 < HB / 32) tmem_ld32(tmem + lf + dpt_col + (c2 + 1) * 32, pv[(c2 + 1) & 1]);
-            uint32_t dd[16];
+            uint32_t pw[16], dd[16];
 #pragma unroll
-            for (int e = 0; e < 32; e += 4) {
+            for (int e = 0; e < 32; e += 2) {  // dS^T = P^T (dP^T - D): the UMMA already subtracted D
               const int r = c2 * 32 + e;
-              const float4 nd = *reinterpret_cast<const float4*>(vs + B + hf * HB + r);  // -D
-              const f2 ds0 = fmul2(mk2(p[r], p[r + 1]), fadd2(mk2(__uint_as_float(pv[c2 & 1][e]),
-                                                                   __uint_as_float(pv[c2 & 1][e + 1])),
-                                                               mk2(nd.x, nd.y)));
-              const f2 ds1 = fmul2(mk2(p[r + 2], p[r + 3]), fadd2(mk2(__uint_as_float(pv[c2 & 1][e + 2]),
-                                                                       __uint_as_float(pv[c2 & 1][e + 3])),
-                                                                   mk2(nd.z, nd.w)));
-              dd[e / 2] = pack_bf16x2(ds0.x, ds0.y);
-              dd[e / 2 + 1] = pack_bf16x2(ds1.x, ds1.y);
+              pw[e / 2] = pack_bf16x2(p[r], p[r + 1]);
+              const f2 ds = fmul2(mk2(p[r], p[r + 1]),
+                                  mk2(__uint_as_float(pv[c2 & 1][e]), __uint_as_float(pv[c2 & 1][e + 1])));
+              dd[e / 2] = pack_bf16x2(ds.x, ds.y);
             }
-            tmem_st16(tmem + lf + dpt_col + c2 * 16, dd);  // over columns already read
-            tmem_wait_ld();
+            tmem_st16(tmem + lf + dpt_col + c2 * 32, pw);
+            tmem_st16(tmem + lf + dpt_col + c2 * 32 + 16, dd);
+            if (c2 + 1 < HB / 32) tmem_wait_ld();
           }
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bars->dst_full);
+        mbar_arrive(&bars->pds_full);
+        if (threadIdx.x == 64) tr(7, g);
         if (threadIdx.x == 64) tr(7, g);
       }
       if (items > 0) {
@@ -609,8 +679,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
     const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off, int nseq, int hq, int hkv,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt, int hsel, int k_max,
     const float* __restrict__ lse2, const float* __restrict__ dvec, int tp, float scale, float scale_log2,
-    uint16_t* __restrict__ dq, const int32_t* __restrict__ order, int n_items) {
+    uint16_t* __restrict__ dq, const int32_t* __restrict__ order, int n_items, unsigned long long* trace) {
   using C = DqCfg<D, B>;
+  auto tr = [&](int slot, int g) {
+    if (trace != nullptr && blockIdx.x == 0 && g < 256 && (threadIdx.x & 31) == 0) trace[g * 16 + slot] = clock64();
+  };
   constexpr int kVS = C::kVStages;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -699,13 +772,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
           const int kv_row = w.seq0 + __ldg(w.list + j) * B;
           if (lane == 0) {
             const int st = g % kStages;
+            tr(12, g);
             mbar_wait(&bars->k_empty[st], ((g / kStages) & 1) ^ 1);
+            tr(13, g);
             mbar_expect_tx(&bars->k_full[st], C::kKVBytes);
             for (int c = 0; c < C::kChunks; ++c)
               tma_load_3d(k_smem + st * C::kKVBytes + c * B * 128, &tm_k, &bars->k_full[st], c * 64, hk, kv_row);
           } else {
             const int vst = g % kVS;
+            tr(14, g);
             mbar_wait(&bars->v_empty[vst], ((g / kVS) & 1) ^ 1);
+            tr(15, g);
             mbar_expect_tx(&bars->v_full[vst], C::kKVBytes);
             for (int c = 0; c < C::kChunks; ++c)
               tma_load_3d(v_smem + vst * C::kKVBytes + c * B * 128, &tm_v, &bars->v_full[vst], c * 64, hk, kv_row);
@@ -717,14 +794,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
   } else if (warp == 1) {
     // Global block stream g over all items: S_0, dP_0 | S_{g+1} (other S buffer) overlaps the
     // math of g | [dS_g] dQ_g, dP_{g+1} | ...  The next item's S / dP follow without a gap.
-    if (lane == 0) {
+    {  // whole warp, converged; `leader` issues
+      const uint32_t leader = elect_one();
       constexpr uint32_t idesc_s = idesc_bf16_f32(kM, B, false, false);
       constexpr uint32_t idesc_dq = idesc_bf16_f32(kM, D, false, true);
       const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
       auto s_col = [](int gg) { return (gg & 1) ? C::kS1 : C::kS0; };
       auto issue_s = [&](int gg, int qb) {
         const int st = gg % kStages;
+        tr(2, gg);
         mbar_wait(&bars->k_full[st], (gg / kStages) & 1);
+        tr(3, gg);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(q_smem + qb * C::kQBytes);
 #pragma unroll
@@ -732,13 +812,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
           const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
           const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
           mma_ss(tmem + s_col(gg), desc_sw128(q_addr + off_m, 16, 1024),
-                 desc_sw128(k_addr + st * C::kKVBytes + off_n, 16, 1024), idesc_s, kk > 0);
+                 desc_sw128(k_addr + st * C::kKVBytes + off_n, 16, 1024), idesc_s, kk > 0, leader);
         }
-        tc_commit(&bars->s_full[gg & 1]);
+        tc_commit(&bars->s_full[gg & 1], leader);
       };
       auto issue_dp = [&](int gg, int qb, bool last_of_item) {
         const int vst = gg % kVS;
+        tr(4, gg);
         mbar_wait(&bars->v_full[vst], (gg / kVS) & 1);
+        tr(5, gg);
         tc_fence_after();
         const uint32_t do_addr = smem_u32(do_smem + qb * C::kQBytes);
 #pragma unroll
@@ -746,11 +828,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
           const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
           const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
           mma_ss(tmem + C::kDP, desc_sw128(do_addr + off_m, 16, 1024),
-                 desc_sw128(v_addr + vst * C::kKVBytes + off_n, 16, 1024), idesc_s, kk > 0);
+                 desc_sw128(v_addr + vst * C::kKVBytes + off_n, 16, 1024), idesc_s, kk > 0, leader);
         }
-        tc_commit(&bars->dp_full);
-        tc_commit(&bars->v_empty[vst]);
-        if (last_of_item) tc_commit(&bars->qdo_empty[qb]);  // last S (earlier) and dP of the item
+        tc_commit(&bars->dp_full, leader);
+        tc_commit(&bars->v_empty[vst], leader);
+        if (last_of_item) tc_commit(&bars->qdo_empty[qb], leader);  // last S (earlier) and dP of the item
       };
       // Flattened stream: for each block g know (item q, local j, item length n).
       int g = 0, q = 0;
@@ -794,7 +876,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
               issue_s(g + 1, qb ^ 1);
             }
           }
+          tr(0, g);
           mbar_wait(&bars->ds_full, g & 1);
+          tr(1, g);
           tc_fence_after();
           if (j == 0) mbar_wait(&bars->dq_free, (q & 1) ^ 1);  // previous item's dQ read out
           const int st = g % kStages;
@@ -802,9 +886,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
           for (int kk = 0; kk < B / 16; ++kk)
             mma_ts(tmem + C::kDQ, tmem + s_col(g) + packed_col<B>(kk),
                    desc_sw128(k_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024), idesc_dq,
-                   (j > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(&bars->k_empty[st]);
-          if (last) tc_commit(&bars->dq_done);
+                   (j > 0 || kk > 0) ? 1u : 0u, leader);
+          tc_commit(&bars->k_empty[st], leader);
+          tr(6, g);
+          if (last) tc_commit(&bars->dq_done, leader);
           if (!last) {
             issue_dp(g + 1, qb, j + 2 == n);
           } else if (have_next) {
@@ -851,6 +936,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         const int lim = valid ? min(key_lim, jb == w.i ? r + 1 : B) : 0;
         const uint32_t s_col = ((g & 1) ? C::kS1 : C::kS0) + hf * HB;
         mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
+        if (threadIdx.x == 64) tr(8, g);
         tc_fence_after();
         float p[HB];
         {
@@ -864,7 +950,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
             dq_p<HB, true>(sv, -l2, scale_log2, hf * HB, lim, p);
           }
         }
+        if (threadIdx.x == 64) tr(9, g);
         mbar_wait(&bars->dp_full, g & 1);
+        if (threadIdx.x == 64) tr(10, g);
         tc_fence_after();
         {
           const uint32_t dp_col = C::kDP + hf * HB;
@@ -890,6 +978,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->ds_full);
+        if (threadIdx.x == 64) tr(11, g);
       }
       mbar_wait(&bars->dq_done, q & 1);
       tc_fence_after();
@@ -928,6 +1017,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
 // ------------------------------------------------------------------------------------ host
 constexpr int kMaxKvCost = 4096;
 unsigned long long* g_trace_bwd = nullptr;  // debug timeline buffer (sb_debug_set_trace_bwd)
+unsigned long long* g_trace_dq = nullptr;   // debug timeline buffer (sb_debug_set_trace_dq)
 
 struct BwdWorkspace {
   size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, total;
@@ -1016,7 +1106,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
                "sb_sparse_attn_bwd: smem attribute (dq)");
     kern<<<std::min(q_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, cu, blk_off, nseq, hq, hkv, idx,
                                                                   cnt, hsel, k_max, lse2, dvec, w.tp, scale,
-                                                                  scale_log2, dq, order_q, q_items);
+                                                                  scale_log2, dq, order_q, q_items, g_trace_dq);
     launched("sb_sparse_attn_bwd/dq");
   }
 }
@@ -1026,6 +1116,8 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
 
 // Debug only: device buffer of 256 x 16 uint64 for CTA 0 of the dK/dV pass (NULL disables).
 SB_API void sb_debug_set_trace_bwd(unsigned long long* buf) { sbk::g_trace_bwd = buf; }
+// Debug only: the same for CTA 0 of the dQ pass.
+SB_API void sb_debug_set_trace_dq(unsigned long long* buf) { sbk::g_trace_dq = buf; }
 
 SB_API size_t sb_sparse_attn_bwd_workspace_size(int total_tokens, int nb_total, int hq, int hkv, int head_dim, int hsel,
                                                 int k_max) {

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
   using C = FwdCfg<D, B>;
   // Debug timeline (sb_debug_set_trace): CTA 0 records clock64 at phase boundaries.
   auto tr = [&](int slot, int g) {
-    if (trace != nullptr && blockIdx.x == 0 && g < 256) trace[g * 8 + slot] = clock64();
+    if (trace != nullptr && blockIdx.x == 0 && g < 256 && (threadIdx.x & 31) == 0) trace[g * 8 + slot] = clock64();
   };
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
     produce(false);
   } else if (warp == 1) {
     // ------------------------------------------------------------ UMMA issuer
-    if (lane == 0) {
+    {  // whole warp, converged; `leader` issues
+      const uint32_t leader = elect_one();
       constexpr uint32_t idesc_qk = idesc_bf16_f32(kM, B, false, false);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(kM, D, false, true);
       const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
@@ -245,10 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
 #pragma unroll
         for (int kk = 0; kk < B / 16; ++kk) {
           const uint64_t b = desc_sw128(v_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024);
-          mma_ts(o_tmem, p_tmem + kk * 8, b, idesc_pv, (pv_j > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(o_tmem, p_tmem + kk * 8, b, idesc_pv, (pv_j > 0 || kk > 0) ? 1u : 0u, leader);
         }
-        tc_commit(&bars->v_empty[st]);
-        tc_commit(&bars->o_done);
+        tc_commit(&bars->v_empty[st], leader);
+        tc_commit(&bars->o_done, leader);
       };
       int g = 0, q = 0;
       for (int k = 0;; ++k) {
@@ -271,11 +272,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
             const uint32_t koff = (kk & 3) * 32;  // 16 bf16 = 32 B inside the swizzle atom
             const uint64_t a = desc_sw128(q_addr + (kk >> 2) * (kM * 128) + koff, 16, 1024);
             const uint64_t b = desc_sw128(k_addr + st * C::kKVBytes + (kk >> 2) * (B * 128) + koff, 16, 1024);
-            mma_ss(d_s, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+            mma_ss(d_s, a, b, idesc_qk, kk > 0 ? 1u : 0u, leader);
           }
-          tc_commit(&bars->s_full[g & 1]);
-          tc_commit(&bars->k_empty[st]);
-          if (j == w.n - 1) tc_commit(&bars->q_empty[qb]);
+          tc_commit(&bars->s_full[g & 1], leader);
+          tc_commit(&bars->k_empty[st], leader);
+          if (j == w.n - 1) tc_commit(&bars->q_empty[qb], leader);
           if (pv_g >= 0) issue_pv();
           pv_g = g;
           pv_j = j;

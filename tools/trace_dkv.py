@@ -23,18 +23,18 @@ t = buf.cpu().numpy().reshape(256, 16).astype(np.int64)
 n = int((t[:, 0] > 0).sum())
 r = slice(2, n - 2)
 print("pairs traced", n)
-print("median period (pt wait start -> next):", np.median(np.diff(t[r, 0])))
-print("median pt_full wait (MMA):", np.median(t[r, 1] - t[r, 0]))
-print("median dV issue + St issue (pt seen -> before dst wait):", np.median(t[r, 2] - t[r, 1]))
-print("median dst_full wait (MMA):", np.median(t[r, 3] - t[r, 2]))
-print("median dK issue + dPt issue (dst seen -> next pt wait):", np.median(t[3:n-1, 0] - t[2:n-2, 3]))
-print("softmax: st seen -> P stored:", np.median(t[r, 5] - t[r, 4]))
-print("softmax: P stored -> dpt seen:", np.median(t[r, 6] - t[r, 5]))
-print("softmax: dpt seen -> dS stored:", np.median(t[r, 7] - t[r, 6]))
-print("softmax: dS stored -> next st seen:", np.median(t[3:n-1, 4] - t[2:n-2, 7]))
-print("UMMA: q_full wait in issue_st:", np.median(t[3:n-1, 9] - t[3:n-1, 8]))
-print("UMMA: dV issue (pt seen -> issue_st start):", np.median(t[3:n-1, 8] - t[2:n-2, 1]))
-print("UMMA: dK issue (dst seen -> after q_empty commit):", np.median(t[r, 10] - t[r, 3]))
-print("producer: q_empty wait:", np.median(t[r, 12] - t[r, 11]))
-print("producer: lead of q_full arrive over its use:", np.median(t[3:n-1, 8] - t[3:n-1, 13]))
-print("producer: TMA+vec issue time:", np.median(t[r, 13] - t[r, 12]))
+med = lambda x: float(np.median(x))
+nx = slice(3, n - 1)
+print("period (pds wait start -> next):", med(np.diff(t[2:n - 1, 0])))
+print("UMMA: pds wait:", med(t[r, 1] - t[r, 0]))
+print("UMMA: dV + dK issue:", med(t[r, 10] - t[r, 1]))
+print("UMMA: q_full wait in issue_st:", med(t[r, 9] - t[r, 8]))
+print("math: st seen -> P done:", med(t[r, 5] - t[r, 4]))
+print("math: dpt wait:", med(t[r, 6] - t[r, 5]))
+print("math: dpt seen -> pds arrive:", med(t[r, 7] - t[r, 6]))
+print("math: pds arrive -> next st seen:", med(t[nx, 4] - t[r, 7]))
+print("producer: q_empty wait:", med(t[r, 12] - t[r, 11]))
+print("producer: lead of q_full arrive over its use:", med(t[r, 8] - t[r, 13]))
+print("producer: Q TMA issue -> landed:", med(t[r, 14] - t[r, 12]))
+print("producer: Q landed -> St issue start:", med(t[r, 8] - t[r, 14]))
+print("UMMA: issue_st start -> St issued (incl. waits):", med(t[r, 9] - t[r, 8]))

@@ -5,17 +5,57 @@
 #include "../paper_2604_13847_b200/csrc/kernels/sm100.cuh"
 using namespace sbk::sm100;
 
-__global__ void __launch_bounds__(320, 1) bench(int mode, int iters, int nwarps_ld, unsigned long long* out) {
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(p));
+  return p != 0;
+}
+
+// Descriptor-lo variant: hi word (SBO, version, layout) and idesc are compile-time immediates.
+template <uint32_t AHI, uint32_t BHI, uint32_t IDESC>
+__device__ __forceinline__ void mma_ss_lo(uint32_t d, uint32_t alo, uint32_t blo, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .b64 a, b;\n\t.reg .pred p;\n\tmov.b64 a, {%1, %4};\n\tmov.b64 b, {%2, %5};\n\t"
+      "setp.ne.b32 p, %3, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, p;\n\t}" ::"r"(d),
+      "r"(alo), "r"(blo), "r"(acc), "n"(AHI), "n"(BHI), "n"(IDESC)
+      : "memory");
+}
+template <uint32_t BHI, uint32_t IDESC>
+__device__ __forceinline__ void mma_ts_lo(uint32_t d, uint32_t a_tmem, uint32_t blo, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .b64 b;\n\t.reg .pred p;\n\tmov.b64 b, {%2, %4};\n\t"
+      "setp.ne.b32 p, %3, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], [%1], b, %5, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "r"(blo), "r"(acc), "n"(BHI), "n"(IDESC)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_ss_p(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc, uint32_t leader) {
+  asm volatile(
+      "{\n\t.reg .pred p, l;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 l, %5, 0;\n\t"
+      "@l tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(leader)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(320, 1) bench(int mode, int iters, int nwarps_ld, unsigned long long* out,
+                                                const uint8_t* src) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;
+  __shared__ volatile int mma_done;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); mma_done = 0; fence_barrier_init(); }
   if (warp == 1) tmem_alloc<512>(&tmem_base);
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tmem = tmem_base;
-  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) {
+    uint32_t x = (i + 1) * 2654435761u ^ (blockIdx.x * 40503u);
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    // random bf16 pairs in [-2, 2) when mode >= 100 (random operands), else 1.0
+    reinterpret_cast<uint32_t*>(smem)[i] = mode >= 100 ? ((x & 0x807F807Fu) | 0x3F003F00u) : 0x3c003c00u;
+  }
+  if (mode >= 100) mode -= 100;
   __syncthreads();
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
@@ -119,6 +159,266 @@ __global__ void __launch_bounds__(320, 1) bench(int mode, int iters, int nwarps_
       t1 = clock64();
       out[2] = t1 - t0;
     }
+  } else if (mode == 11) {  // SS MMA N=128 while warp 3 streams bulk copies (nwarps_ld x 8 KB in flight) into smem
+    if (threadIdx.x == 32) {
+      const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+      const uint32_t idesc = idesc_bf16_f32(128, 128, false, false);
+      for (int i = 0; i < iters; ++i)
+        mma_ss(tmem, desc_sw128(a + (i & 3) * 32, 16, 1024), desc_sw128(b + (i & 3) * 32, 16, 1024), idesc, i > 0);
+      tc_commit(&bar);
+      mbar_wait(&bar, 0);
+      t1 = clock64();
+      out[2] = t1 - t0;
+      mma_done = 1;
+    } else if (threadIdx.x == 96 && nwarps_ld > 0) {
+      unsigned long long bytes = 0;
+      uint32_t ph = 0;
+      for (int r = 0; !mma_done; ++r) {
+        mbar_expect_tx(&bar2, nwarps_ld * 8192);
+        for (int c = 0; c < nwarps_ld; ++c)
+          bulk_load(smem + 65536 + c * 8192, src + ((r * nwarps_ld + c) % 512) * 8192, 8192, &bar2);
+        mbar_wait(&bar2, ph);
+        ph ^= 1;
+        bytes += nwarps_ld * 8192;
+      }
+      out[3] = bytes;
+    }
+  } else if (mode == 12) {  // SS MMA N=128 while nwarps_ld warps issue broadcast LDS.128 (one per 4 FMAs)
+    if (threadIdx.x == 32) {
+      const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+      const uint32_t idesc = idesc_bf16_f32(128, 128, false, false);
+      for (int i = 0; i < iters; ++i)
+        mma_ss(tmem, desc_sw128(a + (i & 3) * 32, 16, 1024), desc_sw128(b + (i & 3) * 32, 16, 1024), idesc, i > 0);
+      tc_commit(&bar);
+      mbar_wait(&bar, 0);
+      t1 = clock64();
+      out[2] = t1 - t0;
+      mma_done = 1;
+    } else if (warp >= 2 && warp < 2 + nwarps_ld) {
+      const float4* src4 = reinterpret_cast<const float4*>(smem + 65536);
+      float acc = 0.f;
+      unsigned long long n = 0;
+      while (!mma_done) {
+#pragma unroll 8
+        for (int e = 0; e < 64; ++e) {
+          const float4 v = src4[e];
+          acc += v.x * v.y + v.z * v.w;
+        }
+        n += 64;
+      }
+      if (acc == 1234.5f) out[1] = n;
+      if (lane == 0) atomicAdd(out + 3, n);
+    }
+  } else if (mode == 13 || mode == 19) {  // dK/dV pass MMA mix per pair: 8 TS (dV) + 8 SS (St) + 8 TS (dK) + 8 SS (dPt); 19: + commits
+    if (threadIdx.x == 32) {
+      const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+      const uint32_t idesc_ss = idesc_bf16_f32(128, 128, false, false);
+      const uint32_t idesc_ts = idesc_bf16_f32(128, 128, false, true);
+      for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem, tmem + 256 + (kk & 3) * 8, desc_sw128(b + (kk & 7) * 2048, 128 * 128, 1024), idesc_ts, 1u);
+        if (mode == 19) tc_commit(&bar2);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ss(tmem + 256, desc_sw128(a + (kk & 3) * 32, 16, 1024), desc_sw128(b + (kk & 3) * 32, 16, 1024), idesc_ss,
+                 kk > 0);
+        if (mode == 19) tc_commit(&bar2);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + 128, tmem + 384 + (kk & 3) * 8, desc_sw128(b + (kk & 7) * 2048, 128 * 128, 1024), idesc_ts, 1u);
+        if (mode == 19) tc_commit(&bar2);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ss(tmem + 384, desc_sw128(a + (kk & 3) * 32, 16, 1024), desc_sw128(b + (kk & 3) * 32, 16, 1024), idesc_ss,
+                 kk > 0);
+        if (mode == 19) tc_commit(&bar2);
+      }
+      tc_commit(&bar);
+      mbar_wait(&bar, 0);
+      t1 = clock64();
+      atomicMax(out + 2, t1 - t0);
+      mma_done = 1;
+    } else if (warp >= 2 && warp < 2 + nwarps_ld) {
+      const uint32_t lf = static_cast<uint32_t>((warp & 3) * 32) << 16;
+      const uint32_t col = 256 + ((warp - 2) / 4) * 64;
+      uint32_t acc = 0;
+      unsigned long long n = 0;
+      while (!mma_done) {
+        uint32_t v[2][32];
+        tmem_ld32(tmem + lf + col, v[0]);
+        tmem_ld32(tmem + lf + col + 32, v[1]);
+        tmem_wait_ld();
+        uint32_t w[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) w[e] = v[0][e] ^ v[1][e + 16];
+        tmem_st16(tmem + lf + col + 128, w);
+        tmem_st16(tmem + lf + col + 144, w);
+        tmem_wait_st();
+        acc ^= v[0][3];
+        ++n;
+      }
+      if (acc == 0xdeadbeef) out[1] = acc;
+      if (lane == 0) atomicAdd(out + 3, n);
+    }
+  } else if (mode == 15 || mode == 16) {  // dK/dV MMA mix while 8 warps run ALU/MUFU work; 16: warp-wide issuer
+    const bool issuer = mode == 15 ? threadIdx.x == 32 : warp == 1;
+    if (issuer) {
+      const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+      const uint32_t idesc_ss = idesc_bf16_f32(128, 128, false, false);
+      const uint32_t idesc_ts = idesc_bf16_f32(128, 128, false, true);
+      const uint64_t da0 = desc_sw128(a, 16, 1024), db0 = desc_sw128(b, 16, 1024), dbm = desc_sw128(b, 128 * 128, 1024);
+      for (int i = 0; i < iters; ++i) {
+        const uint32_t sel = (i & 1) * 0;  // keep descriptors data-dependent on the loop like the kernel
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          if (mode == 15 || elect_one()) mma_ts(tmem, tmem + 256 + (kk & 3) * 8, dbm + (((kk & 7) * 2048 + sel) >> 4), idesc_ts, 1u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          if (mode == 15 || elect_one()) mma_ss(tmem + 256, da0 + ((kk & 3) * 2), db0 + ((kk & 3) * 2), idesc_ss, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          if (mode == 15 || elect_one()) mma_ts(tmem + 128, tmem + 384 + (kk & 3) * 8, dbm + (((kk & 7) * 2048) >> 4), idesc_ts, 1u);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          if (mode == 15 || elect_one()) mma_ss(tmem + 384, da0 + ((kk & 3) * 2), db0 + ((kk & 3) * 2), idesc_ss, kk > 0);
+      }
+      if (mode == 15 || elect_one()) tc_commit(&bar);
+      mbar_wait(&bar, 0);
+      t1 = clock64();
+      if (lane == 0) atomicMax(out + 2, t1 - t0);
+      mma_done = 1;
+    } else if (warp >= 2 && warp < 2 + nwarps_ld) {
+      float x0 = lane, x1 = lane + 1, x2 = lane + 2, x3 = lane + 3;
+      unsigned long long n = 0;
+      while (!mma_done) {
+#pragma unroll 16
+        for (int e = 0; e < 64; ++e) {
+          x0 = fmaf(x0, 0.999f, 0.001f); x1 = exp2f(x1 * -0.5f); x2 = fmaf(x2, x1, x0); x3 = fmaf(x3, x2, 0.5f);
+        }
+        ++n;
+      }
+      if (x0 + x1 + x2 + x3 == 1234.5f) out[1] = n;
+      if (lane == 0) atomicAdd(out + 3, n);
+    }
+  } else if (mode == 17 || mode == 18) {  // kernel-like: stage-dependent descriptors; 17 = desc_sw128, 18 = lo-only
+    if (threadIdx.x == 32) {
+      const uint32_t a = smem_u32(smem), b0 = smem_u32(smem + 32768);
+      constexpr uint32_t idesc_ss = idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_ts = idesc_bf16_f32(128, 128, false, true);
+      constexpr uint32_t HI = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO | version | SW128 (bits 32..63)
+      for (int i = 0; i < iters; ++i) {
+        const uint32_t b = b0 + (i & 1) * 16384;
+        if (mode == 17) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tmem, tmem + 256 + (kk & 3) * 8, desc_sw128(b + kk * 2048, 128 * 64, 1024), idesc_ts, 1u);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss(tmem + 256, desc_sw128(a + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024),
+                   desc_sw128(b + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_ss, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tmem + 128, tmem + 384 + (kk & 3) * 8, desc_sw128(b + kk * 2048, 128 * 64, 1024), idesc_ts, 1u);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss(tmem + 384, desc_sw128(a + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024),
+                   desc_sw128(b + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_ss, kk > 0);
+        } else {
+          const uint32_t alo = ((a >> 4) & 0x3FFFu) | (1u << 16);
+          const uint32_t blo = ((b >> 4) & 0x3FFFu) | (1u << 16);
+          const uint32_t bmlo = ((b >> 4) & 0x3FFFu) | ((128u * 64u >> 4) << 16);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) mma_ts_lo<HI, idesc_ts>(tmem, tmem + 256 + (kk & 3) * 8, bmlo + kk * 128, 1u);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss_lo<HI, HI, idesc_ss>(tmem + 256, alo + (kk >> 2) * 512 + (kk & 3) * 2, blo + (kk >> 2) * 512 + (kk & 3) * 2,
+                                        kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) mma_ts_lo<HI, idesc_ts>(tmem + 128, tmem + 384 + (kk & 3) * 8, bmlo + kk * 128, 1u);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss_lo<HI, HI, idesc_ss>(tmem + 384, alo + (kk >> 2) * 512 + (kk & 3) * 2, blo + (kk >> 2) * 512 + (kk & 3) * 2,
+                                        kk > 0);
+        }
+      }
+      tc_commit(&bar);
+      mbar_wait(&bar, 0);
+      t1 = clock64();
+      atomicMax(out + 2, t1 - t0);
+      mma_done = 1;
+    } else if (warp >= 2 && warp < 2 + nwarps_ld) {
+      float x0 = lane, x1 = lane + 1, x2 = lane + 2, x3 = lane + 3;
+      unsigned long long n = 0;
+      while (!mma_done) {
+#pragma unroll 16
+        for (int e = 0; e < 64; ++e) {
+          x0 = fmaf(x0, 0.999f, 0.001f); x1 = exp2f(x1 * -0.5f); x2 = fmaf(x2, x1, x0); x3 = fmaf(x3, x2, 0.5f);
+        }
+        ++n;
+      }
+      if (x0 + x1 + x2 + x3 == 1234.5f) out[1] = n;
+      if (lane == 0) atomicAdd(out + 3, n);
+    }
+  } else if (mode == 20) {  // cost of mbar_wait on an already-completed phase; MMA issue timestamps
+    if (threadIdx.x == 32) {
+      mbar_arrive(&bar2);  // completes phase 0 of bar2 (count 1)
+      mbar_wait(&bar2, 0);
+      unsigned long long a0 = clock64();
+      for (int i = 0; i < 64; ++i) mbar_wait(&bar2, 0);
+      unsigned long long a1 = clock64();
+      out[0] = (a1 - a0) / 64;
+      const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+      const uint32_t idesc = idesc_bf16_f32(128, 128, false, false);
+      unsigned long long ts[24];
+#pragma unroll
+      for (int i = 0; i < 24; ++i) {
+        mma_ss(tmem, desc_sw128(a + (i & 3) * 32, 16, 1024), desc_sw128(b + (i & 3) * 32, 16, 1024), idesc, i > 0);
+        ts[i] = clock64();
+      }
+      tc_commit(&bar);
+      mbar_wait(&bar, 0);
+      t1 = clock64();
+      out[2] = t1 - ts[0];
+      for (int i = 0; i < 24; ++i) printf("mma issue %2d at %6llu\n", i, ts[i] - a1);
+      printf("mbar_wait on completed phase: %llu cycles each\n", out[0]);
+    }
+  } else if (mode == 21) {  // warp-converged issuer: leader predicate inside the asm, no per-MMA elect
+    if (warp == 1) {
+      const uint32_t leader = elect_one() ? 1u : 0u;
+      const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+      const uint32_t idesc = idesc_bf16_f32(128, 128, false, false);
+      unsigned long long ts[24];
+      const unsigned long long a1 = clock64();
+#pragma unroll
+      for (int i = 0; i < 24; ++i) {
+        mma_ss_p(tmem, desc_sw128(a + (i & 3) * 32, 16, 1024), desc_sw128(b + (i & 3) * 32, 16, 1024), idesc, i > 0, leader);
+        ts[i] = clock64();
+      }
+      if (leader) tc_commit(&bar);
+      mbar_wait(&bar, 0);
+      if (leader) for (int i = 0; i < 24; ++i) printf("conv issue %2d at %6llu\n", i, ts[i] - a1);
+      // throughput: iters x the dK/dV mix
+      const uint32_t idesc_ts = idesc_bf16_f32(128, 128, false, true);
+      unsigned long long b0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        const uint32_t bb = smem_u32(smem + 32768) + (it & 1) * 16384;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ss_p(tmem + 256, desc_sw128(a + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024),
+                   desc_sw128(bb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc, kk > 0, leader);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ss_p(tmem + 384, desc_sw128(a + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024),
+                   desc_sw128(bb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc, kk > 0, leader);
+      }
+      if (leader) tc_commit(&bar);
+      mbar_wait(&bar, 1);
+      t1 = clock64();
+      if (leader) out[2] = t1 - b0;
+      (void)idesc_ts;
+    }
   } else if (mode == 2) {  // tcgen05.ld bandwidth: nwarps_ld warps read 128 columns each, iters times
     if (warp >= 2 && warp < 2 + nwarps_ld) {
       const uint32_t lf = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -158,12 +458,18 @@ __global__ void __launch_bounds__(320, 1) bench(int mode, int iters, int nwarps_
 
 int main() {
   unsigned long long* d; cudaMalloc(&d, 32);
+  uint8_t* src; cudaMalloc(&src, 512 * 8192); cudaMemset(src, 0, 512 * 8192);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  int grid = 1;
   auto run = [&](int mode, int iters, int nw, const char* name, double bytes_or_flop, const char* unit) {
     cudaMemset(d, 0, 32);
-    bench<<<1, 320, 100 * 1024>>>(mode, iters, nw, d);
+    bench<<<grid, 320, 100 * 1024>>>(mode, iters, nw, d, src);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long c = 0; cudaMemcpy(&c, d + 2, 8, cudaMemcpyDeviceToHost);
+    unsigned long long by = 0; cudaMemcpy(&by, d + 3, 8, cudaMemcpyDeviceToHost);
+    if (mode == 13) printf("   (math-warp TMEM ld/st rounds per cycle: %.4f)\n", double(by) / c);
+    if (mode == 12) printf("   (LDS.128 warp-instr per cycle during MMA: %.3f)\n", double(by) / c);
+    if (mode == 11) printf("   (bulk bytes/cycle during MMA: %.1f)\n", double(by) / c);
     printf("%-40s iters=%6d warps=%d cycles=%10llu  %.1f %s/cycle  (%s)\n", name, iters, nw, c, bytes_or_flop / c, unit,
            cudaGetErrorString(e));
   };
@@ -175,6 +481,21 @@ int main() {
   for (int it : {512, 4096}) run(8, it, 0, "SS MMA 128x256x16", 2.0 * 128 * 256 * 16 * it, "FLOP");
   for (int it : {64, 512}) run(9, it, 0, "8 TS + 8 SS overwriting TS A (WAR)", 2.0 * 128 * 128 * 16 * 16 * it, "FLOP");
   for (int it : {64, 512}) run(10, it, 0, "8 TS + 8 SS, disjoint", 2.0 * 128 * 128 * 16 * 16 * it, "FLOP");
+  for (int nw : {0, 1, 2, 4}) run(11, 4096, nw, "SS MMA 128x128x16 + bulk copies", 2.0 * 128 * 128 * 16 * 4096, "FLOP");
+  for (int nw : {0, 2, 4, 8}) run(12, 4096, nw, "SS MMA 128x128x16 + LDS.128 bcast", 2.0 * 128 * 128 * 16 * 4096, "FLOP");
+  for (int nw : {0, 8}) run(13, 256, nw, "dK/dV mix: 32 MMAs per pair", 2.0 * 128 * 128 * 16 * 32 * 256, "FLOP");
+  run(20, 1, 0, "issue timing", 1.0, "x");
+  run(21, 256, 0, "converged issuer, 16 SS per iter", 2.0 * 128 * 128 * 16 * 16 * 256, "FLOP");
+  run(19, 256, 0, "dK/dV mix + commit per group", 2.0 * 128 * 128 * 16 * 32 * 256, "FLOP");
+  for (int nw : {0, 8}) run(15, 256, nw, "dK/dV mix + ALU warps, lane issuer", 2.0 * 128 * 128 * 16 * 32 * 256, "FLOP");
+  for (int nw : {0, 8}) run(16, 256, nw, "dK/dV mix + ALU warps, warp issuer", 2.0 * 128 * 128 * 16 * 32 * 256, "FLOP");
+  for (int nw : {0, 8}) run(17, 256, nw, "kernel-like descs (desc_sw128) + ALU", 2.0 * 128 * 128 * 16 * 32 * 256, "FLOP");
+  for (int nw : {0, 8}) run(18, 256, nw, "kernel-like descs (lo-only) + ALU", 2.0 * 128 * 128 * 16 * 32 * 256, "FLOP");
+  grid = 148;
+  for (int it : {4096, 16384}) run(113, it, 0, "dK/dV mix, 148 CTAs, RANDOM operands", 2.0 * 128 * 128 * 16 * 32 * it, "FLOP");
+  for (int it : {256, 4096}) run(13, it, 0, "dK/dV mix, 148 CTAs (per-SM rate)", 2.0 * 128 * 128 * 16 * 32 * it, "FLOP");
+  for (int it : {4096}) run(0, it * 8, 0, "SS MMA 128x128x16, 148 CTAs", 2.0 * 128 * 128 * 16 * it * 8, "FLOP");
+  grid = 1;
   for (int nw : {0, 4, 8}) run(5, 4096, nw, "TS MMA 128x128x16 + ld warps", 2.0 * 128 * 128 * 16 * 4096, "FLOP");
   for (int nw : {4, 8}) for (int it : {64, 1024}) run(2, it, nw, "tcgen05.ld 32x32b.x32 (128 cols)", 1.0 * nw * 32 * 128 * 4 * it, "B");
   for (int nw : {4, 8}) for (int it : {64, 1024}) run(3, it, nw, "tcgen05.st 32x32b.x32 (64 cols)", 1.0 * nw * 32 * 64 * 4 * it, "B");
