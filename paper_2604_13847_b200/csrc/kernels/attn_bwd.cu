@@ -650,27 +650,41 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
 }
 
 // ------------------------------------------------------------------------------------ dq
-// Persistent over (q head, q block) items longest-first. Per item Q / dO (double-buffered
-// across items) stay resident and the selected K_j / V_j stream through rings.
-// TMEM: S0 | S1 | dP | dQ (S double-buffered so S_{j+1} overlaps the math of j).
+// Persistent over (q head, q block) items longest-first. Q_i / dO_i of the item live in TMEM
+// as the A operands of S = Q K^T and dP = dO V^T: the producer stages them in shared memory
+// with TMA and the UMMA warp moves them in with tcgen05.cp, in order behind the previous item's
+// last S / dP, so the staging buffer is free to prefetch the next item at once. Shared memory
+// is then K / V rings only.
+//   TMEM: S | dP | dQ | Q (packed) | dO (packed).
+//   Flat block stream g: S_g, dP_g | [s_free_g] S_{g+1} | [ds_g] dQ_g, dP_{g+1} | ...
 template <int D, int B>
 struct DqCfg {
   static constexpr int kChunks = D / 64;
-  static constexpr int kQBytes = kChunks * kM * 128;  // Q or dO tile (128 rows)
+  static constexpr int kQBytes = kChunks * kM * 128;  // Q or dO tile (128 rows) in the staging buffer
   static constexpr int kKVBytes = kChunks * B * 128;  // K_j or V_j
-  static constexpr int kVStages = (4 * kQBytes + 4 * kKVBytes + 1280 <= 232448) ? 2 : 1;  // smem opt-in max
-  static constexpr int kSmemTiles = 4 * kQBytes + kStages * kKVBytes + kVStages * kKVBytes;
-  static constexpr int kS0 = 0, kS1 = B, kDP = 2 * B, kDQ = 3 * B;
-  static constexpr uint32_t kCols = pow2_cols(3 * B + D);
-  static constexpr int kSmemBytes = kSmemTiles + 1024 + 256;
+  static constexpr int kBudget = 232448 - 1024 - 512 - 2 * kQBytes;
+  static constexpr int kKStages = (kBudget / kKVBytes - 2) > 4 ? 4 : (kBudget / kKVBytes - 2);
+  static constexpr int kVStages = (kBudget / kKVBytes - kKStages) > 4 ? 4 : (kBudget / kKVBytes - kKStages);
+  static_assert(kKStages >= 2 && kVStages >= 2, "dq smem rings");
+  static constexpr int kSmemTiles = 2 * kQBytes + (kKStages + kVStages) * kKVBytes;
+  static constexpr int kS = 0, kDP = B, kDQ = 2 * B, kQa = 2 * B + D, kDOa = 2 * B + D + D / 2;
+  static constexpr uint32_t kCols = pow2_cols(2 * B + 2 * D);
+  static constexpr int kSmemBytes = kSmemTiles + 1024 + 512;
 };
 
 struct DqBars {
-  uint64_t qdo_full[2], qdo_empty[2];
-  uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2], dp_full, ds_full, dq_done, dq_free;
+  uint64_t stage_full, stage_empty;  // Q / dO staging buffer (TMA -> tcgen05.cp)
+  uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
+  uint64_t s_full, s_free, dp_full, ds_full, dq_done, dq_free;
   uint32_t tmem_base;
 };
+
+__device__ __forceinline__ void tc_cp_128x256b(uint32_t taddr, uint64_t desc, uint32_t leader) {
+  asm volatile(
+      "{\n\t.reg .pred l;\n\tsetp.ne.b32 l, %2, 0;\n\t@l tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(taddr),
+      "l"(desc), "r"(leader)
+      : "memory");
+}
 
 template <int D, int B>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
@@ -681,17 +695,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
     const float* __restrict__ lse2, const float* __restrict__ dvec, int tp, float scale, float scale_log2,
     uint16_t* __restrict__ dq, const int32_t* __restrict__ order, int n_items, unsigned long long* trace) {
   using C = DqCfg<D, B>;
+  constexpr int kKS = C::kKStages, kVS = C::kVStages;
   auto tr = [&](int slot, int g) {
     if (trace != nullptr && blockIdx.x == 0 && g < 256 && (threadIdx.x & 31) == 0) trace[g * 16 + slot] = clock64();
   };
-  constexpr int kVS = C::kVStages;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-  uint8_t* q_smem = smem;                            // [2]
-  uint8_t* do_smem = smem + 2 * C::kQBytes;          // [2]
-  uint8_t* k_smem = smem + 4 * C::kQBytes;           // [kStages]
-  uint8_t* v_smem = k_smem + kStages * C::kKVBytes;  // [kVS]
+  uint8_t* q_stage = smem;                        // staging: Q_i
+  uint8_t* do_stage = smem + C::kQBytes;          // staging: dO_i
+  uint8_t* k_smem = smem + 2 * C::kQBytes;        // [kKS]
+  uint8_t* v_smem = k_smem + kKS * C::kKVBytes;   // [kVS]
   DqBars* bars = reinterpret_cast<DqBars*>(smem + C::kSmemTiles);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -699,17 +713,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
   const int grid = gridDim.x, cta = blockIdx.x;
 
   if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bars->qdo_full[b], 1);
-      mbar_init(&bars->qdo_empty[b], 1);
-      mbar_init(&bars->s_full[b], 1);
-    }
-    for (int st = 0; st < kStages; ++st) {
+    mbar_init(&bars->stage_full, 1);
+    mbar_init(&bars->stage_empty, 1);
+    for (int st = 0; st < 4; ++st) {
       mbar_init(&bars->k_full[st], 1);
       mbar_init(&bars->k_empty[st], 1);
       mbar_init(&bars->v_full[st], 1);
       mbar_init(&bars->v_empty[st], 1);
     }
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->s_free, 256);
     mbar_init(&bars->dp_full, 1);
     mbar_init(&bars->ds_full, 256);
     mbar_init(&bars->dq_done, 1);
@@ -741,10 +754,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
   };
 
   if (warp == 0 || warp == 10) {
-    // Warp 0 streams Q/dO + K, warp 10 streams V (independent rings in separate warps).
-    const int lane = (warp == 10) ? 1 : threadIdx.x & 31;  // role: 0 = Q/dO + K, 1 = V
-    if (lane < 2 && (threadIdx.x & 31) == 0) {
-      if (lane == 0) {
+    // Warp 0 stages Q/dO and streams K, warp 10 streams V (independent rings, separate warps).
+    const int role = (warp == 10) ? 1 : 0;
+    if (lane == 0) {
+      if (role == 0) {
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_do);
@@ -758,22 +771,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         const QItem w = decode_q(it);
         if (w.n <= 0) continue;
         const int hk = w.h / (hq / hkv);
-        if (lane == 0) {
-          const int qb = q & 1;
+        if (role == 0) {
           const int row0 = w.seq0 + w.i * B;
-          mbar_wait(&bars->qdo_empty[qb], ((q >> 1) & 1) ^ 1);
-          mbar_expect_tx(&bars->qdo_full[qb], 2 * C::kQBytes);
+          mbar_wait(&bars->stage_empty, (q & 1) ^ 1);
+          mbar_expect_tx(&bars->stage_full, 2 * C::kQBytes);
           for (int c = 0; c < C::kChunks; ++c) {
-            tma_load_3d(q_smem + qb * C::kQBytes + c * kM * 128, &tm_q, &bars->qdo_full[qb], c * 64, w.h, row0);
-            tma_load_3d(do_smem + qb * C::kQBytes + c * kM * 128, &tm_do, &bars->qdo_full[qb], c * 64, w.h, row0);
+            tma_load_3d(q_stage + c * kM * 128, &tm_q, &bars->stage_full, c * 64, w.h, row0);
+            tma_load_3d(do_stage + c * kM * 128, &tm_do, &bars->stage_full, c * 64, w.h, row0);
           }
         }
         for (int j = 0; j < w.n; ++j, ++g) {
           const int kv_row = w.seq0 + __ldg(w.list + j) * B;
-          if (lane == 0) {
-            const int st = g % kStages;
+          if (role == 0) {
+            const int st = g % kKS;
             tr(12, g);
-            mbar_wait(&bars->k_empty[st], ((g / kStages) & 1) ^ 1);
+            mbar_wait(&bars->k_empty[st], ((g / kKS) & 1) ^ 1);
             tr(13, g);
             mbar_expect_tx(&bars->k_full[st], C::kKVBytes);
             for (int c = 0; c < C::kChunks; ++c)
@@ -792,128 +804,113 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
       }
     }
   } else if (warp == 1) {
-    // Global block stream g over all items: S_0, dP_0 | S_{g+1} (other S buffer) overlaps the
-    // math of g | [dS_g] dQ_g, dP_{g+1} | ...  The next item's S / dP follow without a gap.
-    {  // whole warp, converged; `leader` issues
-      const uint32_t leader = elect_one();
-      constexpr uint32_t idesc_s = idesc_bf16_f32(kM, B, false, false);
-      constexpr uint32_t idesc_dq = idesc_bf16_f32(kM, D, false, true);
-      const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
-      auto s_col = [](int gg) { return (gg & 1) ? C::kS1 : C::kS0; };
-      auto issue_s = [&](int gg, int qb) {
-        const int st = gg % kStages;
-        tr(2, gg);
-        mbar_wait(&bars->k_full[st], (gg / kStages) & 1);
-        tr(3, gg);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(q_smem + qb * C::kQBytes);
+    // ------------------------------------------------------------ UMMA issuer (whole warp)
+    const uint32_t leader = elect_one();
+    constexpr uint32_t idesc_s = idesc_bf16_f32(kM, B, false, false);
+    constexpr uint32_t idesc_dq = idesc_bf16_f32(kM, D, false, true);
+    const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
+    const uint32_t qs_addr = smem_u32(q_stage), ds_addr = smem_u32(do_stage);
+    auto load_qdo = [&](int qq) {  // staging -> TMEM, behind the previous item's last S / dP
+      mbar_wait(&bars->stage_full, qq & 1);
+      tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
-          const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
-          mma_ss(tmem + s_col(gg), desc_sw128(q_addr + off_m, 16, 1024),
-                 desc_sw128(k_addr + st * C::kKVBytes + off_n, 16, 1024), idesc_s, kk > 0, leader);
-        }
-        tc_commit(&bars->s_full[gg & 1], leader);
-      };
-      auto issue_dp = [&](int gg, int qb, bool last_of_item) {
-        const int vst = gg % kVS;
-        tr(4, gg);
-        mbar_wait(&bars->v_full[vst], (gg / kVS) & 1);
-        tr(5, gg);
-        tc_fence_after();
-        const uint32_t do_addr = smem_u32(do_smem + qb * C::kQBytes);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off_m = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
-          const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
-          mma_ss(tmem + C::kDP, desc_sw128(do_addr + off_m, 16, 1024),
-                 desc_sw128(v_addr + vst * C::kKVBytes + off_n, 16, 1024), idesc_s, kk > 0, leader);
-        }
-        tc_commit(&bars->dp_full, leader);
-        tc_commit(&bars->v_empty[vst], leader);
-        if (last_of_item) tc_commit(&bars->qdo_empty[qb], leader);  // last S (earlier) and dP of the item
-      };
-      // Flattened stream: for each block g know (item q, local j, item length n).
-      int g = 0, q = 0;
-      int cur_k = 0;
-      QItem cur;
-      auto next_item = [&](int& kk_, QItem& w) -> bool {
-        for (;; ++kk_) {
-          const int it = sched::snake_item(order, n_items, grid, cta, kk_);
-          if (it < 0) return false;
-          w = decode_q(it);
-          if (w.n > 0) {
-            ++kk_;
-            return true;
-          }
-        }
-      };
-      bool have = next_item(cur_k, cur);
-      if (have) {
-        mbar_wait(&bars->qdo_full[0], 0);
-        issue_s(0, 0);
-        issue_dp(0, 0, cur.n == 1);
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
+        tc_cp_128x256b(tmem + C::kQa + kk * 8, desc_sw128(qs_addr + off, 16, 1024), leader);
+        tc_cp_128x256b(tmem + C::kDOa + kk * 8, desc_sw128(ds_addr + off, 16, 1024), leader);
       }
-      while (have) {
-        const int qb = q & 1;
-        const int n = cur.n;
-        QItem pending = cur;
-        int pending_k = cur_k;
-        bool pending_have = false;
-        for (int j = 0; j < n; ++j, ++g) {
-          // Look ahead: the next block of the stream (same item, or the first of the next one).
-          const bool last = j + 1 == n;
-          QItem nxt;
-          int nk = cur_k;
-          bool have_next = false;
-          if (!last) {
-            issue_s(g + 1, qb);
-          } else {
-            have_next = next_item(nk, nxt);
-            if (have_next) {
-              mbar_wait(&bars->qdo_full[qb ^ 1], ((q + 1) >> 1) & 1);
-              issue_s(g + 1, qb ^ 1);
-            }
-          }
-          tr(0, g);
-          mbar_wait(&bars->ds_full, g & 1);
-          tr(1, g);
-          tc_fence_after();
-          if (j == 0) mbar_wait(&bars->dq_free, (q & 1) ^ 1);  // previous item's dQ read out
-          const int st = g % kStages;
+      tc_commit(&bars->stage_empty, leader);
+    };
+    auto issue_s = [&](int gg) {
+      if (gg > 0) mbar_wait(&bars->s_free, (gg - 1) & 1);  // S_{gg-1} read out of TMEM
+      const int st = gg % kKS;
+      tr(2, gg);
+      mbar_wait(&bars->k_full[st], (gg / kKS) & 1);
+      tr(3, gg);
+      tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < B / 16; ++kk)
-            mma_ts(tmem + C::kDQ, tmem + s_col(g) + packed_col<B>(kk),
-                   desc_sw128(k_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024), idesc_dq,
-                   (j > 0 || kk > 0) ? 1u : 0u, leader);
-          tc_commit(&bars->k_empty[st], leader);
-          tr(6, g);
-          if (last) tc_commit(&bars->dq_done, leader);
-          if (!last) {
-            issue_dp(g + 1, qb, j + 2 == n);
-          } else if (have_next) {
-            issue_dp(g + 1, qb ^ 1, nxt.n == 1);
-          }
-          if (last) {
-            pending = nxt;
-            pending_k = nk;
-            pending_have = have_next;
-          }
-        }
-        cur = pending;
-        cur_k = pending_k;
-        have = pending_have;
-        ++q;
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
+        mma_ts(tmem + C::kS, tmem + C::kQa + kk * 8, desc_sw128(k_addr + st * C::kKVBytes + off_n, 16, 1024), idesc_s,
+               kk > 0, leader);
       }
+      tc_commit(&bars->s_full, leader);
+    };
+    auto issue_dp = [&](int gg) {
+      const int vst = gg % kVS;
+      tr(4, gg);
+      mbar_wait(&bars->v_full[vst], (gg / kVS) & 1);
+      tr(5, gg);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off_n = (kk >> 2) * (B * 128) + (kk & 3) * 32;
+        mma_ts(tmem + C::kDP, tmem + C::kDOa + kk * 8, desc_sw128(v_addr + vst * C::kKVBytes + off_n, 16, 1024),
+               idesc_s, kk > 0, leader);
+      }
+      tc_commit(&bars->dp_full, leader);
+      tc_commit(&bars->v_empty[vst], leader);
+    };
+    auto next_item = [&](int& kk_, QItem& w) -> bool {
+      for (;; ++kk_) {
+        const int it = sched::snake_item(order, n_items, grid, cta, kk_);
+        if (it < 0) return false;
+        w = decode_q(it);
+        if (w.n > 0) {
+          ++kk_;
+          return true;
+        }
+      }
+    };
+    int g = 0, q = 0, cur_k = 0;
+    QItem cur;
+    bool have = next_item(cur_k, cur);
+    if (have) {
+      load_qdo(0);
+      issue_s(0);
+      issue_dp(0);
+    }
+    while (have) {
+      const int n = cur.n;
+      QItem nxt;
+      bool have_next = false;
+      for (int j = 0; j < n; ++j, ++g) {
+        const bool last = j + 1 == n;
+        if (last) have_next = next_item(cur_k, nxt);
+        const bool more = !last || have_next;
+        if (more) {
+          if (last) load_qdo(q + 1);  // in order behind S_g / dP_g, the item's last readers of Q / dO
+          issue_s(g + 1);
+        }
+        tr(0, g);
+        mbar_wait(&bars->ds_full, g & 1);
+        tr(1, g);
+        tc_fence_after();
+        if (j == 0) mbar_wait(&bars->dq_free, (q & 1) ^ 1);  // previous item's dQ read out
+        const int st = g % kKS;
+#pragma unroll
+        for (int kk = 0; kk < B / 16; ++kk)
+          mma_ts(tmem + C::kDQ, tmem + C::kDP + packed_col<B>(kk),
+                 desc_sw128(k_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024), idesc_dq, (j > 0 || kk > 0) ? 1u : 0u,
+                 leader);
+        tc_commit(&bars->k_empty[st], leader);
+        if (last) tc_commit(&bars->dq_done, leader);
+        tr(6, g);
+        if (more) issue_dp(g + 1);
+      }
+      cur = nxt;
+      have = have_next;
+      ++q;
     }
   } else if (warp < 10) {
+    // ------------------------------------------------------------ math + epilogue
     // Two warpgroups split every query row's B key columns and the D output columns in halves.
     constexpr int HB = B / 2;
     const int quarter = warp & 3;
     const int hf = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;
     const uint32_t lf = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t s_col = C::kS + hf * HB, dp_col = C::kDP + hf * HB;
     int g = 0, q = 0;
     for (int k = 0;; ++k) {
       const int it = sched::snake_item(order, n_items, grid, cta, k);
@@ -934,8 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         const int jb = __ldg(w.list + j);
         const int key_lim = min(B, w.seq_len - jb * B);
         const int lim = valid ? min(key_lim, jb == w.i ? r + 1 : B) : 0;
-        const uint32_t s_col = ((g & 1) ? C::kS1 : C::kS0) + hf * HB;
-        mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
+        mbar_wait(&bars->s_full, g & 1);
         if (threadIdx.x == 64) tr(8, g);
         tc_fence_after();
         float p[HB];
@@ -944,6 +940,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
 #pragma unroll
           for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(tmem + lf + s_col + c2 * 32, sv[c2]);
           tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(&bars->s_free);  // S_g is in registers: S_{g+1} may overwrite it
           if (__all_sync(0xffffffffu, lim >= (hf + 1) * HB)) {
             dq_p<HB, false>(sv, -l2, scale_log2, hf * HB, B, p);
           } else {
@@ -955,7 +953,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         if (threadIdx.x == 64) tr(10, g);
         tc_fence_after();
         {
-          const uint32_t dp_col = C::kDP + hf * HB;
+          // dP chunks software-pipelined; dS of chunk c2 is packed into columns [c2 * 16, c2 * 16 + 16)
+          // of this half, which belong to chunks already read.
           uint32_t pv[2][32];
           tmem_ld32(tmem + lf + dp_col, pv[0]);
           tmem_wait_ld();
@@ -971,8 +970,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
                                                               mk2(-dd, -dd)));
               dsp[e / 2] = pack_bf16x2(ds.x, ds.y);
             }
-            tmem_st16(tmem + lf + s_col + c2 * 16, dsp);  // dS over this half's S (already in registers)
-            tmem_wait_ld();
+            tmem_st16(tmem + lf + dp_col + c2 * 16, dsp);
+            if (c2 + 1 < HB / 32) tmem_wait_ld();
           }
         }
         tmem_wait_st();

@@ -29,6 +29,7 @@ print("blocks traced", n)
 print("period (ds wait start -> next):", med(np.diff(t[a:b + 1, 0])))
 print("UMMA ds_full wait:", med(t[r, 1] - t[r, 0]))
 print("UMMA k_full wait (issue_s):", med(t[r, 3] - t[r, 2]))
+print("UMMA issue_s start (after s_free) - prev dQ issued:", med(t[r, 2] - t[r, 6]))
 print("UMMA v_full wait (issue_dp):", med(t[r, 5] - t[r, 4]))
 print("UMMA dQ issue (ds seen -> after commit):", med(t[r, 6] - t[r, 1]))
 print("math: s seen -> P done:", med(t[r, 9] - t[r, 8]))
