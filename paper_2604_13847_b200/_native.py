@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsparsebalance_b200.so")
+# SB_LIB_PATH: experiment builds only (e.g. tools/ A/B timing); the product path is the in-tree lib.
+LIB_PATH = os.environ.get("SB_LIB_PATH") or os.path.join(_HERE, "lib", "libsparsebalance_b200.so")
 
 _lib = None
 

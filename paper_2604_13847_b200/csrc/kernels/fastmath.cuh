@@ -79,8 +79,11 @@ __device__ __forceinline__ f2 ex2_poly2(f2 x) {
 
 // Pair e of a row (columns 2e, 2e+1): 3 of every 8 pairs on the FMA pipe. `e` must be a
 // compile-time constant after unrolling so the branch disappears.
+#ifndef SB_POLY_OF_8
+#define SB_POLY_OF_8 3  // exp2 pairs (of every 8) evaluated on the FMA pipe
+#endif
 __device__ __forceinline__ f2 ex2_pair(f2 x, int e) {
-  if ((e & 7) >= 5) return ex2_poly2(x);
+  if ((e & 7) >= 8 - SB_POLY_OF_8) return ex2_poly2(x);
   return mk2(ex2_sfu(x.x), ex2_sfu(x.y));
 }
 
