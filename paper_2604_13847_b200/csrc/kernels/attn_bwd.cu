@@ -36,37 +36,53 @@ __host__ __device__ constexpr uint32_t pow2_cols(int c) { return c <= 32 ? 32 : 
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ d_o,
                                                        const float* __restrict__ lse, int total, int hq, int d, int tp,
                                                        float* __restrict__ lse2, float* __restrict__ dvec) {
-  // Each thread reduces 8 bf16 products (one 16-byte load of O and of dO); the d/8 threads of a
-  // row (16 for d=128, 8 for d=64) finish with xor-shuffles.
-  const int tpr = d >> 3;  // threads per row
-  const long long rows = static_cast<long long>(total) * hq;
-  const long long nthreads = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; g < rows * tpr; g += nthreads) {
-    const long long row = g / tpr;
-    const uint4 a = __ldg(reinterpret_cast<const uint4*>(o) + g);
-    const uint4 b = __ldg(reinterpret_cast<const uint4*>(d_o) + g);
-    const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
-    float acc = 0.f;
+  // Head h = blockIdx.y; consecutive threads walk consecutive tokens of that head, so the
+  // lse / lse2 / dvec rows are read and written contiguously. Each thread reduces 8 bf16
+  // products (one 16-byte load of O and of dO); the d/8 threads of a row (16 for d=128, 8 for
+  // d=64) finish with xor-shuffles. Two rows per thread per step keep 4 loads in flight.
+  const int h = blockIdx.y;
+  const int tpr_log = d == 128 ? 4 : 3;  // log2(threads per row)
+  const int sub = threadIdx.x & ((1 << tpr_log) - 1);
+  const int rows_per_block = blockDim.x >> tpr_log;
+  const int stride = gridDim.x * rows_per_block;
+  for (int t0 = blockIdx.x * rows_per_block + (threadIdx.x >> tpr_log); t0 < total; t0 += 2 * stride) {
+    const int t1 = t0 + stride;
+    const bool has1 = t1 < total;
+    const size_t e0 = (static_cast<size_t>(t0) * hq + h) * (d >> 3) + sub;
+    const size_t e1 = (static_cast<size_t>(has1 ? t1 : t0) * hq + h) * (d >> 3) + sub;
+    const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(o) + e0);
+    const uint4 b0 = __ldg(reinterpret_cast<const uint4*>(d_o) + e0);
+    const uint4 a1 = __ldg(reinterpret_cast<const uint4*>(o) + e1);
+    const uint4 b1 = __ldg(reinterpret_cast<const uint4*>(d_o) + e1);
+    float acc0 = 0.f, acc1 = 0.f;
+    const uint32_t wa0[4] = {a0.x, a0.y, a0.z, a0.w}, wb0[4] = {b0.x, b0.y, b0.z, b0.w};
+    const uint32_t wa1[4] = {a1.x, a1.y, a1.z, a1.w}, wb1[4] = {b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      acc = fmaf(__uint_as_float(wa[e] << 16), __uint_as_float(wb[e] << 16), acc);
-      acc = fmaf(__uint_as_float(wa[e] & 0xffff0000u), __uint_as_float(wb[e] & 0xffff0000u), acc);
+      acc0 = fmaf(__uint_as_float(wa0[e] << 16), __uint_as_float(wb0[e] << 16), acc0);
+      acc0 = fmaf(__uint_as_float(wa0[e] & 0xffff0000u), __uint_as_float(wb0[e] & 0xffff0000u), acc0);
+      acc1 = fmaf(__uint_as_float(wa1[e] << 16), __uint_as_float(wb1[e] << 16), acc1);
+      acc1 = fmaf(__uint_as_float(wa1[e] & 0xffff0000u), __uint_as_float(wb1[e] & 0xffff0000u), acc1);
     }
-    for (int off = tpr >> 1; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if ((g % tpr) == 0) {
-      const int t = static_cast<int>(row / hq), h = static_cast<int>(row - static_cast<long long>(t) * hq);
-      dvec[static_cast<size_t>(h) * tp + t] = acc;
-      lse2[static_cast<size_t>(h) * tp + t] = lse[static_cast<size_t>(h) * total + t] * kLog2e;
+    for (int off = (1 << tpr_log) >> 1; off; off >>= 1) {
+      acc0 += __shfl_xor_sync(0xffffffffu, acc0, off);
+      acc1 += __shfl_xor_sync(0xffffffffu, acc1, off);
+    }
+    if (sub == 0) {
+      dvec[static_cast<size_t>(h) * tp + t0] = acc0;
+      lse2[static_cast<size_t>(h) * tp + t0] = lse[static_cast<size_t>(h) * total + t0] * kLog2e;
+      if (has1) {
+        dvec[static_cast<size_t>(h) * tp + t1] = acc1;
+        lse2[static_cast<size_t>(h) * tp + t1] = lse[static_cast<size_t>(h) * total + t1] * kLog2e;
+      }
     }
   }
   // Padding columns [total, tp): never read for valid rows, but keep them finite.
-  const int pad = tp - total;
-  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < static_cast<long long>(hq) * pad;
-       e += nthreads) {
-    const int h = static_cast<int>(e / pad), t = total + static_cast<int>(e % pad);
-    dvec[static_cast<size_t>(h) * tp + t] = 0.f;
-    lse2[static_cast<size_t>(h) * tp + t] = 0.f;
-  }
+  if (blockIdx.x == 0)
+    for (int t = total + threadIdx.x; t < tp; t += blockDim.x) {
+      dvec[static_cast<size_t>(h) * tp + t] = 0.f;
+      lse2[static_cast<size_t>(h) * tp + t] = 0.f;
+    }
 }
 
 // ------------------------------------------------------------------------------------ K7
@@ -1061,7 +1077,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   const float scale_log2 = scale * kLog2e;
   const int sms = sched::num_sms();
 
-  bwd_prep_kernel<<<sms * 8, 256, 0, st>>>(o, d_o, lse, total, hq, D, w.tp, lse2, dvec);
+  bwd_prep_kernel<<<dim3(std::max(1, sms * 8 / hq), hq), 256, 0, st>>>(o, d_o, lse, total, hq, D, w.tp, lse2, dvec);
   launched("sb_sparse_attn_bwd/prep");
   const int kv_items = hkv * nb_total;
   const int rows_per_kv = hsel / hkv;

@@ -48,43 +48,41 @@ __global__ void key_hist_kernel(Key key, int n_items, int32_t* __restrict__ hist
 }
 
 // start[b] = number of items with key < b (exclusive scan, one CTA of 1024); resets the
-// histogram so it can serve as the scatter cursor.
+// histogram so it can serve as the scatter cursor. Thread t owns a contiguous run of bins, so
+// the CTA makes two passes over the histogram with a single block-wide scan in between (the
+// bin count reaches ~10^5 for the key-block order).
 __global__ void __launch_bounds__(1024) key_start_kernel(int32_t* __restrict__ hist, int bins,
                                                          int32_t* __restrict__ start) {
   __shared__ int warp_sum[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int base = 0; base < bins; base += 1024) {
-    const int b = base + threadIdx.x;
-    const int v = b < bins ? hist[b] : 0;
-    int x = v;
+  const int per = (bins + 1023) / 1024;
+  const int b0 = min(bins, threadIdx.x * per), b1 = min(bins, b0 + per);
+  int v = 0;
+  for (int b = b0; b < b1; ++b) v += hist[b];
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int ws = warp_sum[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int y = __shfl_up_sync(0xffffffffu, ws, o);
+      if (lane >= o) ws += y;
     }
-    if (lane == 31) warp_sum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      int ws = warp_sum[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, ws, o);
-        if (lane >= o) ws += y;
-      }
-      warp_sum[lane] = ws;
-    }
-    __syncthreads();
-    const int excl = carry + (warp ? warp_sum[warp - 1] : 0) + x - v;
-    if (b < bins) {
-      start[b] = excl;
-      hist[b] = 0;
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
-    __syncthreads();
+    warp_sum[lane] = ws;
+  }
+  __syncthreads();
+  int run = (warp ? warp_sum[warp - 1] : 0) + x - v;
+  for (int b = b0; b < b1; ++b) {
+    const int h = hist[b];
+    start[b] = run;
+    hist[b] = 0;
+    run += h;
   }
 }
 
