@@ -1030,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
 }
 
 // ------------------------------------------------------------------------------------ host
-constexpr int kMaxKvCost = 4096;
+constexpr int kMaxKvCost = 1023;  // longest-first order resolution (costs above share the top bin)
 unsigned long long* g_trace_bwd = nullptr;  // debug timeline buffer (sb_debug_set_trace_bwd)
 unsigned long long* g_trace_dq = nullptr;   // debug timeline buffer (sb_debug_set_trace_dq)
 

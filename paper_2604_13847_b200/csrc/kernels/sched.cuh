@@ -48,41 +48,52 @@ __global__ void key_hist_kernel(Key key, int n_items, int32_t* __restrict__ hist
 }
 
 // start[b] = number of items with key < b (exclusive scan, one CTA of 1024); resets the
-// histogram so it can serve as the scatter cursor. Thread t owns a contiguous run of bins, so
-// the CTA makes two passes over the histogram with a single block-wide scan in between (the
-// bin count reaches ~10^5 for the key-block order).
+// histogram so it can serve as the scatter cursor. Warp w owns a contiguous segment of
+// 32 * per bins and walks it with coalesced loads: pass 1 sums the segment, one block-wide
+// scan of the 32 warp totals, pass 2 re-walks it with a warp inclusive scan per 32 bins (the
+// bin count reaches ~3 * 10^4 for the key-block order).
 __global__ void __launch_bounds__(1024) key_start_kernel(int32_t* __restrict__ hist, int bins,
                                                          int32_t* __restrict__ start) {
   __shared__ int warp_sum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int per = (bins + 1023) / 1024;
-  const int b0 = min(bins, threadIdx.x * per), b1 = min(bins, b0 + per);
+  const int per = (bins + 1023) / 1024;  // 32-bin steps per warp
+  const int seg0 = warp * 32 * per;
   int v = 0;
-  for (int b = b0; b < b1; ++b) v += hist[b];
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+#pragma unroll 4
+  for (int it = 0; it < per; ++it) {
+    const int b = seg0 + it * 32 + lane;
+    v += b < bins ? hist[b] : 0;
   }
-  if (lane == 31) warp_sum[warp] = x;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) warp_sum[warp] = v;
   __syncthreads();
   if (warp == 0) {
-    int ws = warp_sum[lane];
+    const int x = warp_sum[lane];
+    int incl = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, ws, o);
-      if (lane >= o) ws += y;
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    warp_sum[lane] = ws;
+    warp_sum[lane] = incl - x;  // exclusive
   }
   __syncthreads();
-  int run = (warp ? warp_sum[warp - 1] : 0) + x - v;
-  for (int b = b0; b < b1; ++b) {
-    const int h = hist[b];
-    start[b] = run;
-    hist[b] = 0;
-    run += h;
+  int carry = warp_sum[warp];
+  for (int it = 0; it < per; ++it) {
+    const int b = seg0 + it * 32 + lane;
+    const int h = b < bins ? hist[b] : 0;
+    int incl = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (b < bins) {
+      start[b] = carry + incl - h;
+      hist[b] = 0;
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
 

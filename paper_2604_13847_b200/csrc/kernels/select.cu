@@ -1,10 +1,12 @@
 // K3 per-query-block top-k block selector and K4 coverage profile / coverage-at-grid.
 //
-// Selector: one CTA per selection row. Candidates are staged in registers, the k-th largest
-// 32-bit order key is found by a 4-pass 8-bit radix select over shared-memory histograms,
-// and ties at the threshold are resolved to the lowest block index with ordered warp-ballot
-// prefix scans, so the selected set is exactly "score descending, index ascending" and the
-// output comes out in ascending index order without a sort.
+// Selector: rows of up to 256 candidates (sequences up to 32K tokens at B=128) take one WARP
+// per row: 8 candidates per lane in registers, the k-th largest 32-bit order key found by a
+// 32-step bitwise radix select on warp ballots (no shared memory, no block barriers), ties at
+// the threshold resolved to the lowest block index with ordered ballot prefix counts. Longer
+// rows take one CTA: candidates in registers, a 4-pass 8-bit radix select over shared-memory
+// histograms and block-wide ordered ballot scans. Both produce exactly "score descending,
+// index ascending", already in ascending index order without a sort.
 // Profile: per-row softmax masses sorted descending (bitonic sort in shared memory), then a
 // deterministic per-(sequence, rank) fp64 reduction over (head, row).
 #include "common.cuh"
@@ -44,6 +46,90 @@ __device__ __forceinline__ int block_excl_scan(bool flag, int* warp_tot, int* to
   return before + __popc(b & ((1u << lane) - 1u));
 }
 
+constexpr int kWarpRow = 256;  // rows up to this many candidates: one warp per row
+
+__global__ void __launch_bounds__(256) topk_select_warp_kernel(
+    const float* __restrict__ scores, const int32_t* __restrict__ blk_off, const int64_t* __restrict__ tri_off,
+    int nseq, int nbt, int group, const int32_t* __restrict__ k_seq, int k_max, int force_diag,
+    int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int gi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int g = blockIdx.y;
+  if (gi >= nbt) return;
+  const int s = seq_of_block(blk_off, nseq, gi);
+  const int i = gi - blk_off[s];
+  const int n = i + 1;
+  if (n > kWarpRow) return;  // long rows: topk_select_kernel
+  const int64_t tri = tri_off[nseq];
+  const int k = max(1, min(k_seq[s], n));
+  int32_t* out = idx + (static_cast<size_t>(g) * nbt + gi) * k_max;
+  if (lane == 0) cnt[static_cast<size_t>(g) * nbt + gi] = k;
+  const int m = force_diag ? n - 1 : n;     // candidate count
+  const int want = force_diag ? k - 1 : k;  // candidates to keep
+  if (want >= m) {
+    for (int r = lane; r < k_max; r += 32) out[r] = r < n ? r : -1;
+    return;
+  }
+  if (want == 0) {
+    for (int r = lane; r < k_max; r += 32) out[r] = r == 0 ? i : -1;
+    return;
+  }
+  const int64_t row_off = tri_off[s] + static_cast<int64_t>(i) * (i + 1) / 2;
+  const float* base = scores + static_cast<size_t>(g) * group * tri + row_off;
+  uint32_t key[kWarpRow / 32];
+#pragma unroll
+  for (int r = 0; r < kWarpRow / 32; ++r) {
+    const int j = r * 32 + lane;
+    float v = -INFINITY;
+    if (j < m) {
+      v = __ldg(base + j);
+      for (int q = 1; q < group; ++q) v += __ldg(base + static_cast<size_t>(q) * tri + j);
+    }
+    key[r] = j < m ? order_key(v) : 0u;
+  }
+  const int slots = (m + 31) >> 5;
+  // Bitwise radix select of the want-th largest key among the m candidates.
+  uint32_t prefix = 0;
+  int remaining = want;
+#pragma unroll 1
+  for (int bit = 31; bit >= 0; --bit) {
+    const uint32_t hi_mask = bit == 31 ? 0u : (0xffffffffu << (bit + 1));
+    int c = 0;
+#pragma unroll
+    for (int r = 0; r < kWarpRow / 32; ++r) {
+      if (r >= slots) break;
+      const int j = r * 32 + lane;
+      const bool hit = j < m && (key[r] & hi_mask) == prefix && ((key[r] >> bit) & 1u);
+      c += __popc(__ballot_sync(0xffffffffu, hit));
+    }
+    if (c >= remaining) {
+      prefix |= 1u << bit;
+    } else {
+      remaining -= c;
+    }
+  }
+  const uint32_t thresh = prefix;  // keys > thresh all kept; `remaining` of the == thresh kept
+  const uint32_t lt = (1u << lane) - 1u;
+  int ties_before = 0, kept_before = 0;
+#pragma unroll
+  for (int r = 0; r < kWarpRow / 32; ++r) {
+    if (r >= slots) break;
+    const int j = r * 32 + lane;
+    const bool valid = j < m;
+    const bool tie = valid && key[r] == thresh;
+    const uint32_t tb = __ballot_sync(0xffffffffu, tie);
+    const bool keep = valid && (key[r] > thresh || (tie && ties_before + __popc(tb & lt) < remaining));
+    const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+    if (keep) out[kept_before + __popc(kb & lt)] = j;
+    ties_before += __popc(tb);
+    kept_before += __popc(kb);
+  }
+  for (int r = lane; r < k_max; r += 32) {
+    if (r == want && force_diag) out[r] = i;
+    else if (r >= k) out[r] = -1;
+  }
+}
+
 __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(
     const float* __restrict__ scores, const int32_t* __restrict__ blk_off, const int64_t* __restrict__ tri_off,
     int nseq, int group, const int32_t* __restrict__ k_seq, int k_max, int force_diag,
@@ -55,6 +141,7 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(
   const int s = seq_of_block(blk_off, nseq, gi);
   const int i = gi - blk_off[s];
   const int n = i + 1;
+  if (n <= kWarpRow) return;  // short rows: topk_select_warp_kernel
   const int k = max(1, min(k_seq[s], n));
   int32_t* out = idx + (static_cast<size_t>(g) * nbt + gi) * k_max;
   if (threadIdx.x == 0) cnt[static_cast<size_t>(g) * nbt + gi] = k;
@@ -280,10 +367,17 @@ SB_API int sb_topk_select(const float* scores, const int32_t* blk_off, const int
     sbk::require(hs / group <= 65535, "too many selection heads");
     if (nseq == 0 || nb_total == 0) return;
     sbk::require(scores && blk_off && tri_off && k_seq && idx && cnt, "null pointer");
-    dim3 grid(nb_total, hs / group);
-    sbk::topk_select_kernel<<<grid, sbk::kSelThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        scores, blk_off, tri_off, nseq, group, k_seq, k_max, force_diag ? 1 : 0, idx, cnt);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    dim3 wgrid((nb_total + 7) / 8, hs / group);
+    sbk::topk_select_warp_kernel<<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, group, k_seq, k_max,
+                                                         force_diag ? 1 : 0, idx, cnt);
     sbk::launched("sb_topk_select");
+    if (nb_max > sbk::kWarpRow) {  // rows longer than 256 candidates
+      dim3 grid(nb_total, hs / group);
+      sbk::topk_select_kernel<<<grid, sbk::kSelThreads, 0, st>>>(scores, blk_off, tri_off, nseq, group, k_seq, k_max,
+                                                                 force_diag ? 1 : 0, idx, cnt);
+      sbk::launched("sb_topk_select");
+    }
   });
 }
 
