@@ -351,6 +351,31 @@ def main():
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1) / args.steps
+
+    # ---- N > 1 (C3): the same step with the step-end gradient all-reduce of SURVEY 8(e),
+    # one stand-in bucket per layer (the layer's output-projection gradient, H*D x H*D bf16),
+    # all-reduced on NCCL's stream overlapping the following layers. Reported beside the main
+    # number, which (like the metric's max/mean) is measured before this barrier.
+    grad_ar = None
+    if world > 1 and workload_kind == "c3":
+        hidden = H * D
+        buckets = [torch.zeros((hidden, hidden), dtype=torch.bfloat16, device=dev) for _ in range(args.layers)]
+        runner.run(backward=True, grad_buckets=buckets)  # warm the NCCL path
+        torch.cuda.synchronize()
+        dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ar_steps = max(1, min(args.steps, 3))
+        a0.record(stream)
+        for _ in range(ar_steps):
+            runner.run(backward=True, grad_buckets=buckets)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ar_ms = torch.tensor([a0.elapsed_time(a1) / ar_steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(ar_ms, op=dist.ReduceOp.MAX)
+        grad_ar = {"stand_in": f"{args.layers} x [{hidden}, {hidden}] bf16 (output-projection gradient per layer)",
+                   "bytes_per_step": int(args.layers * hidden * hidden * 2),
+                   "ms_per_step_with_allreduce": float(ar_ms[0]),
+                   "overlap": "per-layer async NCCL all_reduce issued after that layer's backward"}
     phase = {}
     for m in markers:
         for k_, v_ in m.durations().items():
@@ -435,6 +460,7 @@ def main():
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                     "note": "pinned H2D of Q,K,V,dO + D2H of O,dQ,dK,dV (last layer) every step"},
             "gpu_launches": int(launches),
+            "grad_allreduce": grad_ar,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -174,9 +174,16 @@ class DPStep:
         return exchange_estimates(self.batch.lengths, layer_profiles, self.width, self.block, self.world, self.group,
                                   self.q.device)
 
-    def run(self, backward: bool = True, mark=None):
+    def run(self, backward: bool = True, mark=None, grad_buckets=None):
         """mark(tag) (optional) is called at phase boundaries: 'decided' after the scorer
-        pre-pass + exchange + DST, then 'fwd' / 'bwd' after each layer's kernels."""
+        pre-pass + exchange + DST, then 'fwd' / 'bwd' after each layer's kernels.
+
+        grad_buckets (optional, one tensor per layer): the step-end gradient all-reduce of
+        SURVEY.md section 8(e). The attention op has no parameters, so the caller passes a stand-in
+        (e.g. the layer's output-projection gradient); each layer's bucket is all-reduced
+        asynchronously on NCCL's stream as soon as that layer's backward is enqueued, DDP-style,
+        overlapping the next layers' kernels, and the compute stream waits for all of them at
+        the end."""
         lay = self.batch.layout
         qbar, kbar, profs, scores = self.scorer_pass()
         pooled = self.exchange(profs)
@@ -190,7 +197,7 @@ class DPStep:
         k_all = np.minimum(k_final[self.rank][:, None], nb[None, :]).astype(np.int32)
         self._k_host = torch.from_numpy(k_all).pin_memory()
         k_dev = self._k_host.to(self.q.device, non_blocking=True)
-        outs = []
+        outs, works = [], []
         for l, s_l in enumerate(self.layer_scales):
             k_max = int(max(1, k_all[l].max()))
             scale = s_l / math.sqrt(self.d)
@@ -201,7 +208,13 @@ class DPStep:
             grads = ops.sparse_attn_bwd(self.q, self.k, self.v, o, self.do, lse, lay, idx, cnt, scale) if backward else None
             if mark:
                 mark("bwd")
+            if grad_buckets is not None and self.world > 1:
+                import torch.distributed as dist
+
+                works.append(dist.all_reduce(grad_buckets[l], group=self.group, async_op=True))
             outs.append((idx, cnt, o, grads))
+        for w_ in works:
+            w_.wait()  # the compute stream waits for every bucket
         return outs
 
 
