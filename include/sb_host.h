@@ -104,7 +104,9 @@ int SBH(plan_batching)(int strategy, int n, const int64_t* ids, const int64_t* l
  * Outputs: out_budgets[dp * mpr * nl] ([rank][mb][layer]); out_ids / out_mb_off as in
  * plan_batching; decisions (cap n_dec_cap) out_dec_i[.][6] = {mb, layer, k_base, k_anchor,
  * k_final, direction}, out_dec_d[.][3]; *out_n_dec. out_stats[2] = {mean_cov_drop,
- * avg_budget}. */
+ * avg_budget}. decisions_csv_path / plan_json_path (nullable): the step's replay files in
+ * the reference formats (write_decisions_csv dst.cpp:171-185 with iter = iter_index,
+ * save_plan_json sab.cpp:312-336). */
 int SBH(plan_step)(int strategy, int n, const int64_t* ids, const int64_t* lengths,
                    const double* profiles, const int64_t* off, const int* setup_i,
                    const double* setup_d, int anchor, const int* dst_grid, int n_dst_grid,
@@ -112,7 +114,8 @@ int SBH(plan_step)(int strategy, int n, const int64_t* ids, const int64_t* lengt
                    const int* est_grid, int n_est_grid, const int64_t* bins, int nx,
                    const int* grid, int nk, const double* lat, int iter_index, int* out_budgets,
                    int64_t* out_ids, int* out_mb_off, int* out_dec_i, double* out_dec_d,
-                   int n_dec_cap, int* out_n_dec, double* out_stats);
+                   int n_dec_cap, int* out_n_dec, double* out_stats,
+                   const char* decisions_csv_path, const char* plan_json_path);
 
 #ifdef __cplusplus
 }

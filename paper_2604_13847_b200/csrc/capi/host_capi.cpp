@@ -432,7 +432,8 @@ SB_EXPORT int SBH(plan_step)(int strategy, int n, const int64_t* ids, const int6
                              const double* lat, int iter_index, int* out_budgets,
                              int64_t* out_ids, int* out_mb_off, int* out_dec_i,
                              double* out_dec_d, int n_dec_cap, int* out_n_dec,
-                             double* out_stats) {
+                             double* out_stats, const char* decisions_csv_path,
+                             const char* plan_json_path) {
   return guarded([&] {
     const int gbs = setup_i[0], mbs = setup_i[1], dp = setup_i[2], nl = setup_i[3];
     const auto samples = make_samples(n, ids, lengths, nl, profiles, off);
@@ -516,6 +517,10 @@ SB_EXPORT int SBH(plan_step)(int strategy, int n, const int64_t* ids, const int6
     stats[0] = sp.mean_cov_drop;
     stats[1] = sp.avg_budget;
 #endif
+    // The step's replay files (decisions CSV dst.cpp:171-185, plan JSON sab.cpp:312-336),
+    // written by this build's own write_decisions_csv / save_plan_json.
+    if (decisions_csv_path != nullptr) sb::write_decisions_csv(decisions, iter_index, decisions_csv_path);
+    if (plan_json_path != nullptr) sb::save_plan_json(plan, plan_json_path);
     if (static_cast<int>(decisions.size()) > n_dec_cap)
       throw sb::ConfigError("plan_step: decision capacity too small");
     *out_n_dec = static_cast<int>(decisions.size());

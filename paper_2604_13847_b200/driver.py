@@ -1,0 +1,202 @@
+"""Measured data-parallel step driver.
+
+The reference's scenario loop (run_scenarios, proj/core/src/sim.cpp:518-585) draws a global
+batch per iteration, plans it (simulate_iteration's decision half, sim.cpp:277-432) and
+*simulates* each rank's 1F1B pipeline from a cost table (simulate_pipeline / micro_batch_time,
+sim.cpp:88-98, 180-275, 435-476). This driver keeps the first two steps bit-identical
+(generate_samples with the reference's seed stream mix_seed(seed, iter), sim.cpp:555-558;
+plan_step == simulate_iteration's decisions, checked in tests/test_host_parity.py) and replaces
+the third with the real kernels: every rank runs its micro-batches' layers (block scorer ->
+top-k selector with the DST keep count of that (micro-batch, layer), clamped per sequence ->
+sparse attention fwd -> bwd) timed with CUDA events, and the per-(rank, micro-batch) times are
+all-gathered.
+
+It emits the reference's replay files per iteration, so a run can be replayed against the
+oracle:
+  * iterations CSV with the reference's header and %.6f fields (report.cpp:55-74):
+    scenario,iter,iter_ms,imbalance,max_mb_ms,mean_mb_ms,bubble_ms,dst_overhead_ms,
+    avg_budget,mean_cov_drop -- iter_ms = max over ranks of the rank's summed micro-batch
+    time (pp = 1, so bubble_ms = 0 as in sim.cpp:272), imbalance = max / mean over all
+    (rank, micro-batch) totals (sim.cpp:483-485), dst_overhead_ms = host planning wall time;
+  * decisions CSV (dst.cpp:171-185) and plan JSON (sab.cpp:312-336) through plan_step.
+
+    python -m torch.distributed.run --nproc-per-node 8 -m paper_2604_13847_b200.driver \\
+        --strategy sab_dst --iters 4 --out runs/sab_dst
+"""
+from __future__ import annotations
+
+import argparse
+import math
+import os
+import time
+
+import numpy as np
+import torch
+
+from . import ops
+from .host import DEFAULT_BUDGET_GRID, ProfileTable, api
+
+MASK64 = (1 << 64) - 1
+
+
+def splitmix64(x: int) -> int:
+    """rng.cpp:13-18."""
+    x = (x + 0x9E3779B97F4A7C15) & MASK64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & MASK64
+    return x ^ (x >> 31)
+
+
+def mix_seed(seed: int, a: int) -> int:
+    """rng.cpp:23-25: the per-iteration seed of run_scenarios (sim.cpp:558)."""
+    return splitmix64(splitmix64(seed & MASK64) ^ (a & MASK64))
+
+
+ITER_HEADER = ("scenario,iter,iter_ms,imbalance,max_mb_ms,mean_mb_ms,bubble_ms,dst_overhead_ms,avg_budget,"
+               "mean_cov_drop\n")
+
+
+def iteration_row(scenario: str, it: int, rec: dict) -> str:
+    """One iterations-CSV line exactly as report.cpp:60-70 formats it (fmt6 = %.6f)."""
+    vals = [rec[k] for k in ("iter_ms", "imbalance", "max_mb_ms", "mean_mb_ms", "bubble_ms", "dst_overhead_ms",
+                             "avg_budget", "mean_cov_drop")]
+    return f"{scenario},{it}," + ",".join("%.6f" % float(v) for v in vals) + "\n"
+
+
+def summarize(mb_ms: list[list[float]]) -> dict:
+    """Per-(rank, micro-batch) measured totals -> the ScheduleResult fields (sim.cpp:448-485)."""
+    flat = [t for r in mb_ms for t in r]
+    mean_all = sum(flat) / len(flat) if flat else 0.0
+    max_all = max(flat) if flat else 0.0
+    return dict(iter_ms=max((sum(r) for r in mb_ms), default=0.0), max_mb_ms=max_all, mean_mb_ms=mean_all,
+                imbalance=max_all / mean_all if mean_all > 0.0 else 1.0, bubble_ms=0.0)
+
+
+class Driver:
+    def __init__(self, strategy="sab_dst", gbs=16, mbs=2, layers=4, block=128, heads=32, kv_heads=32, head_dim=128,
+                 seed=42, dist_spec=None, table: ProfileTable | None = None, anchor="mean", threshold_p=0.1,
+                 dst_scope="global", base_mode="coverage", rank=0, world=1, group=None, device="cuda"):
+        self.h = api()
+        self.strategy, self.gbs, self.mbs, self.layers, self.B = strategy, gbs, mbs, layers, block
+        self.H, self.Hkv, self.D = heads, kv_heads, head_dim
+        self.seed, self.dist_spec = seed, dist_spec
+        self.rank, self.world, self.group, self.device = rank, world, group, device
+        self.table = table if table is not None else self.h.synthesize_table(block_size=block)
+        self.grid = list(self.table.budget_grid) if table is not None else list(DEFAULT_BUDGET_GRID)
+        max_len = int((dist_spec or {}).get("max_length", 65536))
+        self.est = self.h.make_estimator(self.h.default_bin_edges(max_len), budget_grid=self.grid)
+        self.plan_kw = dict(anchor=anchor, threshold_p=threshold_p, dst_scope=dst_scope, base_mode=base_mode)
+        self._buf_T = 0
+        # Per-layer softmax temperature, so layers differ as real layers do (fixed seed).
+        self.layer_scales = np.exp(np.random.default_rng(seed).uniform(-0.5, 1.0, size=layers))
+
+    def _buffers(self, T: int):
+        if T > self._buf_T:
+            g = torch.Generator(device=self.device).manual_seed(self.seed + self.rank)
+            mk = lambda h: torch.randn((T, h, self.D), generator=g, device=self.device).to(torch.bfloat16)  # noqa: E731
+            self.q, self.k, self.v, self.do = mk(self.H), mk(self.Hkv), mk(self.Hkv), mk(self.H)
+            self._buf_T = T
+        return self.q[:T], self.k[:T], self.v[:T], self.do[:T]
+
+    def _run_micro_batch(self, lengths: np.ndarray, budgets: np.ndarray) -> float:
+        cu = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+        T = int(cu[-1])
+        lay = ops.VarlenLayout.build(cu, self.B, device=self.device)
+        q, k, v, do = self._buffers(T)
+        nb = lay.nb_per_seq
+        k_all = torch.from_numpy(np.minimum(budgets[:, None], nb[None, :]).astype(np.int32)).to(self.device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        qbar, kbar = ops.block_pool(q, lay), ops.block_pool(k, lay)
+        for l in range(self.layers):
+            scale = float(self.layer_scales[l]) / math.sqrt(self.D)
+            S = ops.block_scores(q, k, lay, scale, qbar=qbar, kbar=kbar)
+            k_max = int(max(1, min(int(budgets[l]), int(nb.max()))))
+            idx, cnt = ops.topk_select(S, lay, k_all[l], k_max, group=self.H // self.Hkv)
+            o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+            ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    def iteration(self, it: int, decisions_csv=None, plan_json=None) -> dict:
+        lengths, profs = self.h.generate_samples(self.gbs, self.layers, self.B, seed=mix_seed(self.seed, it),
+                                                 dist=self.dist_spec)
+        t0 = time.perf_counter()
+        sp = self.h.plan_step(self.strategy, np.arange(self.gbs), lengths, profs, gbs=self.gbs, mbs=self.mbs,
+                              dp=self.world, num_layers=self.layers, table=self.table, est=self.est, iter_index=it,
+                              decisions_csv=decisions_csv, plan_json=plan_json, **self.plan_kw)
+        host_ms = (time.perf_counter() - t0) * 1e3
+        mine = []
+        for m, ids in enumerate(sp["micro_batch_bins"][self.rank]):
+            mine.append(self._run_micro_batch(np.asarray(lengths)[ids], sp["budgets"][self.rank][m]))
+        if self.world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor(mine, dtype=torch.float64, device=self.device)
+            outs = [torch.zeros_like(t) for _ in range(self.world)]
+            dist.all_gather(outs, t, group=self.group)
+            mb_ms = [o.cpu().tolist() for o in outs]
+        else:
+            mb_ms = [mine]
+        rec = summarize(mb_ms)
+        rec.update(dst_overhead_ms=host_ms, avg_budget=sp["avg_budget"], mean_cov_drop=sp["mean_cov_drop"],
+                   mb_ms=mb_ms)
+        return rec
+
+    def run(self, iters: int, out_dir: str | None = None):
+        records = []
+        if out_dir and self.rank == 0:
+            os.makedirs(out_dir, exist_ok=True)
+        for it in range(iters):
+            files = {}
+            if out_dir and self.rank == 0:
+                files = dict(decisions_csv=os.path.join(out_dir, f"decisions_{it}.csv"),
+                             plan_json=os.path.join(out_dir, f"plan_{it}.json"))
+            records.append(self.iteration(it, **files))
+        if out_dir and self.rank == 0:
+            with open(os.path.join(out_dir, "iterations.csv"), "w") as f:
+                f.write(ITER_HEADER)
+                for it, rec in enumerate(records):
+                    f.write(iteration_row(self.strategy, it, rec))
+        return records
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
+    ap.add_argument("--strategy", default="sab_dst", choices=["baseline", "dst", "sab", "lbb", "sab_dst", "lbb_dst"])
+    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--gbs-per-rank", type=int, default=5)
+    ap.add_argument("--mbs", type=int, default=5)
+    ap.add_argument("--layers", type=int, default=36)
+    ap.add_argument("--mix", default="40/60", help="'40/60' = the C3 40%% 32K / 60%% 2K bimodal mix; 'default' = "
+                                                   "the reference generator's default distribution")
+    ap.add_argument("--table", default=None, help="cost table CSV (x,k,latency_ms), e.g. from profiler.py")
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist_spec = None
+    if args.mix == "40/60":
+        dist_spec = dict(short_weight=0.6, short_log_mean=float(np.log(2048)), short_log_sigma=0.0,
+                         long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
+    table = api().load_table(args.table)[0] if args.table else None
+    drv = Driver(args.strategy, gbs=args.gbs_per_rank * world, mbs=args.mbs, layers=args.layers, dist_spec=dist_spec,
+                 table=table, rank=rank, world=world, device=torch.device("cuda", local))
+    recs = drv.run(args.iters, args.out)
+    if rank == 0:
+        for it, r in enumerate(recs):
+            print(iteration_row(args.strategy, it, r), end="")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -297,7 +297,8 @@ class HostAPI:
     def plan_step(self, strategy: str, ids, lengths, profiles, *, gbs: int, mbs: int, dp: int, num_layers: int,
                   table: ProfileTable, est: SparsityEstimator, iter_index: int = 0, base_budget: int = 32,
                   base_mode: str = "coverage", base_coverage_target: float = 0.9, dst_scope: str = "global",
-                  threshold_p: float = 0.1, anchor: str = "min", dst_grid=None, calibrate_every: int = 1):
+                  threshold_p: float = 0.1, anchor: str = "min", dst_grid=None, calibrate_every: int = 1,
+                  decisions_csv: str | None = None, plan_json: str | None = None):
         n = len(ids)
         flat, off = _flatten([p for s in profiles for p in s])
         setup_i = _a([gbs, mbs, dp, num_layers, base_budget, 1 if base_mode == "coverage" else 0,
@@ -317,7 +318,9 @@ class HostAPI:
                    _p(off), _p(setup_i), _p(setup_d), ANCHORS[anchor], _p(grid if grid.size else np.zeros(1, np.int32)),
                    len(grid), _p(est.bin_edges), len(est.bin_edges), _p(est.ema_budget), C.c_double(est.ema_alpha),
                    _p(est.budget_grid), len(est.budget_grid), *table.args(), iter_index, _p(out_b), _p(out_ids),
-                   _p(out_off), _p(oi), _p(od), cap, C.byref(nd), _p(stats))
+                   _p(out_off), _p(oi), _p(od), cap, C.byref(nd), _p(stats),
+                   None if decisions_csv is None else str(decisions_csv).encode(),
+                   None if plan_json is None else str(plan_json).encode())
         decisions = []
         for i in range(nd.value):
             a, d = oi[6 * i:6 * i + 6], od[3 * i:3 * i + 3]

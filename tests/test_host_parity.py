@@ -6,6 +6,9 @@ so any reordering of a sum would eventually flip a k_final. CPU only. Skipped wh
 reference library is unavailable (the GPU box); tests/test_host_golden.py covers the same
 surface from committed fixtures there.
 """
+import json
+import re
+
 import numpy as np
 import pytest
 
@@ -246,3 +249,34 @@ def test_plan_step_config3_shape(host, ref):
         a = host.plan_step("sab_dst", np.arange(40), lengths, profs, est=est_a, **kw)
         b = ref.plan_step("sab_dst", np.arange(40), lengths, profs, est=est_b, **kw)
         assert a["decisions"] == b["decisions"] and np.array_equal(a["budgets"], b["budgets"])
+
+
+@pytest.mark.parametrize("strategy", ["baseline", "dst", "sab_dst", "lbb_dst"])
+def test_plan_step_replay_files_byte_identical(host, ref, strategy, tmp_path):
+    """The step's replay files -- decisions CSV (dst.cpp:171-185) and plan JSON
+    (sab.cpp:312-336) -- written by this build and by the reference's own writers are
+    byte-identical, over iterations (estimator state evolving)."""
+    table = host.synthesize_table(block_size=128)
+    gbs, mbs, dp, nl = 16, 2, 2, 4
+    est_a = host.make_estimator(host.default_bin_edges(65536))
+    est_b = host.make_estimator(host.default_bin_edges(65536))
+    for it in range(3):
+        lengths, profs = host.generate_samples(gbs, nl, 128, seed=2000 + it)
+        kw = dict(gbs=gbs, mbs=mbs, dp=dp, num_layers=nl, table=table, iter_index=it, anchor="mean",
+                  threshold_p=0.1)
+        pa = {k: tmp_path / f"a_{it}.{k}" for k in ("csv", "json")}
+        pb = {k: tmp_path / f"b_{it}.{k}" for k in ("csv", "json")}
+        host.plan_step(strategy, np.arange(gbs), lengths, profs, est=est_a, decisions_csv=pa["csv"],
+                       plan_json=pa["json"], **kw)
+        ref.plan_step(strategy, np.arange(gbs), lengths, profs, est=est_b, decisions_csv=pb["csv"],
+                      plan_json=pb["json"], **kw)
+        assert pa["csv"].read_bytes() == pb["csv"].read_bytes(), (strategy, it)
+        assert pa["csv"].read_text().startswith("iter,mb,layer,k_base,k_anchor,k_final,cov_drop,dir,")
+        # Plan JSON: identical documents. Byte layout: this build writes upstream nlohmann 3.11.3's
+        # dump(2) (every array expanded); the oracle build's header is cudnn-frontend's copy, whose
+        # "Custom from FE" patch (json.hpp:20610) prints integer arrays on one line -- so compare
+        # bytes after collapsing integer arrays.
+        ta, tb = pa["json"].read_text(), pb["json"].read_text()
+        assert json.loads(ta) == json.loads(tb)
+        collapse = re.compile(r"\[\s*(-?\d+(?:,\s*-?\d+)*)\s*\]")
+        assert collapse.sub(lambda m: "[" + ",".join(x.strip() for x in m.group(1).split(",")) + "]", ta) == tb
