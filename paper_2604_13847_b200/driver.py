@@ -87,6 +87,7 @@ class Driver:
         self.est = self.h.make_estimator(self.h.default_bin_edges(max_len), budget_grid=self.grid)
         self.plan_kw = dict(anchor=anchor, threshold_p=threshold_p, dst_scope=dst_scope, base_mode=base_mode)
         self._buf_T = 0
+        self._warm = False
         # Per-layer softmax temperature, so layers differ as real layers do (fixed seed).
         self.layer_scales = np.exp(np.random.default_rng(seed).uniform(-0.5, 1.0, size=layers))
 
@@ -105,19 +106,25 @@ class Driver:
         q, k, v, do = self._buffers(T)
         nb = lay.nb_per_seq
         k_all = torch.from_numpy(np.minimum(budgets[:, None], nb[None, :]).astype(np.int32)).to(self.device)
+        if not self._warm:  # first micro-batch: one untimed pass so allocator / module load stay out of the timing
+            self._layers(q, k, v, do, lay, nb, k_all, budgets, 1)
+            self._warm = True
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        self._layers(q, k, v, do, lay, nb, k_all, budgets, self.layers)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    def _layers(self, q, k, v, do, lay, nb, k_all, budgets, n_layers):
         qbar, kbar = ops.block_pool(q, lay), ops.block_pool(k, lay)
-        for l in range(self.layers):
+        for l in range(n_layers):
             scale = float(self.layer_scales[l]) / math.sqrt(self.D)
             S = ops.block_scores(q, k, lay, scale, qbar=qbar, kbar=kbar)
             k_max = int(max(1, min(int(budgets[l]), int(nb.max()))))
             idx, cnt = ops.topk_select(S, lay, k_all[l], k_max, group=self.H // self.Hkv)
             o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
             ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1)
 
     def iteration(self, it: int, decisions_csv=None, plan_json=None) -> dict:
         lengths, profs = self.h.generate_samples(self.gbs, self.layers, self.B, seed=mix_seed(self.seed, it),
