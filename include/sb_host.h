@@ -97,8 +97,9 @@ int SBH(plan_batching)(int strategy, int n, const int64_t* ids, const int64_t* l
 
 /* step.hpp: plan_step (reference: the decision half of simulate_iteration).
  * samples: n = gbs, ids, lengths, profiles sample-major with off[(s*nl)+l].
- * setup_i[8] = {gbs, mbs, dp, num_layers, base_budget, base_mode(0 fixed,1 coverage),
- *               dst_scope(0 rank,1 global), calibrate_every}
+ * setup_i[9] = {gbs, mbs, dp, num_layers, base_budget, base_mode(0 fixed,1 coverage),
+ *               dst_scope(0 rank,1 global), calibrate_every, varlen_block_size (0 = the
+ *               reference's summed-length cost; > 0 = predict_members at that block size)}
  * setup_d[2] = {base_coverage_target, threshold_p}; anchor 0/1/2; dst grid (may be empty).
  * estimator: edges[ne], ema_inout[ne], alpha, est grid.
  * Outputs: out_budgets[dp * mpr * nl] ([rank][mb][layer]); out_ids / out_mb_off as in
@@ -107,6 +108,12 @@ int SBH(plan_batching)(int strategy, int n, const int64_t* ids, const int64_t* l
  * avg_budget}. decisions_csv_path / plan_json_path (nullable): the step's replay files in
  * the reference formats (write_decisions_csv dst.cpp:171-185 with iter = iter_index,
  * save_plan_json sab.cpp:312-336). */
+/* Varlen-aware micro-batch cost (opt-in, not in the reference):
+ * sum over members of predict(L_s, min(k, ceil(L_s / block_size))). */
+int SBH(predict_members)(const int64_t* bins, int nx, const int* grid, int nk, const double* lat,
+                         const int64_t* lengths, int n, int k, int block_size, double* out_ms,
+                         int* out_extrapolated);
+
 int SBH(plan_step)(int strategy, int n, const int64_t* ids, const int64_t* lengths,
                    const double* profiles, const int64_t* off, const int* setup_i,
                    const double* setup_d, int anchor, const int* dst_grid, int n_dst_grid,

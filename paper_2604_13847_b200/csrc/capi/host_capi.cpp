@@ -423,6 +423,24 @@ SB_EXPORT int SBH(plan_batching)(int strategy, int n, const int64_t* ids, const 
   });
 }
 
+SB_EXPORT int SBH(predict_members)(const int64_t* bins, int nx, const int* grid, int nk, const double* lat,
+                                   const int64_t* lengths, int n, int k, int block_size, double* out_ms,
+                                   int* out_extrapolated) {
+  return guarded([&] {
+#ifdef SB_REF
+    (void)bins, (void)nx, (void)grid, (void)nk, (void)lat, (void)lengths, (void)n, (void)k, (void)block_size;
+    (void)out_ms, (void)out_extrapolated;
+    throw sb::ConfigError("predict_members is not in the reference");
+#else
+    const auto table = make_table(bins, nx, grid, nk, lat);
+    const auto e = sb::predict_members(table, std::span<const int64_t>(lengths, static_cast<std::size_t>(n)), k,
+                                       block_size);
+    *out_ms = e.value_ms;
+    *out_extrapolated = e.extrapolated ? 1 : 0;
+#endif
+  });
+}
+
 SB_EXPORT int SBH(plan_step)(int strategy, int n, const int64_t* ids, const int64_t* lengths,
                              const double* profiles, const int64_t* off, const int* setup_i,
                              const double* setup_d, int anchor, const int* dst_grid,
@@ -443,6 +461,11 @@ SB_EXPORT int SBH(plan_step)(int strategy, int n, const int64_t* ids, const int6
     dcfg.threshold_p = setup_d[1];
     dcfg.anchor = anchor_of(anchor);
     dcfg.budget_grid.assign(dst_grid, dst_grid + n_dst_grid);
+#ifdef SB_REF
+    if (setup_i[8] != 0) throw sb::ConfigError("plan_step: varlen cost is not in the reference");
+#else
+    dcfg.varlen_block_size = setup_i[8];
+#endif
     if (strategy < 0 || strategy > 5) throw sb::ConfigError("plan_step: strategy out of range");
     const auto strat = static_cast<sb::Strategy>(strategy);
     const auto base_mode = setup_i[5] ? sb::BaseBudgetMode::kCoverage : sb::BaseBudgetMode::kFixed;

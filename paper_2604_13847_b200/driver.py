@@ -75,7 +75,8 @@ def summarize(mb_ms: list[list[float]]) -> dict:
 class Driver:
     def __init__(self, strategy="sab_dst", gbs=16, mbs=2, layers=4, block=128, heads=32, kv_heads=32, head_dim=128,
                  seed=42, dist_spec=None, table: ProfileTable | None = None, anchor="mean", threshold_p=0.1,
-                 dst_scope="global", base_mode="coverage", rank=0, world=1, group=None, device="cuda"):
+                 dst_scope="global", base_mode="coverage", varlen_block_size=0, rank=0, world=1, group=None,
+                 device="cuda"):
         self.h = api()
         self.strategy, self.gbs, self.mbs, self.layers, self.B = strategy, gbs, mbs, layers, block
         self.H, self.Hkv, self.D = heads, kv_heads, head_dim
@@ -85,7 +86,8 @@ class Driver:
         self.grid = list(self.table.budget_grid) if table is not None else list(DEFAULT_BUDGET_GRID)
         max_len = int((dist_spec or {}).get("max_length", 65536))
         self.est = self.h.make_estimator(self.h.default_bin_edges(max_len), budget_grid=self.grid)
-        self.plan_kw = dict(anchor=anchor, threshold_p=threshold_p, dst_scope=dst_scope, base_mode=base_mode)
+        self.plan_kw = dict(anchor=anchor, threshold_p=threshold_p, dst_scope=dst_scope, base_mode=base_mode,
+                            varlen_block_size=varlen_block_size)
         self._buf_T = 0
         self._warm = False
         # Per-layer softmax temperature, so layers differ as real layers do (fixed seed).
@@ -179,6 +181,7 @@ def main():
     ap.add_argument("--mix", default="40/60", help="'40/60' = the C3 40%% 32K / 60%% 2K bimodal mix; 'default' = "
                                                    "the reference generator's default distribution")
     ap.add_argument("--table", default=None, help="cost table CSV (x,k,latency_ms), e.g. from profiler.py")
+    ap.add_argument("--varlen", action="store_true", help="opt-in varlen-aware DST cost (predict_members at B)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
@@ -194,7 +197,8 @@ def main():
                          long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
     table = api().load_table(args.table)[0] if args.table else None
     drv = Driver(args.strategy, gbs=args.gbs_per_rank * world, mbs=args.mbs, layers=args.layers, dist_spec=dist_spec,
-                 table=table, rank=rank, world=world, device=torch.device("cuda", local))
+                 table=table, varlen_block_size=128 if args.varlen else 0, rank=rank, world=world,
+                 device=torch.device("cuda", local))
     recs = drv.run(args.iters, args.out)
     if rank == 0:
         for it, r in enumerate(recs):

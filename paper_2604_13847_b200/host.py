@@ -124,6 +124,15 @@ class HostAPI:
         self._call("predict", *table.args(), C.c_int64(x), C.c_int(k), C.byref(ms), C.byref(ex))
         return ms.value, bool(ex.value)
 
+    def predict_members(self, table: ProfileTable, lengths, k: int, block_size: int):
+        """Opt-in varlen-aware cost (not in the reference): sum over members of
+        predict(L_s, min(k, ceil(L_s / block_size)))."""
+        ms, ex = C.c_double(), C.c_int()
+        la = _a(lengths, np.int64)
+        self._call("predict_members", *table.args(), _p(la), len(la), int(k), int(block_size), C.byref(ms),
+                   C.byref(ex))
+        return ms.value, bool(ex.value)
+
     def align(self, table: ProfileTable, x: int, target_ms: float):
         b, inf = C.c_int(), C.c_int()
         self._call("align", *table.args(), C.c_int64(x), C.c_double(target_ms), C.byref(b), C.byref(inf))
@@ -298,11 +307,11 @@ class HostAPI:
                   table: ProfileTable, est: SparsityEstimator, iter_index: int = 0, base_budget: int = 32,
                   base_mode: str = "coverage", base_coverage_target: float = 0.9, dst_scope: str = "global",
                   threshold_p: float = 0.1, anchor: str = "min", dst_grid=None, calibrate_every: int = 1,
-                  decisions_csv: str | None = None, plan_json: str | None = None):
+                  decisions_csv: str | None = None, plan_json: str | None = None, varlen_block_size: int = 0):
         n = len(ids)
         flat, off = _flatten([p for s in profiles for p in s])
         setup_i = _a([gbs, mbs, dp, num_layers, base_budget, 1 if base_mode == "coverage" else 0,
-                      1 if dst_scope == "global" else 0, calibrate_every], np.int32)
+                      1 if dst_scope == "global" else 0, calibrate_every, varlen_block_size], np.int32)
         setup_d = _a([base_coverage_target, threshold_p], np.float64)
         grid = _a([] if dst_grid is None else dst_grid, np.int32)
         mpr = gbs // (mbs * dp)
