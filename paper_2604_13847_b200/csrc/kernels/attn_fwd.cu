@@ -316,8 +316,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         const int b = g & 1;
         const uint32_t t_s = tmem + lane_field + (b ? C::kTmemS1 : C::kTmemS0);
         const int jb = __ldg(w.list + j);
-        mbar_wait(&bars->s_full[b], (g >> 1) & 1);
+        mbar_wait_spin(&bars->s_full[b], (g >> 1) & 1);
         if (threadIdx.x == 64) tr(4, g);
+        if (trace != nullptr && blockIdx.x == 0 && g < 256 && lane == 0)  // per-warp S seen (debug)
+          trace[3072 + g * 4 + (warp - 2)] = clock64();
         tc_fence_after();
         uint32_t sv[B / 32][32];
 #pragma unroll
@@ -357,6 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         }
         m_run = m_use;
         tc_fence_before();
+        if (trace != nullptr && blockIdx.x == 0 && g < 256 && lane == 0)  // per-warp arrival (debug)
+          trace[2048 + g * 4 + (warp - 2)] = clock64();
         mbar_arrive(&bars->p_full[b]);
       }
       // Epilogue: wait for the item's last PV, O / l -> bf16 rows; LSE (natural log).
@@ -422,7 +426,7 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
 }  // namespace
 }  // namespace sbk
 
-// Debug only: device buffer of 256 x 8 uint64 for CTA 0's phase timeline (NULL disables).
+// Debug only: device buffer of 256 x 16 uint64 for CTA 0's phase timeline (NULL disables).
 SB_API void sb_debug_set_trace(unsigned long long* buf) { sbk::g_trace = buf; }
 
 SB_API size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq, int k_max) {

@@ -63,6 +63,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait_sleep(bar, parity)) {
   }
 }
+// try_wait without a suspend-time hint (the hardware's default suspend window): for the
+// latency-critical softmax waits on a freshly committed S tile.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {

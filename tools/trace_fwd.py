@@ -13,12 +13,15 @@ g = torch.Generator(device="cuda").manual_seed(0)
 q, k, v = (torch.randn((T, H, D), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
 S = ops.block_scores(q, k, lay)
 idx, cnt = ops.topk_select(S, lay, torch.from_numpy(k_seq).cuda(), int(k_seq.max()))
-buf = torch.zeros(256 * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(256 * 16, dtype=torch.int64, device="cuda")
 for it in range(3):
     lib.sb_debug_set_trace(ctypes.c_void_p(buf.data_ptr() if it == 2 else 0))
     ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)
 torch.cuda.synchronize()
-t = buf.cpu().numpy().reshape(256, 8).astype(np.int64)
+allb = buf.cpu().numpy().astype(np.int64)
+t = allb[:2048].reshape(256, 8)
+pw = allb[2048:3072].reshape(256, 4)
+ps = allb[3072:].reshape(256, 4)
 base = t[0, 0]
 names = ["mma:before k_full", "mma:k ready/QK issue", "mma:PV v ready", "mma:PV p_full seen", "smx:S ready", "smx:P done", "smx:o_done seen"]
 print("g  " + " | ".join(f"{n:>20s}" for n in names))
@@ -36,3 +39,6 @@ print("median v_full -> p_full seen:", np.median(t[r, 3] - t[r, 2]))
 print("median p_full seen -> next before-k_full:", np.median(t[3:59, 0] - t[2:58, 3]))
 print("median S ready after QK issue:", np.median(t[r, 4] - t[r, 1]))
 print("median o_done wait (P done -> o_done seen):", np.median(t[r, 6] - t[r, 5]))
+print("per-warp arrival relative to warp 2 (warps 2..5), median over blocks:", [float(np.median(pw[4:40, w] - pw[4:40, 0])) for w in range(4)])
+print("per-warp S seen relative to warp 2:", [float(np.median(ps[4:40, w] - ps[4:40, 0])) for w in range(4)])
+print("per-warp busy (arrive - S seen):", [float(np.median(pw[4:40, w] - ps[4:40, w])) for w in range(4)])
