@@ -12,6 +12,14 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return r;
 }
 
+__device__ __forceinline__ void ex2_h2(float a, float b, float& ra, float& rb) {
+  uint32_t h, r;
+  asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(h));
+  asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
+      : "=f"(ra), "=f"(rb) : "r"(r));
+}
+
 template <int MODE>
 __global__ void k(int iters, float seed, unsigned long long* out, float* sink) {
   float x[16];
@@ -37,6 +45,11 @@ __global__ void k(int iters, float seed, unsigned long long* out, float* sink) {
         f2 p = ffma2(mk2(x[i], x[i + 1]), mk2(0.999f, 0.999f), mk2(0.001f, 0.001f));
         x[i] = p.x;
         x[i + 1] = p.y;
+      } else if (MODE == 5) {  // f16x2 MUFU exp2 pair with f32 in/out
+        float a, b;
+        ex2_h2(x[i], x[i + 1], a, b);
+        x[i] = a - 1.0f;
+        x[i + 1] = b - 1.0f;
       } else if (MODE == 4) {  // the softmax mix per pair: FFMA2, 2 MUFU (5/8) or poly (3/8), FADD2, cvt
         const int e = i / 2 + it;
         f2 p = ex2_pair(ffma2(mk2(x[i], x[i + 1]), mk2(0.5f, 0.5f), mk2(-1.f, -1.f)), i / 2);
@@ -74,5 +87,6 @@ int main() {
   for (int w : {4, 8, 16}) run<2>("cvt.rn.bf16x2 (per elem)", w);
   for (int w : {4, 8, 16}) run<3>("FFMA2 (per elem)", w);
   for (int w : {4, 8, 16}) run<4>("softmax mix (per elem)", w);
+  for (int w : {4, 8, 16}) run<5>("ex2.approx.f16x2 (f32 io)", w);
   return 0;
 }
