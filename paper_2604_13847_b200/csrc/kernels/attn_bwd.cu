@@ -267,7 +267,7 @@ struct DkvBars {
   uint64_t do_full[kStages], do_empty[kStages];  // dO_i (+ its augmented slice) ring
   uint64_t st_full, dpt_full;  // UMMA -> math: S^T / dP^T in TMEM
   uint64_t st_free;            // math -> UMMA: S^T read into registers (the next S^T may overwrite)
-  uint64_t pds_full;           // math -> UMMA: P^T and dS^T (bf16) packed over dP^T's columns
+  uint64_t pds_part[2];        // math -> UMMA: P^T and dS^T (bf16) of 32-column chunk c2 packed over dP^T
   uint64_t acc_done;           // UMMA -> epilogue: the item's dV / dK are final
   uint32_t tmem_base;
 };
@@ -343,7 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     mbar_init(&bars->st_full, 1);
     mbar_init(&bars->dpt_full, 1);
     mbar_init(&bars->st_free, 256);
-    mbar_init(&bars->pds_full, 256);
+    mbar_init(&bars->pds_part[0], 256);
+    mbar_init(&bars->pds_part[1], 256);
     mbar_init(&bars->acc_done, 1);
     fence_barrier_init();
   }
@@ -512,13 +513,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         for (int m = 0; m < items; ++m, ++g) {
           if (m + 1 < items) issue_st(g + 1);
           tr(0, g);
-          mbar_wait(&bars->pds_full, g & 1);
-          tr(1, g);
-          tc_fence_after();
+          // dK first (Q_i is the ring the next S^T waits on), in two K halves: the K steps of
+          // chunk c2 go as soon as both warpgroups packed that chunk's P^T / dS^T.
 #pragma unroll
-          for (int kk = 0; kk < B / 16; ++kk)  // dK first: Q_i is the ring the next S^T waits on
-            mma_ts(tmem + C::kDK, tmem + C::kDPt + pds_col<B>(kk) + 16, desc_sw128(qa(g) + kk * 2048, B * 128, 1024),
-                   idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
+          for (int c2 = 0; c2 < B / 64; ++c2) {
+            mbar_wait(&bars->pds_part[c2], g & 1);
+            if (c2 == 0) tr(1, g);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < B / 16; ++kk) {
+              if (((kk % (B / 32)) >> 1) != c2) continue;
+              mma_ts(tmem + C::kDK, tmem + C::kDPt + pds_col<B>(kk) + 16,
+                     desc_sw128(qa(g) + kk * 2048, B * 128, 1024), idesc_acc, (m > 0 || c2 > 0 || kk > 0) ? 1u : 0u,
+                     leader);
+            }
+          }
           tc_commit(&bars->q_empty[g % kStages], leader);
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
@@ -567,7 +576,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
 #ifdef SB_DKV_NOMATH  // timing experiment only: UMMA stream without the math
         mbar_arrive(&bars->st_free);
         mbar_wait(&bars->dpt_full, g & 1);
-        mbar_arrive(&bars->pds_full);
+        mbar_arrive(&bars->pds_part[0]);
+        if (B / 64 > 1) mbar_arrive(&bars->pds_part[1]);
         continue;
 #endif
         float p[HB];
@@ -608,13 +618,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
             }
             tmem_st16(tmem + lf + dpt_col + c2 * 32, pw);
             tmem_st16(tmem + lf + dpt_col + c2 * 32 + 16, dd);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bars->pds_part[c2]);
             if (c2 + 1 < HB / 32) tmem_wait_ld();
           }
         }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&bars->pds_full);
-        if (threadIdx.x == 64) tr(7, g);
         if (threadIdx.x == 64) tr(7, g);
       }
       if (items > 0) {
@@ -691,7 +700,8 @@ struct DqCfg {
 struct DqBars {
   uint64_t stage_full, stage_empty;  // Q / dO staging buffer (TMA -> tcgen05.cp)
   uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
-  uint64_t s_full, s_free, dp_full, ds_full, dq_done, dq_free;
+  uint64_t s_full, s_free, dp_full, dq_done, dq_free;
+  uint64_t ds_part[2];  // math -> UMMA: dS of 32-column chunk c2 (of both halves) packed in TMEM
   uint32_t tmem_base;
 };
 
@@ -740,7 +750,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->s_free, 256);
     mbar_init(&bars->dp_full, 1);
-    mbar_init(&bars->ds_full, 256);
+    mbar_init(&bars->ds_part[0], 256);
+    mbar_init(&bars->ds_part[1], 256);
     mbar_init(&bars->dq_done, 1);
     mbar_init(&bars->dq_free, 256);
     fence_barrier_init();
@@ -899,16 +910,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
           issue_s(g + 1);
         }
         tr(0, g);
-        mbar_wait(&bars->ds_full, g & 1);
-        tr(1, g);
-        tc_fence_after();
-        if (j == 0) mbar_wait(&bars->dq_free, (q & 1) ^ 1);  // previous item's dQ read out
         const int st = g % kKS;
+        // dQ_g in two K halves: the K steps of dS chunk c2 go as soon as both warpgroups packed
+        // that chunk, so half of the dS tail overlaps the UMMA.
 #pragma unroll
-        for (int kk = 0; kk < B / 16; ++kk)
-          mma_ts(tmem + C::kDQ, tmem + C::kDP + packed_col<B>(kk),
-                 desc_sw128(k_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024), idesc_dq, (j > 0 || kk > 0) ? 1u : 0u,
-                 leader);
+        for (int c2 = 0; c2 < B / 64; ++c2) {
+          mbar_wait(&bars->ds_part[c2], g & 1);
+          if (c2 == 0) tr(1, g);
+          tc_fence_after();
+          if (j == 0 && c2 == 0) mbar_wait(&bars->dq_free, (q & 1) ^ 1);  // previous item's dQ read out
+#pragma unroll
+          for (int kk = 0; kk < B / 16; ++kk) {
+            if (((kk % (B / 32)) >> 1) != c2) continue;
+            mma_ts(tmem + C::kDQ, tmem + C::kDP + packed_col<B>(kk),
+                   desc_sw128(k_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024), idesc_dq,
+                   (j > 0 || c2 > 0 || kk > 0) ? 1u : 0u, leader);
+          }
+        }
         tc_commit(&bars->k_empty[st], leader);
         if (last) tc_commit(&bars->dq_done, leader);
         tr(6, g);
@@ -987,12 +1005,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
               dsp[e / 2] = pack_bf16x2(ds.x, ds.y);
             }
             tmem_st16(tmem + lf + dp_col + c2 * 16, dsp);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bars->ds_part[c2]);
             if (c2 + 1 < HB / 32) tmem_wait_ld();
           }
         }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&bars->ds_full);
         if (threadIdx.x == 64) tr(11, g);
       }
       mbar_wait(&bars->dq_done, q & 1);
