@@ -87,6 +87,17 @@ int sb_coverage_profile(const float* scores, const int32_t* blk_off, const int64
 int sb_coverage_at_grid(const double* profile, const int32_t* blk_off, int nseq, int nb_max,
                         const int32_t* grid, int ngrid, double* coverage, void* stream);
 
+/* K8: on-device DST decision, fixed-base mode. For micro-batch i =
+ * sequences [mb_off[i], mb_off[i+1]): merges the members' K4 profiles (profile [nseq][nb_max],
+ * one layer) exactly as make_micro_batch (workload.cpp:64-99) and applies tune_budget's rule
+ * (dst.cpp:107-143) with the host-precomputed k_base[i], k_anchor[i] = align(x_i, anchor) and
+ * bottleneck[i] = (predict(x_i, k_base_i) > anchor): k_final[i], coverage_drop[i] bit-exact
+ * with the host, and k_seq[s] = min(k_final, nb_s) for the selector. Device pointers. */
+int sb_dst_decide(const double* profile, const int32_t* blk_off, const int32_t* cu_seqlens, int nb_max,
+                  const int32_t* mb_off, int n_mb, const int32_t* k_base, const int32_t* k_anchor,
+                  const int32_t* bottleneck, const int32_t* grid, int ngrid, double threshold_p,
+                  int32_t* k_final, double* coverage_drop, int32_t* k_seq, void* stream);
+
 /* K5: O = softmax(scale * Q K[I]^T) V[I] over the selected blocks of each q block, causal
  * inside the diagonal block, keys beyond the sequence end masked. Saves LSE (natural log).
  * tcgen05/TMEM tensor-core kernel with TMA-loaded K/V blocks; persistent, longest-item-first

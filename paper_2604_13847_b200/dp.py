@@ -130,6 +130,22 @@ def decide_budgets(pooled, table: ProfileTable, cfg: DstSettings, num_layers: in
     return k_final, decisions, np.asarray(k_base), np.asarray(xs)
 
 
+def fixed_base_plan(table: ProfileTable, xs, k_base, cfg: DstSettings):
+    """Host half of the on-device DST (fixed-base mode).
+
+    Everything tune_budget needs except the profile follows from the pooled micro-batches'
+    summed lengths and fixed base budgets (dst.cpp:107-169): T_base = predict(x, k_base), the
+    anchor over all of them, k_anchor = align(x, anchor) and the bottleneck flag. Identical on
+    every rank with no collective; the coverage test then runs on the device per layer
+    (ops.dst_decide)."""
+    h = api()
+    base_ms = [h.predict(table, int(x), int(kb))[0] for x, kb in zip(xs, k_base)]
+    anchor = h.select_anchor(base_ms, cfg.anchor)
+    k_anchor = [h.align(table, int(x), anchor)[0] for x in xs]
+    bottleneck = [1 if t > anchor else 0 for t in base_ms]
+    return np.asarray(k_anchor, np.int32), np.asarray(bottleneck, np.int32), anchor
+
+
 class DPStep:
     """One rank's hot-path step over its micro-batch for `num_layers` layers.
 
@@ -138,7 +154,8 @@ class DPStep:
     budgets -- differ as they do across real layers."""
 
     def __init__(self, batch: RankBatch, q, k, v, do, layer_scales, table: ProfileTable, cfg: DstSettings,
-                 rank: int = 0, world: int = 1, group=None, width: int | None = None, routing_profiles=None):
+                 rank: int = 0, world: int = 1, group=None, width: int | None = None, routing_profiles=None,
+                 pooled_xs=None):
         """routing_profiles (optional): per-layer, per-member RoutingProfiles to feed the tuner
         instead of the GPU coverage profiles -- e.g. the reference workload generator's own
         routing scores for these samples (workload.cpp:239-271), which carry the reference's
@@ -152,6 +169,23 @@ class DPStep:
         self.width = width if width is not None else int(batch.layout.nb_max)
         self.routing_profiles = routing_profiles
         self.last = {}
+        # On-device DST (fixed-base mode): with every rank's micro-batch
+        # summed length known (the SAB plan is deterministic on every rank), the host half
+        # (k_anchor, bottleneck) is computed here once and the per-layer coverage test runs on the
+        # device: no profile download, no all-gather, no per-layer host round trip.
+        self.on_device = pooled_xs is not None
+        if self.on_device:
+            if cfg.base_mode != "fixed":
+                raise ValueError("on-device DST needs base_mode='fixed' (coverage mode needs the pooled profiles)")
+            kb = [cfg.base_budget] * len(pooled_xs)
+            ka, bn, _ = fixed_base_plan(table, pooled_xs, kb, cfg)
+            dev = q.device
+            self._dev_plan = dict(
+                mb_off=torch.tensor([0, batch.layout.nseq], dtype=torch.int32, device=dev),
+                k_base=torch.tensor([cfg.base_budget], dtype=torch.int32, device=dev),
+                k_anchor=torch.tensor([int(ka[rank])], dtype=torch.int32, device=dev),
+                bottleneck=torch.tensor([int(bn[rank])], dtype=torch.int32, device=dev),
+                grid=torch.tensor(list(cfg.budget_grid), dtype=torch.int32, device=dev))
 
     def scorer_pass(self):
         """K1 + K2 + K4 for every layer (the scorer pre-pass coverage-mode budgets need)."""
@@ -185,6 +219,8 @@ class DPStep:
         overlapping the next layers' kernels, and the compute stream waits for all of them at
         the end."""
         lay = self.batch.layout
+        if self.on_device:
+            return self._run_on_device(backward, mark, grad_buckets)
         qbar, kbar, profs, scores = self.scorer_pass()
         pooled = self.exchange(profs)
         k_final, decisions, k_base, xs = decide_budgets(pooled, self.table, self.cfg, len(self.layer_scales))
@@ -215,6 +251,39 @@ class DPStep:
             outs.append((idx, cnt, o, grads))
         for w_ in works:
             w_.wait()  # the compute stream waits for every bucket
+        return outs
+
+    def _run_on_device(self, backward, mark, grad_buckets):
+        """The step with K8 deciding each layer's keep count on the device (fixed-base mode)."""
+        lay = self.batch.layout
+        qbar, kbar = ops.block_pool(self.q, lay), ops.block_pool(self.k, lay)
+        if mark:
+            mark("decided")
+        k_max = int(min(max(self.cfg.budget_grid), lay.nb_max))
+        dp_ = self._dev_plan
+        outs, works, k_finals = [], [], []
+        for l, s_l in enumerate(self.layer_scales):
+            scale = s_l / math.sqrt(self.d)
+            S = ops.block_scores(self.q, self.k, lay, scale, qbar=qbar, kbar=kbar)
+            prof = ops.coverage_profile(S, lay)
+            k_final, _, k_seq = ops.dst_decide(prof, lay, dp_["mb_off"], dp_["k_base"], dp_["k_anchor"],
+                                               dp_["bottleneck"], dp_["grid"], self.cfg.threshold_p)
+            k_finals.append(k_final)
+            idx, cnt = ops.topk_select(S, lay, k_seq, k_max)
+            o, lse = ops.sparse_attn_fwd(self.q, self.k, self.v, lay, idx, cnt, scale)
+            if mark:
+                mark("fwd")
+            grads = ops.sparse_attn_bwd(self.q, self.k, self.v, o, self.do, lse, lay, idx, cnt, scale) if backward else None
+            if mark:
+                mark("bwd")
+            if grad_buckets is not None and self.world > 1:
+                import torch.distributed as dist
+
+                works.append(dist.all_reduce(grad_buckets[l], group=self.group, async_op=True))
+            outs.append((idx, cnt, o, grads))
+        for w_ in works:
+            w_.wait()
+        self.last = dict(k_final_device=k_finals)
         return outs
 
 

@@ -188,6 +188,22 @@ def coverage_at_grid(profile: torch.Tensor, lay: VarlenLayout, grid) -> torch.Te
     return out
 
 
+def dst_decide(profile: torch.Tensor, lay: VarlenLayout, mb_off: torch.Tensor, k_base: torch.Tensor,
+               k_anchor: torch.Tensor, bottleneck: torch.Tensor, grid: torch.Tensor, threshold_p: float):
+    """K8 (fixed-base on-device DST): (k_final [n_mb] int32, coverage_drop [n_mb] fp64,
+    k_seq [nseq] int32 = min(k_final, nb_s)). All inputs device tensors; mb_off int32 [n_mb+1]
+    partitions the layout's sequences into micro-batches."""
+    _need_cuda(profile, mb_off, k_base, k_anchor, bottleneck, grid)
+    n_mb = mb_off.numel() - 1
+    k_final = torch.empty(n_mb, dtype=torch.int32, device=profile.device)
+    drop = torch.empty(n_mb, dtype=torch.float64, device=profile.device)
+    k_seq = torch.empty(lay.nseq, dtype=torch.int32, device=profile.device)
+    _call("sb_dst_decide", _ptr(profile), _ptr(lay.blk_off), _ptr(lay.cu_seqlens), profile.shape[1], _ptr(mb_off),
+          n_mb, _ptr(k_base), _ptr(k_anchor), _ptr(bottleneck), _ptr(grid), grid.numel(), C.c_double(threshold_p),
+          _ptr(k_final), _ptr(drop), _ptr(k_seq), _stream())
+    return k_final, drop, k_seq
+
+
 def sparse_attn_fwd(q, k, v, lay: VarlenLayout, idx, cnt, scale: float | None = None):
     """K5: (O [T, Hq, D] bf16, LSE [Hq, T] fp32 natural log)."""
     _need_cuda(q, k, v, idx, cnt)
