@@ -441,6 +441,50 @@ SB_EXPORT int SBH(predict_members)(const int64_t* bins, int nx, const int* grid,
   });
 }
 
+#ifdef SB_REF
+// Test oracle only (the reference build): the reference step driver with a pipeline-parallel
+// cluster, so the PP projection (pp_projection.py) can be pinned against simulate_iteration's
+// own 1F1B timing (sim.cpp:180-275, 435-489). pp_i = {pp, layers_per_stage};
+// pp_d = {fwd_bwd_ratio, comm_ms, dp_sync_ms}; out_res = {iter_ms, bubble_ms, critical_lb_ms,
+// max_mb_ms, mean_mb_ms, imbalance, avg_budget, mean_cov_drop}.
+SB_EXPORT int SBH(ref_simulate_iteration)(int strategy, int n, const int64_t* ids, const int64_t* lengths,
+                                          const double* profiles, const int64_t* off, const int* setup_i,
+                                          const double* setup_d, int anchor, const int* dst_grid, int n_dst_grid,
+                                          const int64_t* edges, int ne, double* ema_inout, double alpha,
+                                          const int* est_grid, int n_est_grid, const int64_t* bins, int nx,
+                                          const int* grid, int nk, const double* lat, int iter_index,
+                                          const int* pp_i, const double* pp_d, double* out_res) {
+  return guarded([&] {
+    const int gbs = setup_i[0], mbs = setup_i[1], dp = setup_i[2];
+    const int nl = pp_i[0] * pp_i[1];
+    const auto samples = make_samples(n, ids, lengths, nl, profiles, off);
+    const auto table = make_table(bins, nx, grid, nk, lat);
+    auto est = make_est(edges, ne, ema_inout, alpha, est_grid, n_est_grid);
+    sb::IterationSetup setup;
+    setup.cluster.dp = dp;
+    setup.cluster.pp = pp_i[0];
+    setup.cluster.layers_per_stage = pp_i[1];
+    setup.cluster.fwd_bwd_ratio = pp_d[0];
+    setup.cluster.comm_ms = pp_d[1];
+    setup.cluster.dp_sync_ms = pp_d[2];
+    setup.shape = sb::PlanShape{gbs, mbs, dp};
+    setup.base_budget = setup_i[4];
+    setup.base_mode = setup_i[5] ? sb::BaseBudgetMode::kCoverage : sb::BaseBudgetMode::kFixed;
+    setup.base_coverage_target = setup_d[0];
+    setup.dst_scope = setup_i[6] ? sb::DstScope::kGlobal : sb::DstScope::kRank;
+    setup.dst.threshold_p = setup_d[1];
+    setup.dst.anchor = anchor_of(anchor);
+    setup.dst.budget_grid.assign(dst_grid, dst_grid + n_dst_grid);
+    setup.calibrate_every = setup_i[7];
+    const auto r = sb::simulate_iteration(samples, static_cast<sb::Strategy>(strategy), setup, table, est, iter_index,
+                                          nullptr, nullptr);
+    const double v[8] = {r.iter_ms, r.bubble_ms, r.critical_lb_ms, r.max_mb_ms, r.mean_mb_ms, r.imbalance,
+                         r.avg_budget, r.mean_cov_drop};
+    std::memcpy(out_res, v, sizeof(v));
+  });
+}
+#endif
+
 SB_EXPORT int SBH(plan_step)(int strategy, int n, const int64_t* ids, const int64_t* lengths,
                              const double* profiles, const int64_t* off, const int* setup_i,
                              const double* setup_d, int anchor, const int* dst_grid,

@@ -34,6 +34,7 @@ import numpy as np
 import torch
 
 from . import ops
+from . import pp_projection as ppj
 from .host import DEFAULT_BUDGET_GRID, ProfileTable, api
 
 MASK64 = (1 << 64) - 1
@@ -75,8 +76,8 @@ def summarize(mb_ms: list[list[float]]) -> dict:
 class Driver:
     def __init__(self, strategy="sab_dst", gbs=16, mbs=2, layers=4, block=128, heads=32, kv_heads=32, head_dim=128,
                  seed=42, dist_spec=None, table: ProfileTable | None = None, anchor="mean", threshold_p=0.1,
-                 dst_scope="global", base_mode="coverage", varlen_block_size=0, rank=0, world=1, group=None,
-                 device="cuda"):
+                 dst_scope="global", base_mode="coverage", varlen_block_size=0, project_pp=0, rank=0, world=1,
+                 group=None, device="cuda"):
         self.h = api()
         self.strategy, self.gbs, self.mbs, self.layers, self.B = strategy, gbs, mbs, layers, block
         self.H, self.Hkv, self.D = heads, kv_heads, head_dim
@@ -90,6 +91,11 @@ class Driver:
                             varlen_block_size=varlen_block_size)
         self._buf_T = 0
         self._warm = False
+        # PP projection: per-layer fwd / bwd kernel times feed a 1F1B model of
+        # `project_pp` stages (pp_projection.py); 0 = off.
+        self.project_pp = project_pp
+        if project_pp and layers % project_pp:
+            raise ValueError("layers must be a multiple of project_pp")
         # Per-layer softmax temperature, so layers differ as real layers do (fixed seed).
         self.layer_scales = np.exp(np.random.default_rng(seed).uniform(-0.5, 1.0, size=layers))
 
@@ -111,14 +117,15 @@ class Driver:
         if not self._warm:  # first micro-batch: one untimed pass so allocator / module load stay out of the timing
             self._layers(q, k, v, do, lay, nb, k_all, budgets, 1)
             self._warm = True
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        self._layers(q, k, v, do, lay, nb, k_all, budgets, self.layers)
-        e1.record()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * self.layers + 1)]
+        ev[0].record()
+        self._layers(q, k, v, do, lay, nb, k_all, budgets, self.layers, ev)
         torch.cuda.synchronize()
-        return e0.elapsed_time(e1)
+        # per layer: fwd = scorer + selector + forward, bwd = backward (block pooling in layer 0's fwd)
+        t = [ev[i].elapsed_time(ev[i + 1]) for i in range(2 * self.layers)]
+        return ev[0].elapsed_time(ev[-1]), t[0::2], t[1::2]
 
-    def _layers(self, q, k, v, do, lay, nb, k_all, budgets, n_layers):
+    def _layers(self, q, k, v, do, lay, nb, k_all, budgets, n_layers, ev=None):
         qbar, kbar = ops.block_pool(q, lay), ops.block_pool(k, lay)
         for l in range(n_layers):
             scale = float(self.layer_scales[l]) / math.sqrt(self.D)
@@ -126,7 +133,11 @@ class Driver:
             k_max = int(max(1, min(int(budgets[l]), int(nb.max()))))
             idx, cnt = ops.topk_select(S, lay, k_all[l], k_max, group=self.H // self.Hkv)
             o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+            if ev is not None:
+                ev[2 * l + 1].record()
             ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+            if ev is not None:
+                ev[2 * l + 2].record()
 
     def iteration(self, it: int, decisions_csv=None, plan_json=None) -> dict:
         lengths, profs = self.h.generate_samples(self.gbs, self.layers, self.B, seed=mix_seed(self.seed, it),
@@ -136,21 +147,30 @@ class Driver:
                               dp=self.world, num_layers=self.layers, table=self.table, est=self.est, iter_index=it,
                               decisions_csv=decisions_csv, plan_json=plan_json, **self.plan_kw)
         host_ms = (time.perf_counter() - t0) * 1e3
-        mine = []
+        rows = []  # per micro-batch: [total, fwd_0..fwd_{L-1}, bwd_0..bwd_{L-1}]
         for m, ids in enumerate(sp["micro_batch_bins"][self.rank]):
-            mine.append(self._run_micro_batch(np.asarray(lengths)[ids], sp["budgets"][self.rank][m]))
+            tot, tf, tb = self._run_micro_batch(np.asarray(lengths)[ids], sp["budgets"][self.rank][m])
+            rows.append([tot] + tf + tb)
         if self.world > 1:
             import torch.distributed as dist
 
-            t = torch.tensor(mine, dtype=torch.float64, device=self.device)
+            t = torch.tensor(rows, dtype=torch.float64, device=self.device)
             outs = [torch.zeros_like(t) for _ in range(self.world)]
             dist.all_gather(outs, t, group=self.group)
-            mb_ms = [o.cpu().tolist() for o in outs]
+            all_rows = [o.cpu().tolist() for o in outs]
         else:
-            mb_ms = [mine]
+            all_rows = [rows]
+        mb_ms = [[r[0] for r in rr] for rr in all_rows]
         rec = summarize(mb_ms)
         rec.update(dst_overhead_ms=host_ms, avg_budget=sp["avg_budget"], mean_cov_drop=sp["mean_cov_drop"],
                    mb_ms=mb_ms)
+        if self.project_pp:
+            L = self.layers
+            cl = ppj.Cluster(pp=self.project_pp, layers_per_stage=L // self.project_pp, comm_ms=0.05, dp_sync_ms=0.0)
+            times = [[ppj.stage_times_measured(r[1:1 + L], r[1 + L:1 + 2 * L], cl) for r in rr] for rr in all_rows]
+            buds = [[[int(k) for k in sp["budgets"][r][i]] for i in range(len(all_rows[r]))] for r in range(self.world)]
+            rec["pp"] = ppj.project_iteration(times, buds, cl, L)
+            rec["pp"].update(dst_overhead_ms=host_ms, mean_cov_drop=sp["mean_cov_drop"])
         return rec
 
     def run(self, iters: int, out_dir: str | None = None):
@@ -168,6 +188,11 @@ class Driver:
                 f.write(ITER_HEADER)
                 for it, rec in enumerate(records):
                     f.write(iteration_row(self.strategy, it, rec))
+            if self.project_pp:
+                with open(os.path.join(out_dir, f"iterations_pp{self.project_pp}.csv"), "w") as f:
+                    f.write(ITER_HEADER)
+                    for it, rec in enumerate(records):
+                        f.write(iteration_row(self.strategy, it, rec["pp"]))
         return records
 
 
@@ -182,6 +207,8 @@ def main():
                                                    "the reference generator's default distribution")
     ap.add_argument("--table", default=None, help="cost table CSV (x,k,latency_ms), e.g. from profiler.py")
     ap.add_argument("--varlen", action="store_true", help="opt-in varlen-aware DST cost (predict_members at B)")
+    ap.add_argument("--project-pp", type=int, default=0, help="also project a PP-stage 1F1B pipeline from the "
+                                                              "measured per-layer times (pp_projection.py)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
@@ -197,7 +224,8 @@ def main():
                          long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
     table = api().load_table(args.table)[0] if args.table else None
     drv = Driver(args.strategy, gbs=args.gbs_per_rank * world, mbs=args.mbs, layers=args.layers, dist_spec=dist_spec,
-                 table=table, varlen_block_size=128 if args.varlen else 0, rank=rank, world=world,
+                 table=table, varlen_block_size=128 if args.varlen else 0, project_pp=args.project_pp, rank=rank,
+                 world=world,
                  device=torch.device("cuda", local))
     recs = drv.run(args.iters, args.out)
     if rank == 0:

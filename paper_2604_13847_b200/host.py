@@ -341,6 +341,33 @@ class HostAPI:
                     mean_cov_drop=float(stats[0]), avg_budget=float(stats[1]))
 
 
+    def ref_simulate_iteration(self, strategy: str, ids, lengths, profiles, *, gbs: int, mbs: int, dp: int, pp: int,
+                               layers_per_stage: int, table: ProfileTable, est: SparsityEstimator, iter_index: int = 0,
+                               fwd_bwd_ratio: float = 2.0, comm_ms: float = 0.05, dp_sync_ms: float = 5.0,
+                               base_budget: int = 32, base_mode: str = "coverage", base_coverage_target: float = 0.9,
+                               dst_scope: str = "global", threshold_p: float = 0.1, anchor: str = "min",
+                               dst_grid=None, calibrate_every: int = 1) -> dict:
+        """Test oracle only (the compiled reference, prefix sbref_): the reference step driver's
+        ScheduleResult with a pipeline-parallel cluster (sim.cpp:277-489)."""
+        n = len(ids)
+        num_layers = pp * layers_per_stage
+        flat, off = _flatten([p for s in profiles for p in s])
+        setup_i = _a([gbs, mbs, dp, num_layers, base_budget, 1 if base_mode == "coverage" else 0,
+                      1 if dst_scope == "global" else 0, calibrate_every, 0], np.int32)
+        setup_d = _a([base_coverage_target, threshold_p], np.float64)
+        grid = _a([] if dst_grid is None else dst_grid, np.int32)
+        res = np.zeros(8, np.float64)
+        self._call("ref_simulate_iteration", STRATEGIES[strategy], n, _p(_a(ids, np.int64)),
+                   _p(_a(lengths, np.int64)), _p(flat), _p(off), _p(setup_i), _p(setup_d), ANCHORS[anchor],
+                   _p(grid if grid.size else np.zeros(1, np.int32)), len(grid), _p(est.bin_edges), len(est.bin_edges),
+                   _p(est.ema_budget), C.c_double(est.ema_alpha), _p(est.budget_grid), len(est.budget_grid),
+                   *table.args(), iter_index, _p(_a([pp, layers_per_stage], np.int32)),
+                   _p(_a([fwd_bwd_ratio, comm_ms, dp_sync_ms], np.float64)), _p(res))
+        keys = ("iter_ms", "bubble_ms", "critical_lb_ms", "max_mb_ms", "mean_mb_ms", "imbalance", "avg_budget",
+                "mean_cov_drop")
+        return dict(zip(keys, res.tolist()))
+
+
 _api = None
 
 

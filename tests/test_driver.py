@@ -29,13 +29,15 @@ def test_driver_short_run(tmp_path):
 
     dist_spec = dict(short_weight=0.6, short_log_mean=float(np.log(512)), short_log_sigma=0.0,
                      long_log_mean=float(np.log(4096)), long_log_sigma=0.0, max_length=8192)
-    drv = driver.Driver("sab_dst", gbs=4, mbs=2, layers=2, heads=4, kv_heads=2, head_dim=128, dist_spec=dist_spec,
-                        device=torch.device("cuda", 0))
+    drv = driver.Driver("sab_dst", gbs=4, mbs=1, layers=2, heads=4, kv_heads=2, head_dim=128, dist_spec=dist_spec,
+                        project_pp=2, device=torch.device("cuda", 0))
     recs = drv.run(2, str(tmp_path))
     assert len(recs) == 2
     for r in recs:
-        assert r["iter_ms"] > 0 and r["imbalance"] >= 1.0 and len(r["mb_ms"][0]) == 2
+        assert r["iter_ms"] > 0 and r["imbalance"] >= 1.0 and len(r["mb_ms"][0]) == 4
+        assert r["pp"]["iter_ms"] > 0 and r["pp"]["bubble_ms"] >= 0  # 4 micro-batches through 2 projected stages
     lines = (tmp_path / "iterations.csv").read_text().splitlines()
     assert lines[0] + "\n" == driver.ITER_HEADER and len(lines) == 3
     assert (tmp_path / "decisions_1.csv").read_text().startswith("iter,mb,layer,")
     assert (tmp_path / "plan_0.json").exists()
+    assert len((tmp_path / "iterations_pp2.csv").read_text().splitlines()) == 3
