@@ -263,14 +263,19 @@ def main():
                               "scorer+profile+selector+fwd+bwd", "seqs_rank0": int(len(cu) - 1)}
     else:
         lengths_all, profiles_all = c3_global_batch(world, CFG["seed"], args.layers)
-        table = api().synthesize_table(block_size=B)
+        # GPU-measured cost table (profiler.py, committed under profiles/) when present, as SURVEY
+        # 8(f) item 1 intends; the reference's synthetic table otherwise.
+        tpath = os.path.join(ROOT, "profiles", "b200_cost_table_h32_d128_b128.csv")
+        table = api().load_table(tpath)[0] if os.path.exists(tpath) else api().synthesize_table(block_size=B)
+        table_src = "GPU-measured cost table" if os.path.exists(tpath) else "synthetic cost table"
         bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=table)
         mine = [int(lengths_all[i]) for i in bins[rank][0]]
         cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
         k_seq = None
         config = {"workload": f"C3: 40% 32K / 60% 2K global batch (reference generator, seed 42, gbs={5 * world}), "
                               f"SAB plan mbs=5 (one packed micro-batch per rank), {args.layers} layers, per-layer DST "
-                              "(Mean anchor, p=0.1, global scope, coverage base) on the generator's routing profiles "
+                              f"(Mean anchor, p=0.1, global scope, coverage base, {table_src}) on the generator's "
+                              "routing profiles "
                               "(all-gathered), GPU block scores for selection, 32 heads MHA, d128, B128, "
                               "scorer+allgather+DST+selector+fwd+bwd",
                   "tokens_per_rank": [int(x) for x in np.array([sum(int(lengths_all[i]) for i in b[0]) for b in bins])]}
