@@ -401,10 +401,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         const uint32_t ph = (g / kStages) & 1;
         int h, gi;
         pair_of(w, m, h, gi);
-#ifdef SB_DKV_SAMEQ  // timing experiment only: every pair streams the same (L2-hot) Q / dO tile
-        h = 0;
-        gi = blk_off[w.s];
-#endif
         const int q0 = w.seq0 + (gi - blk_off[w.s]) * B;
         const int nq = min(B, w.seq_len - (gi - blk_off[w.s]) * B);
         // lse2 / D of the pair's query rows: all loads in flight before the ring-slot wait.
@@ -573,13 +569,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         mbar_wait(&bars->st_full, g & 1);
         if (threadIdx.x == 64) tr(4, g);
         tc_fence_after();
-#ifdef SB_DKV_NOMATH  // timing experiment only: UMMA stream without the math
-        mbar_arrive(&bars->st_free);
-        mbar_wait(&bars->dpt_full, g & 1);
-        mbar_arrive(&bars->pds_part[0]);
-        if (B / 64 > 1) mbar_arrive(&bars->pds_part[1]);
-        continue;
-#endif
         float p[HB];
         {
           uint32_t sv[HB / 32][32];
