@@ -639,16 +639,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
             for (int e = 0; e < 32; ++e) v[e] = 0u;
           }
           if (store) {
-            uint4* dst = reinterpret_cast<uint4*>(row + cc * 32);
+            uint32_t w16[16];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              uint4 q4;
-              q4.x = pack_bf16x2(__uint_as_float(v[8 * e + 0]) * mul, __uint_as_float(v[8 * e + 1]) * mul);
-              q4.y = pack_bf16x2(__uint_as_float(v[8 * e + 2]) * mul, __uint_as_float(v[8 * e + 3]) * mul);
-              q4.z = pack_bf16x2(__uint_as_float(v[8 * e + 4]) * mul, __uint_as_float(v[8 * e + 5]) * mul);
-              q4.w = pack_bf16x2(__uint_as_float(v[8 * e + 6]) * mul, __uint_as_float(v[8 * e + 7]) * mul);
-              dst[e] = q4;
-            }
+            for (int e = 0; e < 16; ++e)
+              w16[e] = pack_bf16x2(__uint_as_float(v[2 * e]) * mul, __uint_as_float(v[2 * e + 1]) * mul);
+            store_64B(row + cc * 32, w16);
           }
         }
       }
@@ -827,7 +822,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
     const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
     const uint32_t qs_addr = smem_u32(q_stage), ds_addr = smem_u32(do_stage);
     auto load_qdo = [&](int qq) {  // staging -> TMEM, behind the previous item's last S / dP
+      if (trace != nullptr && blockIdx.x == 0 && qq < 64 && lane == 0) trace[4096 + qq * 4 + 2] = clock64();
       mbar_wait(&bars->stage_full, qq & 1);
+      if (trace != nullptr && blockIdx.x == 0 && qq < 64 && lane == 0) trace[4096 + qq * 4 + 3] = clock64();
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
@@ -894,10 +891,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         const bool last = j + 1 == n;
         if (last) have_next = next_item(cur_k, nxt);
         const bool more = !last || have_next;
-        if (more) {
-          if (last) load_qdo(q + 1);  // in order behind S_g / dP_g, the item's last readers of Q / dO
-          issue_s(g + 1);
-        }
+        // Inside an item S_{g+1} goes ahead of dQ_g (it overlaps the math of g). At an item
+        // boundary dQ_g goes first, so the dQ epilogue overlaps the next item's Q / dO copy and S_0.
+        if (more && !last) issue_s(g + 1);
         tr(0, g);
         const int st = g % kKS;
         // dQ_g in two K halves: the K steps of dS chunk c2 go as soon as both warpgroups packed
@@ -919,6 +915,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         tc_commit(&bars->k_empty[st], leader);
         if (last) tc_commit(&bars->dq_done, leader);
         tr(6, g);
+        if (more && last) {
+          load_qdo(q + 1);  // in order behind S_g / dP_g, the item's last readers of Q / dO
+          issue_s(g + 1);
+        }
         if (more) issue_dp(g + 1);
       }
       cur = nxt;
@@ -1003,6 +1003,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         if (threadIdx.x == 64) tr(11, g);
       }
       mbar_wait(&bars->dq_done, q & 1);
+      if (trace != nullptr && blockIdx.x == 0 && q < 64 && threadIdx.x == 64) trace[4096 + q * 4] = clock64();
       tc_fence_after();
       uint32_t v[D / 64][32];
 #pragma unroll
@@ -1013,18 +1014,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
       if (valid) {
 #pragma unroll
         for (int cc = 0; cc < D / 64; ++cc) {
-          uint4* dst = reinterpret_cast<uint4*>(dq_row + cc * 32);
+          uint32_t w16[16];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint4 q4;
-            q4.x = pack_bf16x2(__uint_as_float(v[cc][8 * e + 0]) * scale, __uint_as_float(v[cc][8 * e + 1]) * scale);
-            q4.y = pack_bf16x2(__uint_as_float(v[cc][8 * e + 2]) * scale, __uint_as_float(v[cc][8 * e + 3]) * scale);
-            q4.z = pack_bf16x2(__uint_as_float(v[cc][8 * e + 4]) * scale, __uint_as_float(v[cc][8 * e + 5]) * scale);
-            q4.w = pack_bf16x2(__uint_as_float(v[cc][8 * e + 6]) * scale, __uint_as_float(v[cc][8 * e + 7]) * scale);
-            dst[e] = q4;
-          }
+          for (int e = 0; e < 16; ++e)
+            w16[e] = pack_bf16x2(__uint_as_float(v[cc][2 * e]) * scale, __uint_as_float(v[cc][2 * e + 1]) * scale);
+          store_64B(dq_row + cc * 32, w16);
         }
       }
+      if (trace != nullptr && blockIdx.x == 0 && q < 64 && threadIdx.x == 64) trace[4096 + q * 4 + 1] = clock64();
       ++q;
     }
   }

@@ -377,16 +377,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
       if (store) {
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+          uint32_t w16[16];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint4 o4;
-            o4.x = pack_bf16x2(__uint_as_float(v[c][8 * e + 0]) * inv_l, __uint_as_float(v[c][8 * e + 1]) * inv_l);
-            o4.y = pack_bf16x2(__uint_as_float(v[c][8 * e + 2]) * inv_l, __uint_as_float(v[c][8 * e + 3]) * inv_l);
-            o4.z = pack_bf16x2(__uint_as_float(v[c][8 * e + 4]) * inv_l, __uint_as_float(v[c][8 * e + 5]) * inv_l);
-            o4.w = pack_bf16x2(__uint_as_float(v[c][8 * e + 6]) * inv_l, __uint_as_float(v[c][8 * e + 7]) * inv_l);
-            dst[e] = o4;
-          }
+          for (int e = 0; e < 16; ++e)
+            w16[e] = pack_bf16x2(__uint_as_float(v[c][2 * e]) * inv_l, __uint_as_float(v[c][2 * e + 1]) * inv_l);
+          store_64B(orow + c * 32, w16);
         }
         lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = (m_run + log2f(l_run)) * 0.69314718055994531f;
       }

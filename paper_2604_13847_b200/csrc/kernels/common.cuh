@@ -56,6 +56,24 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
+// 64 contiguous output bytes (16 packed words) from one thread: two 256-bit stores
+// (STG.256, sm_100) when 32-byte aligned, else four 128-bit stores. Halves the store count of
+// the epilogues, whose issue rate bounds the item-boundary time.
+__device__ __forceinline__ void store_64B(void* dst, const uint32_t (&w)[16]) {
+  if ((reinterpret_cast<uintptr_t>(dst) & 31u) == 0) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(w[0]), "r"(w[1]),
+                 "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(static_cast<char*>(dst) + 32),
+                 "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+                 : "memory");
+  } else {
+    uint4* d4 = static_cast<uint4*>(dst);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) d4[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+  }
+}
+
 // Sequence owning global block gi (binary search in blk_off[0..nseq]).
 __device__ __forceinline__ int seq_of_block(const int32_t* blk_off, int nseq, int gi) {
   int lo = 0, hi = nseq;  // blk_off[lo] <= gi < blk_off[hi]

@@ -42,3 +42,8 @@ print("median o_done wait (P done -> o_done seen):", np.median(t[r, 6] - t[r, 5]
 print("per-warp arrival relative to warp 2 (warps 2..5), median over blocks:", [float(np.median(pw[4:40, w] - pw[4:40, 0])) for w in range(4)])
 print("per-warp S seen relative to warp 2:", [float(np.median(ps[4:40, w] - ps[4:40, 0])) for w in range(4)])
 print("per-warp busy (arrive - S seen):", [float(np.median(pw[4:40, w] - ps[4:40, w])) for w in range(4)])
+d = np.diff(t[1:200, 1])
+d = d[d > 0]
+print("QK-issue period percentiles 10/50/90/99:", [float(np.percentile(d, q)) for q in (10, 50, 90, 99)])
+big = d > 2 * np.median(d)
+print("blocks with > 2x median period:", int(big.sum()), "of", len(d), "; their excess:", float((d[big] - np.median(d)).sum()), "; total:", float(d.sum()))
