@@ -239,3 +239,38 @@ def test_autograd_matches_explicit_calls():
     dq, dk, dv = ops.sparse_attn_bwd(q.detach(), k.detach(), v.detach(), o2, do, lse, lay, idx, cnt)
     assert torch.equal(o.detach(), o2)
     assert torch.equal(q.grad, dq) and torch.equal(k.grad, dk) and torch.equal(v.grad, dv)
+
+
+@pytest.mark.parametrize("cu,B", [
+    ([0, 300, 300, 1000, 1000, 1129], 128),  # empty sequences in the middle of the pack
+    ([0, 1, 2, 66, 194, 195], 64),           # length-1 sequences, exactly B, B + 1
+    ([0, 0, 257], 128),                      # leading empty sequence
+])
+def test_edge_layouts_end_to_end(cu, B):
+    """Ragged / empty sequences through scorer -> selector -> fwd -> bwd against the oracle:
+    empty sequences own no blocks and no rows; every other row is computed as usual."""
+    from paper_2604_13847_b200 import ops
+
+    T = cu[-1]
+    hq, hkv, d = 2, 1, 64
+    q, k, v, do = _rand_bf16((T, hq, d), 61), _rand_bf16((T, hkv, d), 62), _rand_bf16((T, hkv, d), 63), \
+        _rand_bf16((T, hq, d), 64)
+    lay = _layout(cu, B)
+    scale = 1.0 / math.sqrt(d)
+    S = ops.block_scores(q, k, lay, scale)
+    rS = orc.block_scores(orc.block_pool(_bits(q), cu, B), orc.block_pool(_bits(k), cu, B), cu, B, scale)
+    np.testing.assert_allclose(S.cpu().numpy()[:, :lay.tri_total], rS[:, :lay.tri_total], rtol=1e-4,
+                               atol=1e-5 * max(1.0, np.abs(rS).max()))
+    k_seq = np.full(len(cu) - 1, 2, np.int32)
+    idx, cnt = ops.topk_select(S, lay, torch.from_numpy(k_seq).cuda(), 2, group=hq)
+    ridx, rcnt = orc.topk_select(S.cpu().numpy(), cu, B, k_seq, 2, group=hq, force_diag=True)
+    assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(cnt.cpu().numpy(), rcnt)
+    o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+    dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+    torch.cuda.synchronize()
+    ic, cc = idx.cpu().numpy(), cnt.cpu().numpy()
+    ro, rlse = orc.sparse_attn_fwd(_bits(q), _bits(k), _bits(v), cu, B, ic, cc, scale)
+    rdq, rdk, rdv = orc.sparse_attn_bwd(_bits(q), _bits(k), _bits(v), ro, _bits(do), rlse, cu, B, ic, cc, scale)
+    for got, ref in ((o, ro), (dq, rdq), (dk, rdk), (dv, rdv)):
+        g = got.float().cpu().numpy()
+        assert np.abs(g - ref).max() <= 2e-2 * max(1.0, np.abs(ref).max())
