@@ -131,6 +131,38 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+def host_cores() -> int:
+    """Host threads this process may use (affinity / cgroup aware). torchrun sets
+    OMP_NUM_THREADS=1 per rank; the CPU arm overrides that to use the whole host."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def c3_rank0_layer0(world, layers):
+    """Rank 0's packed micro-batch of the C3 global batch (SAB plan on the same cost table as the
+    GPU arm) and its layer-0 DST keep count per sequence (the pooled host DST, bit-identical to
+    what every GPU rank decides)."""
+    from paper_2604_13847_b200 import dp
+    from paper_2604_13847_b200.host import api
+
+    lengths_all, profiles_all = c3_global_batch(world, CFG["seed"], layers)
+    tpath = os.path.join(ROOT, "profiles", "b200_cost_table_h32_d128_b128.csv")
+    table = api().load_table(tpath)[0] if os.path.exists(tpath) else api().synthesize_table(block_size=CFG["block"])
+    bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=table)
+    pooled = []
+    for r in range(world):
+        ids = bins[r][0]
+        pooled.append((np.asarray([int(lengths_all[i]) for i in ids]),
+                       [[profiles_all[i][l] for l in range(layers)] for i in ids]))
+    k_final, _, _, _ = dp.decide_budgets(pooled, table, dp.DstSettings(), layers)
+    mine = [int(x) for x in pooled[0][0]]
+    cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
+    nb = (np.diff(cu) + CFG["block"] - 1) // CFG["block"]
+    return cu, np.minimum(int(k_final[0][0]), nb).astype(np.int32)
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference has no CPU attention; the CPU arm is this repo's
     oracle port of the path (oracle/sb_oracle.c, fp64, all host threads) on a bounded sample of
@@ -139,15 +171,9 @@ def run_reference_arm(args, rank, world):
         return
     from oracle import device as orc
 
-    if world > 1 or args.workload == "c3":
-        from paper_2604_13847_b200 import dp
-        from paper_2604_13847_b200.host import api
-
-        lengths_all, _ = c3_global_batch(world, CFG["seed"], args.layers)
-        bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=api().synthesize_table(block_size=CFG["block"]))
-        mine = [int(lengths_all[i]) for i in bins[0][0]]
-        cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
-        k_seq = np.maximum(1, (np.diff(cu) + CFG["block"] - 1) // CFG["block"] // 8).astype(np.int32)
+    c3 = world > 1 or args.workload == "c3"
+    if c3:
+        cu, k_seq = c3_rank0_layer0(world, args.layers)
     else:
         cu, k_seq = workload(0)
     T, D, B = int(cu[-1]), CFG["head_dim"], CFG["block"]
@@ -157,7 +183,7 @@ def run_reference_arm(args, rank, world):
         return (rng.standard_normal(shape).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
 
     q, k, v, do = bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D))
-    threads = orc.set_threads(0)
+    threads = orc.set_threads(host_cores())
     blk, tri = orc.layout(cu, B)
     scale = 1.0 / math.sqrt(D)
     times, flops = [], None
@@ -177,13 +203,16 @@ def run_reference_arm(args, rank, world):
             times.append(dt)
     ms = 1e3 * statistics.mean(times)
     value = flops / (ms * 1e-3) / 1e12
-    sample = (f"q head 0 of 32, one layer, of rank 0's {T}-token micro-batch ({len(cu) - 1} seqs): "
-              "scorer, profile, selector, fwd, bwd")
+    sample = (f"q head 0 of 32, {'layer 0 (DST keep count)' if c3 else 'one layer'}, of rank 0's {T}-token "
+              f"micro-batch ({len(cu) - 1} seqs): scorer, profile, selector, fwd, bwd")
+    workload_txt = ("C3: 40% 32K / 60% 2K global batch, SAB plan, per-layer DST, 32 heads MHA, d128, B128, fwd+bwd "
+                    "(CPU sample: rank 0, layer 0, q head 0)" if c3 else
+                    "C2: 32K-token packed varlen micro-batch per rank, 32 heads, d128, B128, per-sequence keep "
+                    "U[0.05,0.5], fwd+bwd (CPU sample: q head 0)")
     line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C2: 32K-token packed varlen micro-batch per rank, 32 heads, d128, B128, "
-                                   "per-sequence keep U[0.05,0.5], fwd+bwd", "sample": "1 of 32 heads"},
+            "config": {"workload": workload_txt, "sample": "1 of 32 heads"},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -513,7 +542,7 @@ def cpu_baseline(cu, k_seq):
         return (rng.standard_normal(shape).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
 
     q, k, v, do = bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D))
-    threads = orc.set_threads(0)
+    threads = orc.set_threads(host_cores())
     _, tri = orc.layout(cu, B)
     S = rng.standard_normal((1, int(tri[-1]))).astype(np.float32)
     idx, cnt = orc.topk_select(S, cu, B, k_seq, int(k_seq.max()))
