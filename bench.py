@@ -187,7 +187,17 @@ def run_reference_arm(args, rank, world):
     blk, tri = orc.layout(cu, B)
     scale = 1.0 / math.sqrt(D)
     times, flops = [], None
+    budget_s, start, warm_done = args.ref_budget_s, time.perf_counter(), 0
     for it in range(args.warmup + args.steps):
+        # Bounded run: the work per step is deterministic, so once one warm-up and one timed step
+        # are in, further steps only tighten the mean; stop before the wall-clock budget is spent.
+        spent = time.perf_counter() - start
+        est = spent / it if it else 0.0
+        if it < args.warmup:
+            if warm_done and spent + 2 * est > budget_s:  # keep room for one timed step
+                continue
+        elif times and spent + est > budget_s:
+            break
         t0 = time.perf_counter()
         qb, kb = orc.block_pool(q, cu, B), orc.block_pool(k, cu, B)
         S = orc.block_scores(qb, kb, cu, B, scale).astype(np.float32)
@@ -201,6 +211,8 @@ def run_reference_arm(args, rank, world):
             flops = f + b
         if it >= args.warmup:
             times.append(dt)
+        else:
+            warm_done += 1
     ms = 1e3 * statistics.mean(times)
     value = flops / (ms * 1e-3) / 1e12
     sample = (f"q head 0 of 32, {'layer 0 (DST keep count)' if c3 else 'one layer'}, of rank 0's {T}-token "
@@ -212,7 +224,8 @@ def run_reference_arm(args, rank, world):
     line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_txt, "sample": "1 of 32 heads"},
+            "config": {"workload": workload_txt, "sample": "1 of 32 heads", "warmup_run": warm_done,
+                       "steps_timed": len(times), "budget_s": budget_s},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -261,6 +274,8 @@ def main():
                          "32K/2K global batch, SAB plan + per-layer DST across ranks")
     ap.add_argument("--layers", type=int, default=36, help="c3: layers per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: wall-clock budget for the CPU arm (>= 1 warm-up + 1 timed step)")
     ap.add_argument("--profile-only", action="store_true", help="2 plain steps then exit (for ncu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
