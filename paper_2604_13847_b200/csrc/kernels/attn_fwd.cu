@@ -11,9 +11,13 @@
 //               stream g (all items back to back):
 //                 S_g = Q K_g^T   (SS, M=128 N=B K=D)          -> TMEM S[g % 2]
 //                 O  += P_g V_g   (TS, A = P_g from TMEM, B = V_g MN-major in smem)
-//               issue order QK_0, QK_1, PV_0, QK_2, PV_1, ... across item boundaries, so the
-//               next item's first QK overlaps the last softmax and epilogue of the previous.
-//               O is double-buffered per item (TMEM: S0 | S1 | O0 | O1).
+//               issue order QK_0, QK_1, QK_2, PV_0, QK_3, PV_1, ... (QK_g before PV_{g-2})
+//               across item boundaries. S is triple-buffered (TMEM: S0 | S1 | S2 | O): P_g
+//               aliases S_g, so with two buffers QK_{g+1} had to wait for PV_{g-1} and the
+//               chain P_{g-1} -> PV_{g-1} -> QK_{g+1} -> S_{g+1} (~1650 cycles) paced the
+//               softmax; with three the softmax has two blocks of slack. O is single: the
+//               same softmax warps run the epilogue before producing the next item's P_0, so
+//               a second O buffer could never be used early.
 //   warps 2..5  softmax: one TMEM lane (= query row) per thread; online softmax in the log2
 //               domain with lazy O rescaling (only when the row max grows by > 8); 3/8 of the
 //               exponentials on the FMA pipe (fastmath.cuh); P written back into TMEM as packed
@@ -33,6 +37,7 @@ using namespace sm100;
 
 constexpr int kM = 128;                 // UMMA M / Q tile rows
 constexpr int kStages = 2;              // K ring depth
+constexpr int kSBufs = 3;               // S / P buffers in TMEM
 constexpr int kVStages = 3;             // V ring depth (V is consumed last: needs the longest prefetch)
 constexpr int kThreads = 224;           // 7 warps: Q/K producer, UMMA, 4 softmax, V producer
 constexpr float kRescaleThresh = 8.0f;  // log2 units: lazily rescale O only on a 256x max jump
@@ -43,8 +48,8 @@ struct FwdCfg {
   static constexpr int kQBytes = kChunks * kM * 128;  // one Q tile
   static constexpr int kKVBytes = kChunks * B * 128;  // one K or V block
   static constexpr int kSmemTiles = 2 * kQBytes + (kStages + kVStages) * kKVBytes;
-  static constexpr int kTmemS0 = 0, kTmemS1 = B, kTmemO0 = 2 * B, kTmemO1 = 2 * B + D;
-  static constexpr uint32_t kTmemCols = (2 * B + 2 * D) <= 256 ? 256 : 512;
+  static constexpr int kTmemO = kSBufs * B;  // S_b at column b * B
+  static constexpr uint32_t kTmemCols = (kSBufs * B + D) <= 256 ? 256 : 512;
   static constexpr int kSmemBytes = kSmemTiles + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
@@ -52,28 +57,26 @@ struct FwdBars {
   uint64_t q_full[2], q_empty[2];
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kVStages], v_empty[kVStages];
-  uint64_t s_full[2], p_full[2];
-  uint64_t o_done, o_free[2];
+  uint64_t s_full[kSBufs], p_full[kSBufs];
+  uint64_t o_done[kSBufs], o_free;  // o_done[b]: PV of the blocks g with g % kSBufs == b
   uint32_t tmem_base;
 };
 
 struct Item {
-  int h, gi, s, i, seq0, seq_len, n;
+  int h, i, seq0, seq_len, n, first;
   const int32_t* list;
 };
 
-__device__ __forceinline__ Item decode(int it, const int32_t* cu, const int32_t* blk_off, int nseq, int nbt, int hq,
-                                       int hsel, const int32_t* idx, const int32_t* cnt, int k_max) {
+// Item of a prefetched schedule record (sched::q_records_kernel): register arithmetic only.
+__device__ __forceinline__ Item from_rec(const sched::ItemRec& r, int nbt, const int32_t* idx, int k_max) {
   Item w;
-  w.h = it / nbt;
-  w.gi = it - w.h * nbt;
-  w.s = seq_of_block(blk_off, nseq, w.gi);
-  w.i = w.gi - blk_off[w.s];
-  w.seq0 = cu[w.s];
-  w.seq_len = cu[w.s + 1] - w.seq0;
-  const int srow = w.h / (hq / hsel);
-  w.list = idx + (static_cast<size_t>(srow) * nbt + w.gi) * k_max;
-  w.n = cnt[static_cast<size_t>(srow) * nbt + w.gi];
+  w.h = r.it / nbt;
+  w.i = r.loc;
+  w.seq0 = r.seq0;
+  w.seq_len = r.seq_len;
+  w.n = r.n;
+  w.first = r.first;
+  w.list = idx + static_cast<size_t>(r.base) * k_max;
   return w;
 }
 
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
     const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off,
     int nseq, int total_tokens, int hq, int hkv, const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt,
     int hsel, int k_max, float scale_log2, uint16_t* __restrict__ out, float* __restrict__ lse,
-    const int32_t* __restrict__ order, int n_items, unsigned long long* __restrict__ trace) {
+    const sched::ItemRec* __restrict__ recs, int n_items, unsigned long long* __restrict__ trace) {
   using C = FwdCfg<D, B>;
   // Debug timeline (sb_debug_set_trace): CTA 0 records clock64 at phase boundaries.
   auto tr = [&](int slot, int g) {
@@ -153,10 +156,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars->q_full[b], 1);
       mbar_init(&bars->q_empty[b], 1);
+    }
+    for (int b = 0; b < kSBufs; ++b) {
       mbar_init(&bars->s_full[b], 1);
       mbar_init(&bars->p_full[b], 128);
-      mbar_init(&bars->o_free[b], 128);
+      mbar_init(&bars->o_done[b], 1);
     }
+    mbar_init(&bars->o_free, 128);
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&bars->k_full[st], 1);
       mbar_init(&bars->k_empty[st], 1);
@@ -165,7 +171,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
       mbar_init(&bars->v_full[st], 1);
       mbar_init(&bars->v_empty[st], 1);
     }
-    mbar_init(&bars->o_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(&bars->tmem_base);
@@ -184,10 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
       tma_prefetch(&tm_k);
     }
     int g = 0, q = 0;
-    for (int k = 0;; ++k) {
-      const int it = sched::snake_item(order, n_items, grid, cta, k);
-      if (it < 0) break;
-      const Item w = decode(it, cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
+    for (sched::RecCursor cur(recs, n_items, grid, cta);;) {
+      const sched::ItemRec rec = cur.next();
+      if (rec.it < 0) break;
+      const Item w = from_rec(rec, nbt, idx, k_max);
       if (w.n <= 0) continue;
       const int hk = w.h / (hq / hkv);
       if (!v_stream) {
@@ -230,32 +235,34 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
       constexpr uint32_t idesc_qk = idesc_bf16_f32(kM, B, false, false);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(kM, D, false, true);
       const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem);
-      // Pending PV (the previous global block), issued after the next QK.
-      int pv_g = -1, pv_j = 0, pv_q = 0;
+      // Pending PVs (the two previous global blocks), issued two QKs late: a ring of 2.
+      int pv_g[2] = {-1, -1}, pv_j[2] = {0, 0}, pv_q[2] = {0, 0}, pv_n = 0, pv_h = 0;
       auto issue_pv = [&]() {
-        const int st = pv_g % kVStages;
-        const int ob = pv_q & 1;
-        mbar_wait(&bars->v_full[st], (pv_g / kVStages) & 1);
-        tr(2, pv_g);
-        mbar_wait(&bars->p_full[pv_g & 1], (pv_g >> 1) & 1);
-        tr(3, pv_g);
-        if (pv_j == 0) mbar_wait(&bars->o_free[ob], ((pv_q >> 1) & 1) ^ 1);  // epilogue of item q-2 done
+        const int g = pv_g[pv_h], j = pv_j[pv_h], q = pv_q[pv_h];
+        pv_h ^= 1;
+        --pv_n;
+        const int st = g % kVStages;
+        mbar_wait(&bars->v_full[st], (g / kVStages) & 1);
+        tr(2, g);
+        mbar_wait(&bars->p_full[g % kSBufs], (g / kSBufs) & 1);
+        tr(3, g);
+        if (j == 0) mbar_wait(&bars->o_free, (q & 1) ^ 1);  // epilogue of item q-1 read O
         tc_fence_after();
-        const uint32_t p_tmem = tmem + ((pv_g & 1) ? C::kTmemS1 : C::kTmemS0);
-        const uint32_t o_tmem = tmem + (ob ? C::kTmemO1 : C::kTmemO0);
+        const uint32_t p_tmem = tmem + (g % kSBufs) * B;
+        const uint32_t o_tmem = tmem + C::kTmemO;
 #pragma unroll
         for (int kk = 0; kk < B / 16; ++kk) {
           const uint64_t b = desc_sw128(v_addr + st * C::kKVBytes + kk * 2048, B * 128, 1024);
-          mma_ts(o_tmem, p_tmem + kk * 8, b, idesc_pv, (pv_j > 0 || kk > 0) ? 1u : 0u, leader);
+          mma_ts(o_tmem, p_tmem + kk * 8, b, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u, leader);
         }
         tc_commit(&bars->v_empty[st], leader);
-        tc_commit(&bars->o_done, leader);
+        tc_commit(&bars->o_done[g % kSBufs], leader);
       };
       int g = 0, q = 0;
-      for (int k = 0;; ++k) {
-        const int it = sched::snake_item(order, n_items, grid, cta, k);
-        if (it < 0) break;
-        const Item w = decode(it, cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
+      for (sched::RecCursor cur(recs, n_items, grid, cta);;) {
+        const sched::ItemRec rec = cur.next();
+        if (rec.it < 0) break;
+        const Item w = from_rec(rec, nbt, idx, k_max);
         if (w.n <= 0) continue;
         const int qb = q & 1;
         const uint32_t q_addr = smem_u32(q_smem + qb * C::kQBytes);
@@ -266,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
           mbar_wait(&bars->k_full[st], (g / kStages) & 1);
           tr(1, g);
           tc_fence_after();
-          const uint32_t d_s = tmem + ((g & 1) ? C::kTmemS1 : C::kTmemS0);
+          const uint32_t d_s = tmem + (g % kSBufs) * B;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t koff = (kk & 3) * 32;  // 16 bf16 = 32 B inside the swizzle atom
@@ -274,17 +281,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
             const uint64_t b = desc_sw128(k_addr + st * C::kKVBytes + (kk >> 2) * (B * 128) + koff, 16, 1024);
             mma_ss(d_s, a, b, idesc_qk, kk > 0 ? 1u : 0u, leader);
           }
-          tc_commit(&bars->s_full[g & 1], leader);
+          tc_commit(&bars->s_full[g % kSBufs], leader);
           tc_commit(&bars->k_empty[st], leader);
           if (j == w.n - 1) tc_commit(&bars->q_empty[qb], leader);
-          if (pv_g >= 0) issue_pv();
-          pv_g = g;
-          pv_j = j;
-          pv_q = q;
+          if (pv_n == 2) issue_pv();
+          const int t = (pv_h + pv_n) & 1;
+          pv_g[t] = g;
+          pv_j[t] = j;
+          pv_q[t] = q;
+          ++pv_n;
         }
         ++q;
       }
-      if (pv_g >= 0) issue_pv();
+      while (pv_n > 0) issue_pv();
     }
   } else if (warp == 6) {
     produce(true);
@@ -294,10 +303,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
     const int r = quarter * 32 + lane;
     const uint32_t lane_field = static_cast<uint32_t>(quarter * 32) << 16;
     int g = 0, q = 0;
-    for (int k = 0;; ++k) {
-      const int it = sched::snake_item(order, n_items, grid, cta, k);
-      if (it < 0) break;
-      const Item w = decode(it, cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
+    for (sched::RecCursor cur(recs, n_items, grid, cta);;) {
+      const sched::ItemRec rec = cur.next();
+      if (rec.it < 0) break;
+      const Item w = from_rec(rec, nbt, idx, k_max);
       const int row0 = w.seq0 + w.i * B;
       const int nrows = min(B, w.seq_len - w.i * B);
       const bool store = r < nrows;
@@ -309,14 +318,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         }
         continue;
       }
-      const int ob = q & 1;
-      const uint32_t t_o = tmem + lane_field + (ob ? C::kTmemO1 : C::kTmemO0);
+      const uint32_t t_o = tmem + lane_field + C::kTmemO;
       float m_run = -INFINITY, l_run = 0.f;
+      // Key block ids are loaded one block ahead: a global load consumed right after the
+      // s_full wait put its L2 latency (~300 cycles) on every block when S was already ready.
+      int jb_next = w.first;
       for (int j = 0; j < w.n; ++j, ++g) {
-        const int b = g & 1;
-        const uint32_t t_s = tmem + lane_field + (b ? C::kTmemS1 : C::kTmemS0);
-        const int jb = __ldg(w.list + j);
-        mbar_wait_spin(&bars->s_full[b], (g >> 1) & 1);
+        const int b = g % kSBufs;
+        const uint32_t t_s = tmem + lane_field + b * B;
+        const int jb = jb_next;
+        if (j + 1 < w.n) jb_next = __ldg(w.list + j + 1);
+        mbar_wait_spin(&bars->s_full[b], (g / kSBufs) & 1);
         if (threadIdx.x == 64) tr(4, g);
         if (trace != nullptr && blockIdx.x == 0 && g < 256 && lane == 0)  // per-warp S seen (debug)
           trace[3072 + g * 4 + (warp - 2)] = clock64();
@@ -340,11 +352,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         l_run = l_run * alpha + (sum0 + sum1);
         tmem_wait_st();
         if (threadIdx.x == 64) tr(5, g);
-        if (j > 0) {
-          mbar_wait(&bars->o_done, (g - 1) & 1);  // PV_{g-1} (same item) finished writing O
+        // Rescale O only when a lane's max jumped; only then wait for PV_{g-1} (same item) to
+        // finish writing O. Skipping the wait is safe with per-slot barriers: s_full(g) implies
+        // PV_{g-2} completed (in-order pipe, QK_g issued after PV_{g-2}), so o_done[(g-1) % 3]
+        // has completed either PV_{g-4} or PV_{g-1} and the parity test is unambiguous.
+        if (j > 0 && __any_sync(0xffffffffu, rescale)) {
+          mbar_wait(&bars->o_done[(g - 1) % kSBufs], ((g - 1) / kSBufs) & 1);
           if (threadIdx.x == 64) tr(6, g);
           tc_fence_after();
-          if (__any_sync(0xffffffffu, rescale)) {
+          {
 #pragma unroll
             for (int c = 0; c < D / 32; ++c) {
               uint32_t v[32];
@@ -364,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         mbar_arrive(&bars->p_full[b]);
       }
       // Epilogue: wait for the item's last PV, O / l -> bf16 rows; LSE (natural log).
-      mbar_wait(&bars->o_done, (g - 1) & 1);
+      mbar_wait(&bars->o_done[(g - 1) % kSBufs], ((g - 1) / kSBufs) & 1);
       tc_fence_after();
       const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
       uint16_t* orow = out + (static_cast<size_t>(row0 + r) * hq + w.h) * D;
@@ -373,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
       for (int c = 0; c < D / 32; ++c) tmem_ld32(t_o + c * 32, v[c]);
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(&bars->o_free[ob]);  // O buffer may be overwritten by item q + 2
+      mbar_arrive(&bars->o_free);  // O may be overwritten by item q + 1
       if (store) {
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
@@ -406,6 +422,11 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
   const int n_items = hq * nb_total;
   const int32_t* order = sched::build_order(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, n_items, ws, st,
                                             "sb_sparse_attn_fwd/order");
+  auto* recs = reinterpret_cast<sched::ItemRec*>(
+      (reinterpret_cast<uintptr_t>(ws) + sched::order_workspace_bytes(n_items, hq * (k_max + 1)) + 255) & ~uintptr_t(255));
+  sched::q_records_kernel<<<(n_items + 255) / 256, 256, 0, st>>>(order, n_items, cu, blk_off, nseq, nb_total, hq, hsel,
+                                                                 idx, cnt, k_max, recs);
+  launched("sb_sparse_attn_fwd/records");
   const CUtensorMap tq = make_thd_map(q, total, hq, D, kM);
   const CUtensorMap tk = make_thd_map(k, total, hkv, D, B);
   const CUtensorMap tv = make_thd_map(v, total, hkv, D, B);
@@ -414,7 +435,7 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
              "sb_sparse_attn_fwd: smem attribute");
   const int grid = std::min(n_items, sched::num_sms());
   kern<<<grid, kThreads, C::kSmemBytes, st>>>(tq, tk, tv, cu, blk_off, nseq, total, hq, hkv, idx, cnt, hsel, k_max,
-                                              scale * 1.4426950408889634f, o, lse, order, n_items, g_trace);
+                                              scale * 1.4426950408889634f, o, lse, recs, n_items, g_trace);
   launched("sb_sparse_attn_fwd");
 }
 
@@ -425,7 +446,8 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
 SB_API void sb_debug_set_trace(unsigned long long* buf) { sbk::g_trace = buf; }
 
 SB_API size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq, int k_max) {
-  return sbk::sched::order_workspace_bytes(nb_total * hq, hq * (k_max + 1));
+  return sbk::sched::order_workspace_bytes(nb_total * hq, hq * (k_max + 1)) + 256 +
+         sbk::sched::rec_workspace_bytes(nb_total * hq);
 }
 
 SB_API int sb_sparse_attn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* cu_seqlens,

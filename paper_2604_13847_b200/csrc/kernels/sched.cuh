@@ -134,6 +134,89 @@ __device__ __forceinline__ int snake_item(const int32_t* __restrict__ order, int
   return pos < n_items ? __ldg(order + pos) : -1;
 }
 
+// One record per schedule position, so a persistent CTA's roles read an item with one 32-byte
+// load (prefetched a whole item ahead by RecCursor) instead of decoding it at the item
+// boundary through a chain of dependent global loads (order -> blk_off binary search -> cu ->
+// cnt / tr_off -> list[0]); that chain put ~2-3k cycles on every boundary of every role.
+struct ItemRec {
+  int it;       // item id (h * nbt + gi for q items, hk * nbt + gj for kv items)
+  int s;        // sequence
+  int loc;      // block index inside the sequence
+  int seq0;     // first token of the sequence
+  int seq_len;  // tokens in the sequence
+  int n;        // q items: selected key blocks (cnt); kv items: listing selection rows
+  int base;     // q items: selection row srow * nbt + gi; kv items: tr_off[it]
+  int first;    // q items: first selected key block; kv items: first listing entry
+};
+static_assert(sizeof(ItemRec) == 32, "ItemRec is two 16-byte loads");
+
+inline size_t rec_workspace_bytes(int n_items) { return static_cast<size_t>(n_items) * sizeof(ItemRec) + 256; }
+
+__global__ void q_records_kernel(const int32_t* __restrict__ order, int n_items, const int32_t* __restrict__ cu,
+                                 const int32_t* __restrict__ blk_off, int nseq, int nbt, int hq, int hsel,
+                                 const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt, int k_max,
+                                 ItemRec* __restrict__ rec) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n_items) return;
+  ItemRec r;
+  r.it = order[pos];
+  const int h = r.it / nbt, gi = r.it - h * nbt;
+  r.s = seq_of_block(blk_off, nseq, gi);
+  r.loc = gi - blk_off[r.s];
+  r.seq0 = cu[r.s];
+  r.seq_len = cu[r.s + 1] - r.seq0;
+  r.base = (h / (hq / hsel)) * nbt + gi;
+  r.n = cnt[r.base];
+  r.first = r.n > 0 ? idx[static_cast<size_t>(r.base) * k_max] : 0;
+  rec[pos] = r;
+}
+
+__global__ void kv_records_kernel(const int32_t* __restrict__ order, int n_items, const int32_t* __restrict__ cu,
+                                  const int32_t* __restrict__ blk_off, int nseq, int nbt,
+                                  const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent,
+                                  ItemRec* __restrict__ rec) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n_items) return;
+  ItemRec r;
+  r.it = order[pos];
+  const int hk = r.it / nbt, gj = r.it - hk * nbt;
+  r.s = seq_of_block(blk_off, nseq, gj);
+  r.loc = gj - blk_off[r.s];
+  r.seq0 = cu[r.s];
+  r.seq_len = cu[r.s + 1] - r.seq0;
+  r.base = tr_off[r.it];
+  r.n = tr_off[r.it + 1] - r.base;
+  r.first = r.n > 0 ? tr_ent[r.base] : 0;
+  rec[pos] = r;
+}
+
+// Walks a CTA's snake-order records; next() returns the current record (it = -1 past the end)
+// while the load of the following one is already in flight.
+struct RecCursor {
+  const int4* rec;
+  int n_items, grid, cta, k;
+  int4 a, b;
+  __device__ RecCursor(const ItemRec* r, int n, int g, int c) : rec(reinterpret_cast<const int4*>(r)), n_items(n), grid(g), cta(c), k(0) {
+    load();
+  }
+  __device__ __forceinline__ void load() {
+    const int pos = k * grid + ((k & 1) ? (grid - 1 - cta) : cta);
+    if (pos < n_items) {
+      a = __ldg(rec + 2 * pos);
+      b = __ldg(rec + 2 * pos + 1);
+    } else {
+      a = make_int4(-1, 0, 0, 0);
+      b = make_int4(0, 0, 0, 0);
+    }
+  }
+  __device__ __forceinline__ ItemRec next() {
+    const ItemRec r{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    ++k;
+    if (r.it >= 0) load();
+    return r;
+  }
+};
+
 inline int num_sms() {
   static int n = 0;
   if (n == 0) {

@@ -47,3 +47,8 @@ d = d[d > 0]
 print("QK-issue period percentiles 10/50/90/99:", [float(np.percentile(d, q)) for q in (10, 50, 90, 99)])
 big = d > 2 * np.median(d)
 print("blocks with > 2x median period:", int(big.sum()), "of", len(d), "; their excess:", float((d[big] - np.median(d)).sum()), "; total:", float(d.sum()))
+print("per-warp period (S seen -> next S seen):", [float(np.median(np.diff(ps[4:40, w]))) for w in range(4)])
+print("per-warp gap (arrive -> next S seen):", [float(np.median(ps[5:41, w] - pw[4:40, w])) for w in range(4)])
+print("warp-5 S seen minus QK issue of same g:", float(np.median(ps[4:40, 3] - t[4:40, 1])))
+print("warp-2 S seen minus QK issue of same g:", float(np.median(ps[4:40, 0] - t[4:40, 1])))
+print("PV p_full seen minus warp-5 arrive:", float(np.median(t[4:40, 3] - pw[4:40, 3])))
