@@ -38,7 +38,7 @@ using namespace sm100;
 constexpr int kM = 128;                 // UMMA M / Q tile rows
 constexpr int kStages = 2;              // K ring depth
 constexpr int kSBufs = 3;               // S / P buffers in TMEM
-constexpr int kVStages = 3;             // V ring depth (V is consumed last: needs the longest prefetch)
+constexpr int kVStages = 2;             // V ring depth (3 measured no faster; the slot holds the O staging tile)
 constexpr int kThreads = 224;           // 7 warps: Q/K producer, UMMA, 4 softmax, V producer
 constexpr float kRescaleThresh = 8.0f;  // log2 units: lazily rescale O only on a 256x max jump
 
@@ -47,7 +47,8 @@ struct FwdCfg {
   static constexpr int kChunks = D / 64;              // 128-byte swizzle atoms along D
   static constexpr int kQBytes = kChunks * kM * 128;  // one Q tile
   static constexpr int kKVBytes = kChunks * B * 128;  // one K or V block
-  static constexpr int kSmemTiles = 2 * kQBytes + (kStages + kVStages) * kKVBytes;
+  static constexpr int kStageBytes = kChunks * B * 128;  // bf16 O tile staged for the TMA store
+  static constexpr int kSmemTiles = 2 * kQBytes + (kStages + kVStages) * kKVBytes + kStageBytes;
   static constexpr int kTmemO = kSBufs * B;  // S_b at column b * B
   static constexpr uint32_t kTmemCols = (kSBufs * B + D) <= 256 ? 256 : 512;
   static constexpr int kSmemBytes = kSmemTiles + 1024 /*align slack*/ + 256 /*barriers*/;
@@ -80,20 +81,37 @@ __device__ __forceinline__ Item from_rec(const sched::ItemRec& r, int nbt, const
   return w;
 }
 
+// Diagonal block (causal + sequence end: columns >= lim masked): the masked columns of S are
+// overwritten with -inf in TMEM, 32 columns at a time from the warp's first partial chunk, so
+// every block then runs the one unmasked softmax below. This path runs once per item and its
+// code is cold in the instruction cache; an unrolled masked softmax variant (~1100
+// instructions) cost ~3000 cycles per item in instruction fetch alone, this loop is ~60.
+// P of a masked column is 0 from the SFU lanes and <= 2^-126 from the FMA-pipe exp2 lanes
+// (fastmath.cuh clamps at -126): below any bf16 / fp32 tolerance.
+template <int B>
+__device__ __forceinline__ void mask_diag_tmem(uint32_t t_s, int lim) {
+  const int first = __reduce_min_sync(0xffffffffu, lim) >> 5;  // first chunk with a masked column
+  for (int ch = first; ch < B / 32; ++ch) {
+    uint32_t v[32];
+    tmem_ld32(t_s + ch * 32, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = ch * 32 + e < lim ? v[e] : 0xff800000u;
+    tmem_st32(t_s + ch * 32, v);
+  }
+  tmem_wait_st();
+}
+
 // One key block of one query row (this thread's TMEM lane): row max (FMNMX3), lazy rescale
 // decision, P = 2^(S*scale_log2 - m) with packed FFMA2 / FADD2 and the SFU/FMA exp2 split,
-// packed bf16 P written back over the first B/2 columns of S. kMasked handles the diagonal
-// block (causal + sequence end: columns >= lim are masked).
-template <int B, bool kMasked>
-__device__ __forceinline__ void softmax_block(const uint32_t (&sv)[B / 32][32], int lim, float scale_log2,
-                                              float m_run, uint32_t t_s, float& m_use, float& alpha, float& sum,
-                                              bool& rescale) {
+// packed bf16 P written back over the first B/2 columns of S.
+template <int B>
+__device__ __forceinline__ void softmax_block(const uint32_t (&sv)[B / 32][32], float scale_log2, float m_run,
+                                              uint32_t t_s, float& m_use, float& alpha, float& sum, bool& rescale,
+                                              unsigned long long* dbg) {
   float xs[B];
 #pragma unroll
-  for (int c = 0; c < B; ++c) {
-    xs[c] = __uint_as_float(sv[c / 32][c % 32]);
-    if (kMasked) xs[c] = c < lim ? xs[c] : -INFINITY;
-  }
+  for (int c = 0; c < B; ++c) xs[c] = __uint_as_float(sv[c / 32][c % 32]);
   float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
   for (int c = 0; c < B; c += 8) {
@@ -103,6 +121,7 @@ __device__ __forceinline__ void softmax_block(const uint32_t (&sv)[B / 32][32], 
     m3 = fmax3(m3, xs[c + 6], xs[c + 7]);
   }
   const float m_new = fmaxf(m_run, fmax3(m0, m1, fmaxf(m2, m3)) * scale_log2);
+  if (dbg) dbg[1] = clock64();
   rescale = m_new > m_run + kRescaleThresh;
   m_use = rescale ? m_new : m_run;
   alpha = rescale ? ex2_sfu(m_run - m_use) : 1.0f;
@@ -114,15 +133,12 @@ __device__ __forceinline__ void softmax_block(const uint32_t (&sv)[B / 32][32], 
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
       const int pe = c2 * 32 + e;  // column pair (2pe, 2pe+1)
-      f2 p = ex2_pair(ffma2(mk2(xs[2 * pe], xs[2 * pe + 1]), sc, nm), pe);
-      if (kMasked) {
-        p.x = 2 * pe < lim ? p.x : 0.f;
-        p.y = 2 * pe + 1 < lim ? p.y : 0.f;
-      }
+      const f2 p = ex2_pair(ffma2(mk2(xs[2 * pe], xs[2 * pe + 1]), sc, nm), pe);
       acc[e & 3] = fadd2(acc[e & 3], p);
       pw[e] = pack_bf16x2(p.x, p.y);
     }
     tmem_st32(t_s + c2 * 32, pw);  // P (packed bf16) over the first B/2 columns of S
+    if (dbg && c2 < 2) dbg[2 + c2] = clock64();
   }
   const f2 a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
   sum = a01.x + a01.y;
@@ -131,7 +147,7 @@ __device__ __forceinline__ void softmax_block(const uint32_t (&sv)[B / 32][32], 
 template <int D, int B>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-    const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off,
+    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off,
     int nseq, int total_tokens, int hq, int hkv, const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt,
     int hsel, int k_max, float scale_log2, uint16_t* __restrict__ out, float* __restrict__ lse,
     const sched::ItemRec* __restrict__ recs, int n_items, unsigned long long* __restrict__ trace) {
@@ -145,7 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* q_smem = smem;                                // [2]
   uint8_t* k_smem = smem + 2 * C::kQBytes;               // [kStages]
-  uint8_t* v_smem = k_smem + kStages * C::kKVBytes;      // [kStages]
+  uint8_t* v_smem = k_smem + kStages * C::kKVBytes;      // [kVStages]
+  uint8_t* o_stage = v_smem + kVStages * C::kKVBytes;    // O tile for the TMA store (SW128, [chunk][row])
   FwdBars* bars = reinterpret_cast<FwdBars*>(smem + C::kSmemTiles);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -333,21 +350,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         if (trace != nullptr && blockIdx.x == 0 && g < 256 && lane == 0)  // per-warp S seen (debug)
           trace[3072 + g * 4 + (warp - 2)] = clock64();
         tc_fence_after();
+        // Keys of off-diagonal blocks are all valid (earlier blocks of a sequence are full);
+        // the diagonal block masks the causal upper triangle and keys past the sequence end.
+        if (jb == w.i) mask_diag_tmem<B>(t_s, min(min(B, w.seq_len - jb * B), r + 1));
         uint32_t sv[B / 32][32];
 #pragma unroll
         for (int c = 0; c < B / 32; ++c) tmem_ld32(t_s + c * 32, sv[c]);
         tmem_wait_ld();
-        // Keys of off-diagonal blocks are all valid (earlier blocks of a sequence are full);
-        // the diagonal block masks the causal upper triangle and keys past the sequence end.
-        const bool diag = jb == w.i;
-        const int lim = diag ? min(min(B, w.seq_len - jb * B), r + 1) : B;
+        unsigned long long* dbg =
+            (trace != nullptr && blockIdx.x == 0 && g < 256 && threadIdx.x == 64) ? trace + 5120 + g * 4 : nullptr;
+        if (dbg) dbg[0] = clock64();
         float m_use, alpha, sum;
         bool rescale;
-        if (diag) {
-          softmax_block<B, true>(sv, lim, scale_log2, m_run, t_s, m_use, alpha, sum, rescale);
-        } else {
-          softmax_block<B, false>(sv, lim, scale_log2, m_run, t_s, m_use, alpha, sum, rescale);
-        }
+        softmax_block<B>(sv, scale_log2, m_run, t_s, m_use, alpha, sum, rescale, dbg);
+        if (threadIdx.x == 64) tr(7, g);
         const float sum0 = sum, sum1 = 0.f;
         l_run = l_run * alpha + (sum0 + sum1);
         tmem_wait_st();
@@ -380,7 +396,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
         mbar_arrive(&bars->p_full[b]);
       }
       // Epilogue: wait for the item's last PV, O / l -> bf16 rows; LSE (natural log).
+      auto tre = [&](int slot) {  // debug: per-item epilogue stamps of warp 2
+        if (trace != nullptr && blockIdx.x == 0 && q < 256 && threadIdx.x == 64) trace[4096 + q * 4 + slot] = clock64();
+      };
+      tre(0);
       mbar_wait(&bars->o_done[(g - 1) % kSBufs], ((g - 1) / kSBufs) & 1);
+      tre(1);
       tc_fence_after();
       const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
       uint16_t* orow = out + (static_cast<size_t>(row0 + r) * hq + w.h) * D;
@@ -390,7 +411,40 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bars->o_free);  // O may be overwritten by item q + 1
-      if (store) {
+      tre(2);
+      if (nrows == B) {
+        // Full tile: rows -> SW128 staging tile -> one TMA store per 64-column chunk, issued by
+        // one thread and completed asynchronously. Row-per-thread global stores put 32 rows
+        // (8 KB apart) in every warp store: ~1000 LSU cycles per item, 4% of the kernel.
+        if (threadIdx.x == 64) bulk_wait_read();  // the previous item's store has read the tile
+        named_bar_sync(1, 128);
+        if (r < B) {
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int d0 = c * 64 + u * 8;
+              uint4 q4;
+              q4.x = pack_bf16x2(__uint_as_float(v[d0 / 32][d0 % 32]) * inv_l,
+                                 __uint_as_float(v[d0 / 32][d0 % 32 + 1]) * inv_l);
+              q4.y = pack_bf16x2(__uint_as_float(v[d0 / 32][d0 % 32 + 2]) * inv_l,
+                                 __uint_as_float(v[d0 / 32][d0 % 32 + 3]) * inv_l);
+              q4.z = pack_bf16x2(__uint_as_float(v[d0 / 32][d0 % 32 + 4]) * inv_l,
+                                 __uint_as_float(v[d0 / 32][d0 % 32 + 5]) * inv_l);
+              q4.w = pack_bf16x2(__uint_as_float(v[d0 / 32][d0 % 32 + 6]) * inv_l,
+                                 __uint_as_float(v[d0 / 32][d0 % 32 + 7]) * inv_l);
+              *reinterpret_cast<uint4*>(o_stage + c * (B * 128) + r * 128 + ((u ^ (r & 7)) << 4)) = q4;
+            }
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 64) {
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) tma_store_3d(&tm_o, o_stage + c * (B * 128), c * 64, w.h, row0);
+          bulk_commit();
+        }
+      } else if (store) {  // the last (partial) tile of a sequence: the box would cross into the next
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t w16[16];
@@ -399,10 +453,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
             w16[e] = pack_bf16x2(__uint_as_float(v[c][2 * e]) * inv_l, __uint_as_float(v[c][2 * e + 1]) * inv_l);
           store_64B(orow + c * 32, w16);
         }
-        lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = (m_run + log2f(l_run)) * 0.69314718055994531f;
       }
+      if (store) lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = (m_run + log2f(l_run)) * 0.69314718055994531f;
+      tre(3);
       ++q;
     }
+    if (threadIdx.x == 64) bulk_wait_all();  // outstanding O stores read smem and reach global
   }
   tc_fence_before();
   __syncthreads();
@@ -430,11 +486,12 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
   const CUtensorMap tq = make_thd_map(q, total, hq, D, kM);
   const CUtensorMap tk = make_thd_map(k, total, hkv, D, B);
   const CUtensorMap tv = make_thd_map(v, total, hkv, D, B);
+  const CUtensorMap to = make_thd_map(o, total, hq, D, B);
   auto kern = attn_fwd_kernel<D, B>;
   cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes),
              "sb_sparse_attn_fwd: smem attribute");
   const int grid = std::min(n_items, sched::num_sms());
-  kern<<<grid, kThreads, C::kSmemBytes, st>>>(tq, tk, tv, cu, blk_off, nseq, total, hq, hkv, idx, cnt, hsel, k_max,
+  kern<<<grid, kThreads, C::kSmemBytes, st>>>(tq, tk, tv, to, cu, blk_off, nseq, total, hq, hkv, idx, cnt, hsel, k_max,
                                               scale * 1.4426950408889634f, o, lse, recs, n_items, g_trace);
   launched("sb_sparse_attn_fwd");
 }
@@ -442,7 +499,7 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
 }  // namespace
 }  // namespace sbk
 
-// Debug only: device buffer of 256 x 16 uint64 for CTA 0's phase timeline (NULL disables).
+// Debug only: device buffer of 256 x 32 uint64 for CTA 0's phase timeline (NULL disables).
 SB_API void sb_debug_set_trace(unsigned long long* buf) { sbk::g_trace = buf; }
 
 SB_API size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq, int k_max) {

@@ -62,11 +62,14 @@ __device__ __forceinline__ float ex2_sfu(float x) {
 
 // 2^x for a pair: x = j + f, j = rint(x) via the 1.5*2^23 magic-number add (the low mantissa
 // bits of x + magic hold j in two's complement), f in [-0.5, 0.5], 2^f by a degree-3
-// polynomial, j folded into the exponent field with one shift + add. x is clamped to >= -127
-// first so the exponent never wraps (2^-127 ~ 0 for softmax).
+// polynomial, j folded into the exponent field with one shift + add. x is clamped to >= -126
+// first so the exponent never wraps: the polynomial is 0.99998866 < 1 at f = 0, so j = -127
+// would take the bits below zero (0xffffff42, a NaN) -- every x <= -127 (a score 127 log2
+// units under the row max, or a masked -inf) came out NaN. With j >= -126 the result is a
+// non-negative float <= 2^-126 (~0 for softmax).
 __device__ __forceinline__ f2 ex2_poly2(f2 x) {
-  x.x = fmaxf(x.x, -127.0f);
-  x.y = fmaxf(x.y, -127.0f);
+  x.x = fmaxf(x.x, -126.0f);
+  x.y = fmaxf(x.y, -126.0f);
   const f2 t = fadd2(x, mk2(12582912.0f, 12582912.0f));
   const f2 jf = fadd2(t, mk2(-12582912.0f, -12582912.0f));
   const f2 f = ffma2(jf, mk2(-1.0f, -1.0f), x);

@@ -209,6 +209,34 @@ def test_sparse_attn_bwd_vs_oracle(cu, hq, hkv, d, B, mode, keep):
         assert np.linalg.norm(g - ref) / max(1e-12, np.linalg.norm(ref)) < 2e-2, name
 
 
+def test_fwd_bwd_large_dynamic_range():
+    """Scores spanning hundreds of log2 units: exp2 of x <= -127 must give ~0, not NaN (the
+    FMA-pipe exp2 once wrapped its exponent field there), in the fwd and in both bwd passes."""
+    from paper_2604_13847_b200 import ops
+
+    cu, hq, d, B = [0, 700, 2000], 2, 128, 128
+    T = cu[-1]
+    q = (_rand_bf16((T, hq, d), 31).float() * 8).to(torch.bfloat16)  # exact: power-of-two scale
+    k, v, do = _rand_bf16((T, hq, d), 32), _rand_bf16((T, hq, d), 33), _rand_bf16((T, hq, d), 34)
+    lay = _layout(cu, B)
+    idx, cnt = _selection(lay, hq, 0.6, 3)
+    scale = 1.0  # std of the scores ~ 90: most exp2 arguments are far below -127
+    o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+    dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+    torch.cuda.synchronize()
+    for t in (o, lse, dq, dk, dv):
+        assert torch.isfinite(t.float()).all()
+    ic, cc = idx.cpu().numpy(), cnt.cpu().numpy()
+    ro, rlse = orc.sparse_attn_fwd(_bits(q), _bits(k), _bits(v), cu, B, ic, cc, scale)
+    g = o.float().cpu().numpy()
+    assert np.abs(g - ro).max() <= 2e-2 * max(1.0, np.abs(ro).max())
+    np.testing.assert_allclose(lse.cpu().numpy(), rlse, atol=2e-3, rtol=1e-4)
+    rdq, rdk, rdv = orc.sparse_attn_bwd(_bits(q), _bits(k), _bits(v), ro, _bits(do), rlse, cu, B, ic, cc, scale)
+    for got, ref, name in ((dq, rdq, "dq"), (dk, rdk, "dk"), (dv, rdv, "dv")):
+        g = got.float().cpu().numpy()
+        assert np.abs(g - ref).max() <= 2e-2 * max(1.0, np.abs(ref).max()), name
+
+
 def test_bwd_deterministic():
     from paper_2604_13847_b200 import ops
 
