@@ -27,6 +27,7 @@ using namespace sm100;
 
 constexpr int kM = 128;
 constexpr int kStages = 2;
+constexpr int kBwdPoly = 2;  // exp2 pairs of every 8 on the FMA pipe (fastmath.cuh ex2_pair_n)
 constexpr int kThreads = 352;  // warp 0 TMA, warp 1 UMMA, warps 2..9 two column-split math warpgroups, warp 10 TMA (V)
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -177,7 +178,7 @@ __device__ __forceinline__ void dkv_p(const uint32_t (&sv)[NC / 32][32], float s
 #pragma unroll
   for (int pe = 0; pe < NC / 2; ++pe) {
     const int r = 2 * pe;
-    f2 e = ex2_pair(fmul2(mk2(__uint_as_float(sv[r / 32][r % 32]), __uint_as_float(sv[r / 32][r % 32 + 1])), sc), pe);
+    f2 e = ex2_pair_n<kBwdPoly>(fmul2(mk2(__uint_as_float(sv[r / 32][r % 32]), __uint_as_float(sv[r / 32][r % 32 + 1])), sc), pe);
     if (kMasked) {
       e.x = (col0 + r < nq && col0 + r >= r_lo) ? e.x : 0.f;
       e.y = (col0 + r + 1 < nq && col0 + r + 1 >= r_lo) ? e.y : 0.f;
@@ -196,7 +197,7 @@ __device__ __forceinline__ void dq_p(const uint32_t (&sv)[NC / 32][32], float ne
 #pragma unroll
   for (int pe = 0; pe < NC / 2; ++pe) {
     const int c = 2 * pe;
-    f2 e = ex2_pair(ffma2(mk2(__uint_as_float(sv[c / 32][c % 32]), __uint_as_float(sv[c / 32][c % 32 + 1])), sc, nl),
+    f2 e = ex2_pair_n<kBwdPoly>(ffma2(mk2(__uint_as_float(sv[c / 32][c % 32]), __uint_as_float(sv[c / 32][c % 32 + 1])), sc, nl),
                     pe);
     if (kMasked) {
       e.x = col0 + c < lim ? e.x : 0.f;
