@@ -468,6 +468,259 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(
   }
 }
 
+// ------------------------------------------------------------------ two-stream variant
+// The single-stream kernel above is paced by its softmax: one softmax warp per SM
+// sub-partition, ~1300 busy cycles per key block plus ~300 cycles of fixed latency (TMEM
+// load, P store wait, barrier) against a 1024-cycle MMA floor. Here each CTA runs TWO
+// independent item streams (rounds k = s, s + 2, ... of its snake order), each with its own
+// Q / K / V slots, S and O in TMEM (S0 | S1 | O0 | O1), producer warp, UMMA issuer warp and
+// softmax warpgroup, so every sub-partition holds two softmax warps and the tensor core works
+// on one stream while the other one's softmax runs. Per stream the order is QK_j, PV_j,
+// QK_{j+1} (P_j aliases S_j): s_full(j) therefore implies PV_{j-1} completed and a lazy O
+// rescale needs no wait. Registers: WG0 (producers, issuers) drops to 56, the softmax
+// warpgroups rise to 224 (setmaxnreg).
+constexpr int kThreads2 = 384;
+
+template <int D, int B>
+struct Fwd2Cfg {
+  static constexpr int kChunks = D / 64;
+  static constexpr int kQBytes = kChunks * kM * 128;
+  static constexpr int kKVBytes = kChunks * B * 128;
+  static constexpr int kSmemTiles = 2 * kQBytes + 4 * kKVBytes;  // per stream: Q, K, V
+  static constexpr int kTmemO = 2 * B;                          // S_s at s * B, O_s at 2B + s * D
+  static constexpr uint32_t kTmemCols = (2 * B + 2 * D) <= 256 ? 256 : 512;
+  static constexpr int kSmemBytes = kSmemTiles + 1024 + 256;
+};
+
+struct Fwd2Bars {
+  uint64_t q_full[2], q_empty[2], k_full[2], k_empty[2], v_full[2], v_empty[2];
+  uint64_t s_full[2], p_full[2], o_done[2], o_free[2];
+  uint32_t tmem_base;
+};
+
+template <int D, int B>
+__global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
+    const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+    const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ blk_off, int nseq, int total_tokens,
+    int hq, int hkv, const int32_t* __restrict__ idx, int k_max, float scale_log2, uint16_t* __restrict__ out,
+    float* __restrict__ lse, const sched::ItemRec* __restrict__ recs, int n_items,
+    unsigned long long* __restrict__ trace) {
+  using C = Fwd2Cfg<D, B>;
+  // Debug timeline: CTA 0, per stream s and block g < 256: [s][g][slot] (slots: 0 k_full seen
+  // + QK issued, 1 PV issued, 2 S seen by softmax warp 0, 3 P arrived, 4 epilogue start, 5 end).
+  auto tr2 = [&](int st, int g, int slot) {
+    if (trace != nullptr && blockIdx.x == 0 && g < 256) trace[(st * 256 + g) * 8 + slot] = clock64();
+  };
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint8_t* q_smem = smem;                         // [stream]
+  uint8_t* k_smem = smem + 2 * C::kQBytes;        // [stream]
+  uint8_t* v_smem = k_smem + 2 * C::kKVBytes;     // [stream]
+  Fwd2Bars* bars = reinterpret_cast<Fwd2Bars*>(smem + C::kSmemTiles);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbt = blk_off[nseq];
+  const int grid = gridDim.x, cta = blockIdx.x;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars->q_full[s], 1);
+      mbar_init(&bars->q_empty[s], 1);
+      mbar_init(&bars->k_full[s], 1);
+      mbar_init(&bars->k_empty[s], 1);
+      mbar_init(&bars->v_full[s], 1);
+      mbar_init(&bars->v_empty[s], 1);
+      mbar_init(&bars->s_full[s], 1);
+      mbar_init(&bars->p_full[s], 128);
+      mbar_init(&bars->o_done[s], 1);
+      mbar_init(&bars->o_free[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<C::kTmemCols>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp < 4) {
+    setmaxnreg_dec<56>();
+    const int s = warp >> 1;  // warps 0, 1: stream 0; warps 2, 3: stream 1
+    if ((warp & 1) == 0) {
+      // -------------------------------------------------------- TMA producer of stream s
+      if (lane == 0) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        uint8_t* qs = q_smem + s * C::kQBytes;
+        uint8_t* ks = k_smem + s * C::kKVBytes;
+        uint8_t* vs = v_smem + s * C::kKVBytes;
+        int g = 0, q = 0;
+        for (sched::RecCursor cur(recs, n_items, grid, cta, s, 2);;) {
+          const sched::ItemRec rec = cur.next();
+          if (rec.it < 0) break;
+          const Item w = from_rec(rec, nbt, idx, k_max);
+          if (w.n <= 0) continue;
+          const int hk = w.h / (hq / hkv);
+          mbar_wait(&bars->q_empty[s], (q & 1) ^ 1);
+          mbar_expect_tx(&bars->q_full[s], C::kQBytes);
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_3d(qs + c * kM * 128, &tm_q, &bars->q_full[s], c * 64, w.h, w.seq0 + w.i * B);
+          for (int j = 0; j < w.n; ++j, ++g) {
+            const int kv_row = w.seq0 + __ldg(w.list + j) * B;
+            mbar_wait(&bars->k_empty[s], (g & 1) ^ 1);
+            mbar_expect_tx(&bars->k_full[s], C::kKVBytes);
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_load_3d(ks + c * B * 128, &tm_k, &bars->k_full[s], c * 64, hk, kv_row);
+            mbar_wait(&bars->v_empty[s], (g & 1) ^ 1);
+            mbar_expect_tx(&bars->v_full[s], C::kKVBytes);
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_load_3d(vs + c * B * 128, &tm_v, &bars->v_full[s], c * 64, hk, kv_row);
+          }
+          ++q;
+        }
+      }
+    } else {
+      // -------------------------------------------------------- UMMA issuer of stream s
+      const uint32_t leader = elect_one();
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(kM, B, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(kM, D, false, true);
+      const uint32_t q_addr = smem_u32(q_smem + s * C::kQBytes);
+      const uint32_t k_addr = smem_u32(k_smem + s * C::kKVBytes), v_addr = smem_u32(v_smem + s * C::kKVBytes);
+      const uint32_t d_s = tmem + s * B, d_o = tmem + C::kTmemO + s * D;
+      int g = 0, q = 0;
+      for (sched::RecCursor cur(recs, n_items, grid, cta, s, 2);;) {
+        const sched::ItemRec rec = cur.next();
+        if (rec.it < 0) break;
+        const int n = rec.n;
+        if (n <= 0) continue;
+        mbar_wait(&bars->q_full[s], q & 1);
+        for (int j = 0; j < n; ++j, ++g) {
+          mbar_wait(&bars->k_full[s], g & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t koff = (kk & 3) * 32;
+            const uint64_t a = desc_sw128(q_addr + (kk >> 2) * (kM * 128) + koff, 16, 1024);
+            const uint64_t b = desc_sw128(k_addr + (kk >> 2) * (B * 128) + koff, 16, 1024);
+            mma_ss(d_s, a, b, idesc_qk, kk > 0 ? 1u : 0u, leader);
+          }
+          tc_commit(&bars->s_full[s], leader);
+          tc_commit(&bars->k_empty[s], leader);
+          if (lane == 0) tr2(s, g, 0);
+          if (j == n - 1) tc_commit(&bars->q_empty[s], leader);
+          mbar_wait(&bars->v_full[s], g & 1);
+          mbar_wait(&bars->p_full[s], g & 1);
+          if (j == 0) mbar_wait(&bars->o_free[s], (q & 1) ^ 1);  // epilogue of the stream's previous item
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < B / 16; ++kk) {
+            const uint64_t b = desc_sw128(v_addr + kk * 2048, B * 128, 1024);
+            mma_ts(d_o, d_s + kk * 8, b, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u, leader);
+          }
+          tc_commit(&bars->v_empty[s], leader);
+          if (lane == 0) tr2(s, g, 1);
+          if (j == n - 1) tc_commit(&bars->o_done[s], leader);
+        }
+        ++q;
+      }
+    }
+  } else {
+    setmaxnreg_inc<224>();
+    // ---------------------------------------------------------- softmax / epilogue of stream s
+    const int s = (warp >> 2) - 1;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_field = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t t_s = tmem + lane_field + s * B, t_o = tmem + lane_field + C::kTmemO + s * D;
+    int g = 0, q = 0;
+    for (sched::RecCursor cur(recs, n_items, grid, cta, s, 2);;) {
+      const sched::ItemRec rec = cur.next();
+      if (rec.it < 0) break;
+      const Item w = from_rec(rec, nbt, idx, k_max);
+      const int row0 = w.seq0 + w.i * B;
+      const int nrows = min(B, w.seq_len - w.i * B);
+      const bool store = r < nrows;
+      if (w.n <= 0) {  // nothing selected: zero output, LSE = -inf
+        if (store) {
+          uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<size_t>(row0 + r) * hq + w.h) * D);
+          for (int e = 0; e < D / 8; ++e) dst[e] = make_uint4(0, 0, 0, 0);
+          lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = -INFINITY;
+        }
+        continue;
+      }
+      float m_run = -INFINITY, l_run = 0.f;
+      int jb_next = w.first;
+      for (int j = 0; j < w.n; ++j, ++g) {
+        const int jb = jb_next;
+        if (j + 1 < w.n) jb_next = __ldg(w.list + j + 1);
+        mbar_wait_spin(&bars->s_full[s], g & 1);
+        if (r == 0) tr2(s, g, 2);
+        tc_fence_after();
+        if (jb == w.i) mask_diag_tmem<B>(t_s, min(min(B, w.seq_len - jb * B), r + 1));
+        uint32_t sv[B / 32][32];
+#pragma unroll
+        for (int c = 0; c < B / 32; ++c) tmem_ld32(t_s + c * 32, sv[c]);
+        tmem_wait_ld();
+        float m_use, alpha, sum;
+        bool rescale;
+        softmax_block<B>(sv, scale_log2, m_run, t_s, m_use, alpha, sum, rescale, nullptr);
+        l_run = l_run * alpha + sum;
+        tmem_wait_st();
+        // PV_{j-1} completed before S_j was committed (same issuer, in order): O is final.
+        if (j > 0 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(t_o + c * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+            tmem_st32(t_o + c * 32, v);
+          }
+          tmem_wait_st();
+        }
+        m_run = m_use;
+        tc_fence_before();
+        if (r == 0) tr2(s, g, 3);
+        mbar_arrive(&bars->p_full[s]);
+      }
+      // Epilogue: the item's last PV, O / l -> bf16 rows; LSE (natural log).
+      if (r == 0) tr2(s, g - 1, 4);
+      mbar_wait(&bars->o_done[s], q & 1);
+      tc_fence_after();
+      const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
+      uint32_t v[D / 32][32];
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) tmem_ld32(t_o + c * 32, v[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars->o_free[s]);  // O may be overwritten by the stream's next item
+      if (store) {
+        uint16_t* orow = out + (static_cast<size_t>(row0 + r) * hq + w.h) * D;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t w16[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            w16[e] = pack_bf16x2(__uint_as_float(v[c][2 * e]) * inv_l, __uint_as_float(v[c][2 * e + 1]) * inv_l);
+          store_64B(orow + c * 32, w16);
+        }
+        lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = (m_run + log2f(l_run)) * 0.69314718055994531f;
+      }
+      if (r == 0) tr2(s, g - 1, 5);
+      ++q;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem);
+  }
+}
+
 unsigned long long* g_trace = nullptr;  // debug timeline buffer (sb_debug_set_trace)
 
 template <int D, int B>
@@ -491,6 +744,20 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
   cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes),
              "sb_sparse_attn_fwd: smem attribute");
   const int grid = std::min(n_items, sched::num_sms());
+  static const bool two = [] {
+    const char* e = std::getenv("SB_FWD_STREAMS");
+    return !(e && e[0] == '1');
+  }();
+  if (two) {
+    using C2 = Fwd2Cfg<D, B>;
+    auto k2 = attn_fwd2_kernel<D, B>;
+    cuda_check(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::kSmemBytes),
+               "sb_sparse_attn_fwd: smem attribute");
+    k2<<<grid, kThreads2, C2::kSmemBytes, st>>>(tq, tk, tv, blk_off, nseq, total, hq, hkv, idx, k_max,
+                                                scale * 1.4426950408889634f, o, lse, recs, n_items, g_trace);
+    launched("sb_sparse_attn_fwd");
+    return;
+  }
   kern<<<grid, kThreads, C::kSmemBytes, st>>>(tq, tk, tv, to, cu, blk_off, nseq, total, hq, hkv, idx, cnt, hsel, k_max,
                                               scale * 1.4426950408889634f, o, lse, recs, n_items, g_trace);
   launched("sb_sparse_attn_fwd");

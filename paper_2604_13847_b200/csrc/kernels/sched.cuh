@@ -194,9 +194,11 @@ __global__ void kv_records_kernel(const int32_t* __restrict__ order, int n_items
 // while the load of the following one is already in flight.
 struct RecCursor {
   const int4* rec;
-  int n_items, grid, cta, k;
+  int n_items, grid, cta, k, kstep;
   int4 a, b;
-  __device__ RecCursor(const ItemRec* r, int n, int g, int c) : rec(reinterpret_cast<const int4*>(r)), n_items(n), grid(g), cta(c), k(0) {
+  // Rounds k0, k0 + kstep, ... of the CTA's snake order (kstep 2: one of two item streams).
+  __device__ RecCursor(const ItemRec* r, int n, int g, int c, int k0 = 0, int step = 1)
+      : rec(reinterpret_cast<const int4*>(r)), n_items(n), grid(g), cta(c), k(k0), kstep(step) {
     load();
   }
   __device__ __forceinline__ void load() {
@@ -211,7 +213,7 @@ struct RecCursor {
   }
   __device__ __forceinline__ ItemRec next() {
     const ItemRec r{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    ++k;
+    k += kstep;
     if (r.it >= 0) load();
     return r;
   }
