@@ -33,3 +33,4 @@ for s in range(2):
     print("  median QK issued -> S seen:", np.median(t[s, r, 2] - t[s, r, 0]))
     nx = t[s, 3:151, 0] - t[s, 2:150, 1]
     print("  median PV issued -> next QK issued:", np.median(nx))
+    print("  median PV issued -> next k_full seen:", np.median(t[s, 3:151, 6] - t[s, 2:150, 1]))
