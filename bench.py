@@ -264,6 +264,10 @@ def c3_global_batch(world: int, seed: int, layers: int = 1):
 
 
 def main():
+    if os.environ.get("SB_HANG_DUMP"):  # debug: dump every thread's Python stack, then exit
+        import faulthandler
+
+        faulthandler.dump_traceback_later(int(os.environ["SB_HANG_DUMP"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
