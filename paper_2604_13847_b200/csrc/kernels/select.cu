@@ -249,8 +249,89 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(
 
 // ---- K4a: sorted softmax masses per row -> workspace, then per-(s, r) fp64 mean ----
 
+// Rows of at most 32 * E blocks: one warp per row, element e of lane l is column e * 32 + l,
+// so register e's lane butterfly is the block kernel's warp-e reduction and summing the
+// registers in order is its sum over warps -- max, exponentials, z, the normalised values and
+// the sorted output are bit-identical to row_sorted_mass_kernel, without its ~30 CTA-wide
+// barriers per row (bitonic network in registers: shuffles for strides < 32, register pairs
+// above; the compare-exchange keeps the block kernel's predicate, NaNs included).
+template <int E>
+__global__ void __launch_bounds__(256) row_sorted_mass_warp_kernel(const float* __restrict__ scores,
+                                                                   const int32_t* __restrict__ blk_off,
+                                                                   const int64_t* __restrict__ tri_off, int nseq,
+                                                                   int nb_total, float* __restrict__ sorted) {
+  const int gi = blockIdx.x * 8 + (threadIdx.x >> 5), h = blockIdx.y, lane = threadIdx.x & 31;
+  if (gi >= nb_total) return;
+  const int64_t tri = tri_off[nseq];
+  const int s = seq_of_block(blk_off, nseq, gi);
+  const int i = gi - blk_off[s];
+  const int n = i + 1;
+  if (n > 32 * E) return;  // the block kernel's rows
+  const size_t off = static_cast<size_t>(h) * tri + tri_off[s] + static_cast<int64_t>(i) * (i + 1) / 2;
+  const float* row = scores + off;
+  float v[E];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = e * 32 + lane;
+    v[e] = j < n ? row[j] : 0.f;
+    if (j < n) mx = fmaxf(mx, v[e]);
+  }
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float z = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = e * 32 + lane;
+    float t = 0.f;
+    if (j < n) {
+      v[e] = __expf(v[e] - mx);
+      t = v[e];
+    }
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    z += t;
+  }
+  const float inv = 1.0f / z;
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = e * 32 + lane < n ? v[e] * inv : -1.0f;
+  // Bitonic sort of 32 * E values, descending (element x = e * 32 + lane).
+#pragma unroll
+  for (int size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const int rs = stride >> 5;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (e & rs) continue;
+          const bool desc = ((e * 32 + lane) & size) == 0;
+          const float a = v[e], b = v[e + rs];
+          if ((a < b) == desc) {
+            v[e] = b;
+            v[e + rs] = a;
+          }
+        }
+      } else {
+        const bool is_lo = (lane & stride) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const float other = __shfl_xor_sync(0xffffffffu, v[e], stride);
+          const int x_lo = (e * 32 + lane) & ~stride;
+          const bool desc = (x_lo & size) == 0;
+          const float a = is_lo ? v[e] : other, b = is_lo ? other : v[e];
+          const bool swap = (a < b) == desc;
+          v[e] = is_lo ? (swap ? b : a) : (swap ? a : b);
+        }
+      }
+    }
+  }
+  float* dst = sorted + off;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (e * 32 + lane < n) dst[e * 32 + lane] = v[e];
+}
+
 __global__ void row_sorted_mass_kernel(const float* __restrict__ scores, const int32_t* __restrict__ blk_off,
-                                       const int64_t* __restrict__ tri_off, int nseq, int pow2,
+                                       const int64_t* __restrict__ tri_off, int nseq, int pow2, int min_n,
                                        float* __restrict__ sorted) {
   extern __shared__ float buf[];
   __shared__ float red[32];
@@ -259,6 +340,7 @@ __global__ void row_sorted_mass_kernel(const float* __restrict__ scores, const i
   const int s = seq_of_block(blk_off, nseq, gi);
   const int i = gi - blk_off[s];
   const int n = i + 1;
+  if (n <= min_n) return;  // the warp kernel's rows
   int p2 = 1;
   while (p2 < n) p2 <<= 1;
   const float* row = scores + static_cast<size_t>(h) * tri + tri_off[s] + static_cast<int64_t>(i) * (i + 1) / 2;
@@ -400,10 +482,24 @@ SB_API int sb_coverage_profile(const float* scores, const int32_t* blk_off, cons
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     float* sorted = static_cast<float*>(workspace);
     if (nb_total > 0) {
-      dim3 grid(nb_total, hs);
-      sbk::row_sorted_mass_kernel<<<grid, 256, p2 * sizeof(float), st>>>(scores, blk_off, tri_off, nseq, p2,
-                                                                        sorted);
+      // Rows of <= 256 blocks: one warp each; longer rows: one CTA each (shared-memory sort).
+      const dim3 wgrid((nb_total + 7) / 8, hs);
+      if (p2 <= 32) {
+        sbk::row_sorted_mass_warp_kernel<1><<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, sorted);
+      } else if (p2 <= 64) {
+        sbk::row_sorted_mass_warp_kernel<2><<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, sorted);
+      } else if (p2 <= 128) {
+        sbk::row_sorted_mass_warp_kernel<4><<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, sorted);
+      } else {
+        sbk::row_sorted_mass_warp_kernel<8><<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, sorted);
+      }
       sbk::launched("sb_coverage_profile/sort");
+      if (nb_max > 256) {
+        dim3 grid(nb_total, hs);
+        sbk::row_sorted_mass_kernel<<<grid, 256, p2 * sizeof(float), st>>>(scores, blk_off, tri_off, nseq, p2, 256,
+                                                                          sorted);
+        sbk::launched("sb_coverage_profile/sort_long");
+      }
     }
     const size_t sorted_bytes = (static_cast<size_t>(tri_total_host) * hs * sizeof(float) + 255) & ~size_t(255);
     double* partial = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + sorted_bytes);

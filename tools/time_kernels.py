@@ -28,6 +28,8 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(10):
         ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)
         ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
+        ops.coverage_profile(S, lay)
+        ops.block_scores(q, k, lay)
     torch.cuda.synchronize()
 agg = {}
 for e in prof.events():
