@@ -53,7 +53,8 @@ int sb_block_pool(const uint16_t* x, const int32_t* cu_seqlens, const int32_t* b
                   int nb_total, int heads, int head_dim, int block_size, float* xbar,
                   void* stream);
 
-/* K2: S[h][row(s,i)][j] = scale * <Qbar[s,i,h], Kbar[s,j,h / (Hq/Hkv)]> for j <= i.
+/* K2: S[h][row(s,i)][j] = scale * <Qbar[s,i,h], Kbar[s,j,h / (Hq/Hkv)]> for j <= i
+ * (head_dim 64 or 128; fp32 fma over d in order).
  * Replaces: the RoutingProfile score vectors (reference workload.hpp:15-22). */
 int sb_block_scores(const float* qbar, const float* kbar, const int32_t* blk_off,
                     const int64_t* tri_off, int nseq, int nb_max, int hq, int hkv, int head_dim,

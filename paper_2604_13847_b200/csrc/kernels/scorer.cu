@@ -85,62 +85,61 @@ __global__ void __launch_bounds__(kPoolThreads) block_pool_kernel(
   }
 }
 
-constexpr int kTile = 64;
-constexpr int kTk = 32;
+constexpr int kRowsPerCta = 8;  // one warp per score row
 
-// S tile (ti, tj) of sequence s, q head h: rows i in [64 ti, 64 ti + 64), cols j in
-// [64 tj, ...), only j <= i < nb_s written. 256 threads, 4x4 outputs per thread.
+// Scores of 8 consecutive rows i of sequence s, q head h (one warp per row): the rows' Qbar
+// and 32-key chunks of Kbar (transposed, conflict-free) are staged in shared memory and lane
+// l computes S[i][j0 + l] for j0 + l <= i. Every score is acc = fma over d = 0..D-1 in order
+// from 0, times scale -- the same operation sequence as the 64x64-tile kernel this replaced
+// (bit-identical output), which launched mostly-empty CTAs and ran four latency-bound rounds
+// each (36 us on C2).
+template <int D>
 __global__ void __launch_bounds__(256) block_scores_kernel(
     const float* __restrict__ qbar, const float* __restrict__ kbar, const int32_t* __restrict__ blk_off,
-    const int64_t* __restrict__ tri_off, int nseq, int hq, int hkv, int d, float scale,
-    float* __restrict__ scores) {
-  const int ti = blockIdx.x, tj = blockIdx.y;
-  if (tj > ti) return;
-  const int s = blockIdx.z / hq;
-  const int h = blockIdx.z % hq;
+    const int64_t* __restrict__ tri_off, int nseq, int hq, int hkv, float scale, float* __restrict__ scores) {
+  constexpr int kV = D / 4;  // float4 per row
+  const int s = blockIdx.y, h = blockIdx.z;
   const int nb = blk_off[s + 1] - blk_off[s];
-  if (ti * kTile >= nb) return;
-  const int hk = h / (hq / hkv);
+  const int i0 = blockIdx.x * kRowsPerCta;
+  if (i0 >= nb) return;
   const int b0 = blk_off[s];
-
-  __shared__ float qs[kTk][kTile + 4];
-  __shared__ float ks[kTk][kTile + 4];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[4][4] = {};
-  for (int c0 = 0; c0 < d; c0 += kTk) {
-    // Load 64 rows x 32 cols of Qbar and Kbar (transposed into [col][row]).
-    for (int e = threadIdx.x; e < kTile * kTk; e += 256) {
-      const int row = e / kTk, col = e % kTk;
-      const int qi = ti * kTile + row, kj = tj * kTile + row;
-      qs[col][row] = qi < nb ? qbar[(static_cast<size_t>(b0 + qi) * hq + h) * d + c0 + col] : 0.f;
-      ks[col][row] = kj < nb ? kbar[(static_cast<size_t>(b0 + kj) * hkv + hk) * d + c0 + col] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int c = 0; c < kTk; ++c) {
-      float a[4], b[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = qs[c][ty + 16 * u];
-        b[u] = ks[c][tx + 16 * u];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int w = 0; w < 4; ++w) acc[u][w] = fmaf(a[u], b[w], acc[u][w]);
-    }
-    __syncthreads();
+  const int hk = h / (hq / hkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = i0 + warp;
+  const int i_last = min(i0 + kRowsPerCta - 1, nb - 1);
+  __shared__ float4 qs[kRowsPerCta][kV];
+  __shared__ float kt[D][33];
+  for (int e = threadIdx.x; e < kRowsPerCta * kV; e += blockDim.x) {
+    const int r = e / kV, c = e % kV;
+    qs[r][c] = i0 + r < nb ? reinterpret_cast<const float4*>(qbar + (static_cast<size_t>(b0 + i0 + r) * hq + h) * D)[c]
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const int64_t tri_total = tri_off[nseq];
-  float* srow = scores + static_cast<size_t>(h) * tri_total + tri_off[s];
+  float* srow = scores + static_cast<size_t>(h) * tri_off[nseq] + tri_off[s] + static_cast<int64_t>(i) * (i + 1) / 2;
+  for (int j0 = 0; j0 <= i_last; j0 += 32) {
+    __syncthreads();  // the previous chunk is consumed (first pass: qs is written)
+    for (int e = threadIdx.x; e < 32 * kV; e += blockDim.x) {
+      const int jr = e / kV, c = e % kV;
+      const int j = j0 + jr;
+      const float4 x = j <= i_last ? reinterpret_cast<const float4*>(kbar + (static_cast<size_t>(b0 + j) * hkv + hk) * D)[c]
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      kt[4 * c][jr] = x.x;
+      kt[4 * c + 1][jr] = x.y;
+      kt[4 * c + 2][jr] = x.z;
+      kt[4 * c + 3][jr] = x.w;
+    }
+    __syncthreads();
+    const int j = j0 + lane;
+    if (i <= i_last && j <= i) {
+      float acc = 0.f;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int i = ti * kTile + ty + 16 * u;
-    if (i >= nb) continue;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const int j = tj * kTile + tx + 16 * w;
-      if (j <= i) srow[static_cast<int64_t>(i) * (i + 1) / 2 + j] = acc[u][w] * scale;
+      for (int c = 0; c < kV; ++c) {
+        const float4 qv = qs[warp][c];
+        acc = fmaf(qv.x, kt[4 * c][lane], acc);
+        acc = fmaf(qv.y, kt[4 * c + 1][lane], acc);
+        acc = fmaf(qv.z, kt[4 * c + 2][lane], acc);
+        acc = fmaf(qv.w, kt[4 * c + 3][lane], acc);
+      }
+      srow[j] = acc * scale;
     }
   }
 }
@@ -167,14 +166,17 @@ SB_API int sb_block_scores(const float* qbar, const float* kbar, const int32_t* 
                            void* stream) {
   return sbk::abi_call([&] {
     sbk::require(hq >= 1 && hkv >= 1 && hq % hkv == 0, "hq must be a positive multiple of hkv");
-    sbk::require(head_dim % sbk::kTk == 0 && head_dim > 0, "head_dim must be a multiple of 32");
+    sbk::require(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128");
     if (nseq == 0 || nb_max == 0) return;
     sbk::require(qbar && kbar && blk_off && tri_off && scores, "null pointer");
-    const int tiles = (nb_max + sbk::kTile - 1) / sbk::kTile;
-    sbk::require(static_cast<int64_t>(nseq) * hq <= 65535, "nseq * hq must be <= 65535");
-    dim3 grid(tiles, tiles, nseq * hq);
-    sbk::block_scores_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        qbar, kbar, blk_off, tri_off, nseq, hq, hkv, head_dim, scale, scores);
+    sbk::require(nseq <= 65535 && hq <= 65535, "nseq and hq must be <= 65535");
+    dim3 grid((nb_max + sbk::kRowsPerCta - 1) / sbk::kRowsPerCta, nseq, hq);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (head_dim == 128) {
+      sbk::block_scores_kernel<128><<<grid, 256, 0, st>>>(qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, scores);
+    } else {
+      sbk::block_scores_kernel<64><<<grid, 256, 0, st>>>(qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, scores);
+    }
     sbk::launched("sb_block_scores");
   });
 }
