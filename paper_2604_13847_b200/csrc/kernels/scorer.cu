@@ -1,88 +1,59 @@
 // K1 block mean-pool and K2 block scorer (MoBA gate: PAPER.md:119).
 //
-// K1 streams X [T][H][D] once with 128-bit coalesced loads (one CTA per block covers the
-// whole contiguous B x H x D slab) and writes the fp32 block means: HBM-bound.
-// K2 forms the per-sequence lower-triangular score matrix S = scale * Qbar Kbar^T as a
-// tiled fp32 GEMM (64 x 64 tiles, only tiles on/below the diagonal launch work).
+// K1 streams X [T][H][D] once with 128-bit coalesced loads (CTAs split each block's
+// contiguous B x H x D slab by columns) and writes the fp32 block means: HBM-bound.
+// K2 forms the per-sequence lower-triangular score matrix S = scale * Qbar Kbar^T (one warp
+// per score row, Kbar staged through shared memory in 32-key chunks).
 #include "common.cuh"
 #include "sb_kernels.h"
 
 namespace sbk {
 namespace {
 
-constexpr int kPoolThreads = 256;
-constexpr int kPoolMaxChunks = 4;  // (H*D/8) / 256 <= 4  ->  H*D <= 8192
+constexpr int kPoolThreads = 128;
+constexpr int kPoolRows = 8;  // rows in flight per thread
 
-// One CTA per global block. Thread c owns 16-byte column chunk(s) c, c+256, ... of the
-// flattened [H*D] row and accumulates the block's valid rows in fp32.
+// CTA (gi, y): block gi, 16-byte column chunks [128 y, 128 y + 128) of the flattened [H*D]
+// row, one chunk per thread, the block's valid rows accumulated in fp32 in row order (the
+// same per-element sum as the one-CTA-per-block kernel this replaced). Splitting the columns
+// over grid.y gives C2 1024 CTAs (~7 per SM, no 1-vs-2 CTA imbalance across SMs) instead of
+// 256 whole-slab CTAs.
 __global__ void __launch_bounds__(kPoolThreads) block_pool_kernel(
     const uint16_t* __restrict__ x, const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off,
     int nseq, int row_elems, int block_size, float* __restrict__ xbar) {
   const int gi = blockIdx.x;
+  const int ch = blockIdx.y * kPoolThreads + threadIdx.x;
+  const int chunks = row_elems >> 3;
+  if (ch >= chunks) return;
   const int s = seq_of_block(blk_off, nseq, gi);
   const int i = gi - blk_off[s];
   const int t0 = cu[s] + i * block_size;
-  const int t1 = min(t0 + block_size, cu[s + 1]);
-  const int chunks = row_elems >> 3;
-  float acc[kPoolMaxChunks][8];
+  const int rows = min(t0 + block_size, cu[s + 1]) - t0;
+  float acc[8];
 #pragma unroll
-  for (int c = 0; c < kPoolMaxChunks; ++c)
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t0) * row_elems) + ch;
+  auto add = [&](const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[c][e] = 0.f;
-
-  const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t0) * row_elems);
-  const int rows = t1 - t0;
-  int r = 0;
-  // Four rows in flight per iteration for memory-level parallelism.
-  for (; r + 4 <= rows; r += 4) {
-    uint4 v[4][kPoolMaxChunks];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int c = 0; c < kPoolMaxChunks; ++c) {
-        const int ch = threadIdx.x + c * kPoolThreads;
-        if (ch < chunks) v[u][c] = __ldg(base + static_cast<size_t>(r + u) * chunks + ch);
-      }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int c = 0; c < kPoolMaxChunks; ++c) {
-        const int ch = threadIdx.x + c * kPoolThreads;
-        if (ch < chunks) {
-          const uint32_t w[4] = {v[u][c].x, v[u][c].y, v[u][c].z, v[u][c].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            acc[c][2 * e] += __uint_as_float(w[e] << 16);
-            acc[c][2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
-          }
-        }
-      }
-  }
-  for (; r < rows; ++r) {
-#pragma unroll
-    for (int c = 0; c < kPoolMaxChunks; ++c) {
-      const int ch = threadIdx.x + c * kPoolThreads;
-      if (ch < chunks) {
-        const uint4 vv = __ldg(base + static_cast<size_t>(r) * chunks + ch);
-        const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          acc[c][2 * e] += __uint_as_float(w[e] << 16);
-          acc[c][2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
-        }
-      }
+    for (int e = 0; e < 4; ++e) {
+      acc[2 * e] += __uint_as_float(w[e] << 16);
+      acc[2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
     }
+  };
+  int r = 0;
+  for (; r + kPoolRows <= rows; r += kPoolRows) {
+    uint4 v[kPoolRows];
+#pragma unroll
+    for (int u = 0; u < kPoolRows; ++u) v[u] = __ldg(base + static_cast<size_t>(r + u) * chunks);
+#pragma unroll
+    for (int u = 0; u < kPoolRows; ++u) add(v[u]);
   }
+  for (; r < rows; ++r) add(__ldg(base + static_cast<size_t>(r) * chunks));
   const float inv = 1.0f / static_cast<float>(rows);
   float4* out = reinterpret_cast<float4*>(xbar + static_cast<size_t>(gi) * row_elems);
-#pragma unroll
-  for (int c = 0; c < kPoolMaxChunks; ++c) {
-    const int ch = threadIdx.x + c * kPoolThreads;
-    if (ch < chunks) {
-      out[2 * ch] = make_float4(acc[c][0] * inv, acc[c][1] * inv, acc[c][2] * inv, acc[c][3] * inv);
-      out[2 * ch + 1] = make_float4(acc[c][4] * inv, acc[c][5] * inv, acc[c][6] * inv, acc[c][7] * inv);
-    }
-  }
+  out[2 * ch] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+  out[2 * ch + 1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
 }
 
 constexpr int kRowsPerCta = 8;  // one warp per score row
@@ -151,11 +122,11 @@ SB_API int sb_block_pool(const uint16_t* x, const int32_t* cu_seqlens, const int
                          int nb_total, int heads, int head_dim, int block_size, float* xbar, void* stream) {
   return sbk::abi_call([&] {
     sbk::require(heads >= 1 && (head_dim == 64 || head_dim == 128), "heads >= 1 and head_dim in {64,128}");
-    sbk::require(heads * head_dim <= 8 * 256 * 4, "heads * head_dim must be <= 8192");
     sbk::require(block_size == 64 || block_size == 128, "block_size must be 64 or 128");
     if (nb_total == 0 || nseq == 0) return;
     sbk::require(x && cu_seqlens && blk_off && xbar, "null pointer");
-    sbk::block_pool_kernel<<<nb_total, sbk::kPoolThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+    const dim3 grid(nb_total, (heads * head_dim / 8 + sbk::kPoolThreads - 1) / sbk::kPoolThreads);
+    sbk::block_pool_kernel<<<grid, sbk::kPoolThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         x, cu_seqlens, blk_off, nseq, heads * head_dim, block_size, xbar);
     sbk::launched("sb_block_pool");
   });
