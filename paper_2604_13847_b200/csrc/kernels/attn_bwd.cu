@@ -316,6 +316,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
   auto tr = [&](int slot, int g) {
     if (trace != nullptr && blockIdx.x == 0 && g < 256 && (threadIdx.x & 31) == 0) trace[g * 16 + slot] = clock64();
   };
+  // Per-item boundary stamps (items t < 64): 0 K/V TMA issued, 1 issuer starts waiting for
+  // kv_full, 2 kv_full seen, 3 math sees acc_done, 4 math epilogue done.
+  auto tri = [&](int slot, int t) {
+    if (trace != nullptr && blockIdx.x == 0 && t < 64 && (threadIdx.x & 31) == 0) trace[4096 + t * 8 + slot] = clock64();
+  };
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -398,6 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
           tma_load_3d(k_smem + c * kM * 128, &tm_k, &bars->kv_full, c * 64, w.hk, kv0);
           tma_load_3d(v_smem + c * kM * 128, &tm_v, &bars->kv_full, c * 64, w.hk, kv0);
         }
+        tri(0, t);
       }
       for (int m = 0; m < items; ++m, ++g) {
         const int st = g % kStages;
@@ -505,7 +511,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
         const int items = w.ne * sg;
         if (items == 0) continue;
+        tri(1, t);
         mbar_wait(&bars->kv_full, t & 1);
+        tri(2, t);
         issue_st(g);
         issue_dpt(g);
         if (items == 1) tc_commit(&bars->kv_empty, leader);  // last S^T / dP^T of the item issued
@@ -625,6 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
       }
       if (items > 0) {
         mbar_wait(&bars->acc_done, t & 1);
+        if (threadIdx.x == 64) tri(3, t);
         tc_fence_after();
         ++t;
       }
@@ -655,6 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
           }
         }
       }
+      if (threadIdx.x == 64 && items > 0) tri(4, t - 1);
       tc_fence_before();  // epilogue TMEM reads precede the next item's dV / dK (ordered via pt/dst_full)
     }
   }

@@ -14,12 +14,14 @@ q, k, v, do = (torch.randn((T, H, D), generator=g, device="cuda").to(torch.bfloa
 S = ops.block_scores(q, k, lay)
 idx, cnt = ops.topk_select(S, lay, torch.from_numpy(k_seq).cuda(), int(k_seq.max()))
 o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)
-buf = torch.zeros(256 * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(256 * 16 + 64 * 8, dtype=torch.int64, device="cuda")
 for it in range(3):
     lib.sb_debug_set_trace_bwd(ctypes.c_void_p(buf.data_ptr() if it == 2 else 0))
     ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
 torch.cuda.synchronize()
-t = buf.cpu().numpy().reshape(256, 16).astype(np.int64)
+allb = buf.cpu().numpy().astype(np.int64)
+t = allb[:4096].reshape(256, 16)
+ti = allb[4096:].reshape(64, 8)
 n = int((t[:, 0] > 0).sum())
 r = slice(2, n - 2)
 print("pairs traced", n)
@@ -38,3 +40,12 @@ print("producer: lead of q_full arrive over its use:", med(t[r, 8] - t[r, 13]))
 print("producer: Q TMA issue -> landed:", med(t[r, 14] - t[r, 12]))
 print("producer: Q landed -> St issue start:", med(t[r, 8] - t[r, 14]))
 print("UMMA: issue_st start -> St issued (incl. waits):", med(t[r, 9] - t[r, 8]))
+
+nt = int((ti[:, 0] > 0).sum())
+print("items traced", nt)
+print("t  KV issued | issuer kv wait start | kv_full seen | (wait) | prev acc_done seen | prev epi done")
+for tt in range(1, min(nt, 14)):
+    print(tt, int(ti[tt, 0] - ti[tt, 0]), int(ti[tt, 1] - ti[tt, 0]), int(ti[tt, 2] - ti[tt, 0]), int(ti[tt, 2] - ti[tt, 1]),
+          int(ti[tt - 1, 3] - ti[tt, 0]), int(ti[tt - 1, 4] - ti[tt, 0]))
+print("median K/V latency (issued -> seen):", float(np.median(ti[1:nt, 2] - ti[1:nt, 0])))
+print("median issuer wait on kv_full:", float(np.median(ti[1:nt, 2] - ti[1:nt, 1])))
