@@ -270,6 +270,7 @@ struct DkvBars {
   uint64_t st_free;            // math -> UMMA: S^T read into registers (the next S^T may overwrite)
   uint64_t pds_part[2];        // math -> UMMA: P^T and dS^T (bf16) of 32-column chunk c2 packed over dP^T
   uint64_t acc_done;           // UMMA -> epilogue: the item's dV / dK are final
+  uint64_t epi_free[kStages];  // epilogue -> producer: the item's dV / dK store read ring stage st
   uint32_t tmem_base;
 };
 
@@ -308,11 +309,15 @@ template <int D, int B>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+    const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dv,
     const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off, int nseq, int hq, int hkv, int hsel,
     const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent, const float* __restrict__ lse2,
     const float* __restrict__ dvec, int tp, float scale, float scale_log2, uint16_t* __restrict__ dk,
     uint16_t* __restrict__ dv, const int32_t* __restrict__ order, int n_items, unsigned long long* trace) {
   using C = DkvCfg<D, B>;
+  // D = B = 128: an item's dV / dK (32 KB each) are stored by TMA through the Q / dO slots of
+  // the ring stage its last pair used, free once acc_done fires (see the epilogue).
+  constexpr bool kStagedEpi = D == 128 && B == 128;
   auto tr = [&](int slot, int g) {
     if (trace != nullptr && blockIdx.x == 0 && g < 256 && (threadIdx.x & 31) == 0) trace[g * 16 + slot] = clock64();
   };
@@ -354,6 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     mbar_init(&bars->pds_part[0], 256);
     mbar_init(&bars->pds_part[1], 256);
     mbar_init(&bars->acc_done, 1);
+    for (int st = 0; st < kStages; ++st) mbar_init(&bars->epi_free[st], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kCols>(&bars->tmem_base);
@@ -389,6 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
       tma_prefetch(&tm_do);
     }
     int g = 0, t = 0;  // global pair counter, item counter
+    uint32_t epi_need = 0;            // bit st: an item epilogue is staging through ring stage st
+    int epi_uses0 = 0, epi_uses1 = 0;  // epilogues assigned to stage 0 / 1 so far
     for (int k = 0;; ++k) {
       const int it = sched::snake_item(order, n_items, grid, cta, k);
       if (it < 0) break;
@@ -423,6 +431,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         }
         // Q and dO are separate rings: the UMMA releases Q_i after dK_i and dO_i after dV_i.
         if (lane == 0) tr(11, g);
+        if (kStagedEpi && ((epi_need >> st) & 1u)) {  // an item's dV / dK store reads this stage
+          mbar_wait(&bars->epi_free[st], ((st ? epi_uses1 : epi_uses0) - 1) & 1);
+          epi_need &= ~(1u << st);
+        }
         mbar_wait(&bars->q_empty[st], ph ^ 1);
         if (lane == 0) tr(12, g);
         if (lane == 0) {
@@ -455,6 +467,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->do_full[st]);
+      }
+      if (kStagedEpi) {  // the item's epilogue stages through its last pair's ring stage
+        const int sl = (g - 1) % kStages;
+        if (sl) {
+          ++epi_uses1;
+        } else {
+          ++epi_uses0;
+        }
+        epi_need |= 1u << sl;
       }
       ++t;
     }
@@ -640,6 +661,48 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
       // Epilogue: dV and dK * scale for the valid key rows (zeros if nobody selected the block);
       // warpgroup hf writes output columns [hf * D/2, (hf + 1) * D/2).
       const bool store = c < nkv;
+      if (kStagedEpi && items > 0 && nkv == kM) {
+        // Full key tile: dV -> the Q slot, dK -> the dO slot of the ring stage the item's last
+        // pair used (all its UMMAs are complete), SW128 [chunk hf][key row], then TMA stores.
+        // Row-per-thread stores held the math warps ~3000 cycles per item (skip-store bound
+        // 6 % of the pass). The producer reloads that stage only after epi_free[sl].
+        const int sl = (g - 1) % kStages;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          const uint32_t col = (part == 0 ? C::kDV : C::kDK) + hf * (D / 2);
+          const float mul = part == 0 ? 1.0f : scale;
+          uint8_t* sp = (part == 0 ? q_smem : do_smem) + sl * C::kQBytes + hf * (kM * 128) + c * 128;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            uint32_t v[32];
+            tmem_ld32(tmem + lf + col + cc * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int u = cc * 4 + k;
+              uint4 q4;
+              q4.x = pack_bf16x2(__uint_as_float(v[8 * k]) * mul, __uint_as_float(v[8 * k + 1]) * mul);
+              q4.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
+              q4.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
+              q4.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
+              *reinterpret_cast<uint4*>(sp + ((u ^ (c & 7)) << 4)) = q4;
+            }
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 256);
+        if (threadIdx.x == 64) {
+#pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            tma_store_3d(&tm_dv, q_smem + sl * C::kQBytes + ch * (kM * 128), ch * 64, w.hk, kv0);
+            tma_store_3d(&tm_dk, do_smem + sl * C::kQBytes + ch * (kM * 128), ch * 64, w.hk, kv0);
+          }
+          bulk_commit();
+          bulk_wait_read();
+          mbar_arrive(&bars->epi_free[sl]);
+        }
+      } else {
+        if (kStagedEpi && items > 0 && threadIdx.x == 64) mbar_arrive(&bars->epi_free[(g - 1) % kStages]);
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
         const uint32_t col = (part == 0 ? C::kDV : C::kDK) + hf * (D / 2);
@@ -664,9 +727,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
           }
         }
       }
+      }
       if (threadIdx.x == 64 && items > 0) tri(4, t - 1);
       tc_fence_before();  // epilogue TMEM reads precede the next item's dV / dK (ordered via pt/dst_full)
     }
+    if (threadIdx.x == 64) bulk_wait_all();  // outstanding dV / dK stores reach global before exit
   }
   tc_fence_before();
   __syncthreads();
@@ -1172,10 +1237,12 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
     const CUtensorMap tdo = make_thd_map(d_o, total, hq, D, B);
     const CUtensorMap tk = make_thd_map(k, total, hkv, D, kM);
     const CUtensorMap tv = make_thd_map(v, total, hkv, D, kM);
+    const CUtensorMap tdk = make_thd_map(dk, total, hkv, D, kM);
+    const CUtensorMap tdv = make_thd_map(dv, total, hkv, D, kM);
     auto kern = attn_bwd_dkv_kernel<D, B>;
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes),
                "sb_sparse_attn_bwd: smem attribute (dkv)");
-    kern<<<std::min(kv_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, cu, blk_off, nseq, hq, hkv, hsel,
+    kern<<<std::min(kv_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, tdk, tdv, cu, blk_off, nseq, hq, hkv, hsel,
                                                                    tr_off, tr_ent, lse2, dvec, w.tp, scale,
                                                                    scale_log2, dk, dv, order_kv, kv_items, g_trace_bwd);
     launched("sb_sparse_attn_bwd/dkv");
