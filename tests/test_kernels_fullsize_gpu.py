@@ -95,3 +95,16 @@ def test_c5_long_context(keep):
     the CTA path), GQA 4:1 group selection, k = ceil(keep * 1024); kv head 0's group checked."""
     k = int(math.ceil(keep * 1024))
     _run_and_check([0, 131072], 8, 2, 128, 128, 2, [k], [0, 1, 2, 3], 400)
+
+
+@pytest.mark.parametrize("d,B", [(128, 128), (64, 64)])
+def test_ragged_many_items_per_cta(d, B):
+    """Ragged sequence lengths (partial last tiles) with ~10-40 work items per persistent CTA:
+    exercises the staged TMA-store epilogues of the dq pass (Q/dO staging buffer, stage_free)
+    and of the dK/dV pass (last pair's ring stage, epi_free) interleaved with the direct-store
+    path of partial tiles, over many item boundaries per CTA."""
+    lens = [5000, 3001, 777, 12345, 130, 2112, 1, 4095, 9000]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nb = [(n + B - 1) // B for n in lens]
+    k_seq = [max(1, int(math.ceil(0.3 * m))) for m in nb]
+    _run_and_check(list(cu), 16, 16, d, B, 16, k_seq, [0, 15], 500)
