@@ -131,6 +131,24 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+C2_WORKLOAD = ("C2: 32K-token packed varlen micro-batch per rank ([12288, 8192, 4096, 2048x4], SURVEY 8d), "
+               "32 heads MHA, d128, B128, per-sequence keep U[0.05,0.5], scorer+profile+selector+fwd+bwd")
+
+
+def c3_workload(world: int, layers: int, table_src: str) -> str:
+    """The C3 workload label, shared by our arm and the CPU reference arm."""
+    return (f"C3: 40% 32K / 60% 2K global batch (reference generator, seed 42, gbs={5 * world}), "
+            f"SAB plan mbs=5 (one packed micro-batch per rank), {layers} layers, per-layer DST "
+            f"(Mean anchor, p=0.1, global scope, coverage base, {table_src}) on the generator's "
+            "routing profiles (all-gathered), GPU block scores for selection, 32 heads MHA, d128, B128, "
+            "scorer+allgather+DST+selector+fwd+bwd")
+
+
+def cost_table_source() -> str:
+    tpath = os.path.join(ROOT, "profiles", "b200_cost_table_h32_d128_b128.csv")
+    return "GPU-measured cost table" if os.path.exists(tpath) else "synthetic cost table"
+
+
 def host_cores() -> int:
     """Host threads this process may use (affinity / cgroup aware). torchrun sets
     OMP_NUM_THREADS=1 per rank; the CPU arm overrides that to use the whole host."""
@@ -217,14 +235,11 @@ def run_reference_arm(args, rank, world):
     value = flops / (ms * 1e-3) / 1e12
     sample = (f"q head 0 of 32, {'layer 0 (DST keep count)' if c3 else 'one layer'}, of rank 0's {T}-token "
               f"micro-batch ({len(cu) - 1} seqs): scorer, profile, selector, fwd, bwd")
-    workload_txt = ("C3: 40% 32K / 60% 2K global batch, SAB plan, per-layer DST, 32 heads MHA, d128, B128, fwd+bwd "
-                    "(CPU sample: rank 0, layer 0, q head 0)" if c3 else
-                    "C2: 32K-token packed varlen micro-batch per rank, 32 heads, d128, B128, per-sequence keep "
-                    "U[0.05,0.5], fwd+bwd (CPU sample: q head 0)")
+    workload_txt = c3_workload(world, args.layers, cost_table_source()) if c3 else C2_WORKLOAD
     line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_txt, "sample": "1 of 32 heads", "warmup_run": warm_done,
+            "config": {"workload": workload_txt, "sample": "CPU port: " + sample, "warmup_run": warm_done,
                        "steps_timed": len(times), "budget_s": budget_s},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -306,26 +321,19 @@ def main():
 
     if workload_kind == "c2":
         cu, k_seq = workload(rank)
-        config = {"workload": "C2: 32K-token packed varlen micro-batch per rank ([12288, 8192, 4096, 2048x4], SURVEY "
-                              "8d), 32 heads MHA, d128, B128, per-sequence keep U[0.05,0.5], "
-                              "scorer+profile+selector+fwd+bwd", "seqs_rank0": int(len(cu) - 1)}
+        config = {"workload": C2_WORKLOAD, "seqs_rank0": int(len(cu) - 1)}
     else:
         lengths_all, profiles_all = c3_global_batch(world, CFG["seed"], args.layers)
         # GPU-measured cost table (profiler.py, committed under profiles/) when present, as SURVEY
         # 8(f) item 1 intends; the reference's synthetic table otherwise.
         tpath = os.path.join(ROOT, "profiles", "b200_cost_table_h32_d128_b128.csv")
         table = api().load_table(tpath)[0] if os.path.exists(tpath) else api().synthesize_table(block_size=B)
-        table_src = "GPU-measured cost table" if os.path.exists(tpath) else "synthetic cost table"
+        table_src = cost_table_source()
         bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=table)
         mine = [int(lengths_all[i]) for i in bins[rank][0]]
         cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
         k_seq = None
-        config = {"workload": f"C3: 40% 32K / 60% 2K global batch (reference generator, seed 42, gbs={5 * world}), "
-                              f"SAB plan mbs=5 (one packed micro-batch per rank), {args.layers} layers, per-layer DST "
-                              f"(Mean anchor, p=0.1, global scope, coverage base, {table_src}) on the generator's "
-                              "routing profiles "
-                              "(all-gathered), GPU block scores for selection, 32 heads MHA, d128, B128, "
-                              "scorer+allgather+DST+selector+fwd+bwd",
+        config = {"workload": c3_workload(world, args.layers, table_src),
                   "tokens_per_rank": [int(x) for x in np.array([sum(int(lengths_all[i]) for i in b[0]) for b in bins])]}
     T = int(cu[-1])
     lay = ops.VarlenLayout.build(cu, B, device=dev)
