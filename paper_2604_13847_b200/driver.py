@@ -209,8 +209,13 @@ def main():
     ap.add_argument("--varlen", action="store_true", help="opt-in varlen-aware DST cost (predict_members at B)")
     ap.add_argument("--project-pp", type=int, default=0, help="also project a PP-stage 1F1B pipeline from the "
                                                               "measured per-layer times (pp_projection.py)")
+    ap.add_argument("--heads", type=int, default=32, help="query heads")
+    ap.add_argument("--kv-heads", type=int, default=32, help="kv heads; < --heads = GQA with group-shared selection "
+                                                             "(BASELINE C4: 32q / 8kv)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
+    if args.heads % args.kv_heads:
+        ap.error("--heads must be a multiple of --kv-heads")
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -225,7 +230,7 @@ def main():
     table = api().load_table(args.table)[0] if args.table else None
     drv = Driver(args.strategy, gbs=args.gbs_per_rank * world, mbs=args.mbs, layers=args.layers, dist_spec=dist_spec,
                  table=table, varlen_block_size=128 if args.varlen else 0, project_pp=args.project_pp, rank=rank,
-                 world=world,
+                 world=world, heads=args.heads, kv_heads=args.kv_heads,
                  device=torch.device("cuda", local))
     recs = drv.run(args.iters, args.out)
     if rank == 0:
