@@ -88,7 +88,7 @@ def main():
         print(json.dumps(r), flush=True)
         rows.append(r)
         del S, idx, cnt, o, lse
-    res = dict(workload=f"C5: 1 x {T} tokens, {Hq}q/{Hkv}kv heads (GQA group selection), d={D}, B={B}",
+    res = dict(workload=f"C5: 1 x {T} tokens, {Hq}q/{Hkv}kv heads{" (GQA group selection)" if group > 1 else ""}, d={D}, B={B}",
                peak_tflops=peak_tf, peak_kind=peak_kind, device=torch.cuda.get_device_name(), rows=rows)
     if a.out:
         os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
