@@ -23,6 +23,14 @@ def test_iteration_row_format_and_summary():
     assert driver.ITER_HEADER.count(",") == row.count(",")
 
 
+def test_cli_rejects_ungrouped_heads(monkeypatch):
+    """--heads must be a multiple of --kv-heads (GQA groups); rejected before any CUDA call."""
+    monkeypatch.setattr("sys.argv", ["driver", "--heads", "32", "--kv-heads", "5"])
+    with pytest.raises(SystemExit) as e:
+        driver.main()
+    assert e.value.code == 2
+
+
 @pytest.mark.gpu
 def test_driver_short_run(tmp_path):
     import torch
