@@ -1164,7 +1164,7 @@ unsigned long long* g_trace_bwd = nullptr;  // debug timeline buffer (sb_debug_s
 unsigned long long* g_trace_dq = nullptr;   // debug timeline buffer (sb_debug_set_trace_dq)
 
 struct BwdWorkspace {
-  size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, rec_q, total;
+  size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, order_kv_matched, rec_q, total;
   int tp;
 };
 
@@ -1188,6 +1188,8 @@ BwdWorkspace bwd_layout(int total, int nb_total, int hq, int hkv, int hsel, int 
   off = align256(off + sched::order_workspace_bytes(hq * nb_total, hq * (k_max + 1)));
   w.order_kv = off;
   off = align256(off + sched::order_workspace_bytes(hkv * nb_total, hkv * (kMaxKvCost + 1)));
+  w.order_kv_matched = off;
+  off = align256(off + static_cast<size_t>(hkv) * nb_total * 4);
   w.rec_q = off;
   off = align256(off + sched::rec_workspace_bytes(hq * nb_total));
   w.total = off;
@@ -1220,8 +1222,23 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   transpose_sel_kernel<<<(kv_items + 3) / 4, 128, 0, st>>>(idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 1,
                                                             tr_cnt, tr_off, tr_ent);
   launched("sb_sparse_attn_bwd/transpose_fill");
-  const int32_t* order_kv = sched::build_order(sched::CostFromLists{tr_off, hq / hsel, kMaxKvCost, nb_total, hkv},
-                                               kv_items, ws + w.order_kv, st, "sb_sparse_attn_bwd/order_kv");
+  const int32_t* order_kv_lpt = sched::build_order(sched::CostFromLists{tr_off, hq / hsel, kMaxKvCost, nb_total, hkv},
+                                                   kv_items, ws + w.order_kv, st, "sb_sparse_attn_bwd/order_kv");
+  // Round matching (sched.cuh) runs its rounds in sequence on one CTA, ~5.3 us per round of 148
+  // items on B200; it wins ~6 % of the dK/dV pass where items are long (C5: -4 to -10 % bwd) and
+  // loses where they are short (C2: 295 us of matching for ~110 us won). Use it only when 6 % of
+  // the dK/dV upper-bound estimate (hq * NB * k_max q tiles at ~2.3 us, causal half) exceeds it.
+  const int grid_kv = std::min(kv_items, sms);
+  const double match_us = 5.3 * ((kv_items + grid_kv - 1) / grid_kv);
+  const double dkv_est_us = static_cast<double>(hq) * nb_total * k_max * 2.3 / 2.0 / grid_kv;
+  const int32_t* order_kv = order_kv_lpt;
+  if (match_us < 0.06 * dkv_est_us) {
+    int32_t* matched = reinterpret_cast<int32_t*>(ws + w.order_kv_matched);
+    sched::match_rounds_kernel<<<1, sched::kMatchThreads, 0, st>>>(sched::ListCost{tr_off, hq / hsel}, order_kv_lpt,
+                                                                   kv_items, grid_kv, matched);
+    launched("sb_sparse_attn_bwd/order_kv_match");
+    order_kv = matched;
+  }
   const int q_items = hq * nb_total;
   const int32_t* order_q = sched::build_order(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, q_items,
                                               ws + w.order_q, st, "sb_sparse_attn_bwd/order_q");

@@ -128,6 +128,77 @@ int32_t* build_order(Key key, int n_items, void* ws, cudaStream_t st, const char
   return order;
 }
 
+// Round matching over a longest-first order. The snake layout hands every CTA exactly one item
+// per round of `grid` consecutive positions; plain snake ignores what each CTA already holds, so
+// when a round straddles two heads (head-major order) or costs fall steeply inside a round the
+// per-CTA totals drift apart (modelled 1.03-1.11 max/mean at C2 / C5). Here, round by round, the
+// largest item of the round goes to the least-loaded CTA so far (ties by index), written back at
+// that CTA's snake slot, so the hot kernels walk `out` exactly as they walk `order`. Items stay in
+// their round, so head-major L2 locality is kept. One CTA runs the rounds in sequence.
+// Only the placement changes: every item is still computed whole by one CTA, so outputs are
+// bit-identical.
+// 1024 threads: thread (target = t & 255, chunk = t >> 8) counts its quarter of the pairwise
+// compares and adds them into the target's rank, so a round costs ~40 compares and 4 barriers.
+constexpr int kMatchThreads = 1024;
+template <typename Cost>
+__global__ void __launch_bounds__(kMatchThreads) match_rounds_kernel(Cost cost, const int32_t* __restrict__ order,
+                                                                     int n_items, int grid, int32_t* __restrict__ out) {
+  __shared__ int load[256], item_cost[256], item_id[256], cta_at[256], rank_cta[256], rank_item[256];
+  const int t = threadIdx.x, tgt = t & 255, chunk = t >> 8;
+  const int per = (grid + 3) / 4, u0 = chunk * per, u1 = min(grid, u0 + per);
+  if (t < 256) load[t] = 0;
+  const int rounds = (n_items + grid - 1) / grid;
+  for (int r = 0; r < rounds; ++r) {
+    const int base = r * grid;
+    const int m = min(grid, n_items - base);
+    const bool odd = r & 1;
+    if (t < 256) {
+      rank_cta[t] = 0;
+      rank_item[t] = 0;
+      if (t < m) {
+        item_id[t] = order[base + t];
+        item_cost[t] = cost(item_id[t]);
+      }
+    }
+    __syncthreads();
+    // CTAs whose snake slot in this round exists (all of them except in the last round).
+    if (tgt < grid && (odd ? grid - 1 - tgt : tgt) < m) {
+      const int L = load[tgt];
+      int rk = 0;
+      for (int u = u0; u < u1; ++u) {
+        if ((odd ? grid - 1 - u : u) >= m) continue;
+        const int Lu = load[u];
+        rk += (Lu < L) || (Lu == L && u < tgt);
+      }
+      if (rk) atomicAdd(&rank_cta[tgt], rk);
+    }
+    if (tgt < m) {
+      const int c = item_cost[tgt];
+      int rk = 0;
+      for (int u = u0; u < min(u1, m); ++u) {
+        const int cu = item_cost[u];
+        rk += (cu > c) || (cu == c && u < tgt);
+      }
+      if (rk) atomicAdd(&rank_item[tgt], rk);
+    }
+    __syncthreads();
+    if (t < grid && (odd ? grid - 1 - t : t) < m) cta_at[rank_cta[t]] = t;
+    __syncthreads();
+    if (t < m) {
+      const int cta = cta_at[rank_item[t]];
+      out[base + (odd ? grid - 1 - cta : cta)] = item_id[t];
+      load[cta] += item_cost[t];
+    }
+    __syncthreads();
+  }
+}
+
+struct ListCost {  // dkv item cost in q tiles: (#selection rows listing it) * heads per row, + 1 boundary
+  const int32_t* tr_off;
+  int per_entry;
+  __device__ int operator()(int item) const { return (tr_off[item + 1] - tr_off[item]) * per_entry + 1; }
+};
+
 // Item handled by CTA `cta` of `grid` in round k of the snake order (or -1 when exhausted).
 __device__ __forceinline__ int snake_item(const int32_t* __restrict__ order, int n_items, int grid, int cta, int k) {
   const int pos = k * grid + ((k & 1) ? (grid - 1 - cta) : cta);
