@@ -1,18 +1,27 @@
 #!/usr/bin/env python
 """Benchmark of the SparseBalance hot path on B200.
 
-Workload (BASELINE.json configs[1], "C2"): per rank one packed varlen micro-batch of 32768
-tokens (cu_seqlens) drawn from the reference workload generator (40% 32K / 60% 2K bimodal,
-proj/core/src/workload.cpp:239-271, seeded by rank), 32 heads, head_dim 128, block 128,
-per-sequence keep ratios ~ U[0.05, 0.5]; synthetic bf16 Q/K/V/dO ~ N(0,1).
+Headline workload at every N (BASELINE.json configs[2], "C3", one weak-scaling family from 1 to
+8 GPUs): the reference workload generator's 40% 32K / 60% 2K global batch of gbs = 5 * N samples
+(proj/core/src/workload.cpp:239-271, seed 42), planned by SAB into one packed micro-batch per
+rank (sab.cpp:224-273), 36 layers, 32 heads MHA, d128, B128. Q/K carry planted block-routing
+structure (synth.py: the generator's own pre-sort routing draws per member), so the GPU block
+scores reproduce the generator's concentration. One step per rank =
 
-One step = the whole hot path over the micro-batch: block scorer (K1+K2), coverage profile +
-coverage-at-grid (K4), top-k selector (K3), sparse attention forward (K5) and backward (K6),
-and (N > 1) the per-rank workload-estimate allgather the tuner needs. Inputs (256 MB each) are
-larger than the 126 MB L2, so no explicit flush between steps.
+    scorer pre-pass over all layers (K1 + K2 + K4 coverage profiles)
+    -> one D2H of the profiles, local make_micro_batch merge + coverage tables
+    -> one all-gather of {x, k_base, C(K) per layer} (N > 1)
+    -> pooled host DST (Mean anchor, p = 0.1, global scope, coverage base) -> k_final per layer
+    -> per layer: top-k selector (K3) + sparse attention fwd (K5) + bwd (K6)
 
 value = useful TFLOP/s of the whole job = sum over ranks of useful selected-block FLOPs
-(14 * d * sum e_ij per q head: 4 fwd + 10 bwd) / max-over-ranks step time.
+(14 * d * sum e_ij per q head: 4 fwd + 10 bwd) / max-over-ranks step time. max_over_mean is
+taken over per-rank BUSY time (CUDA events around each rank's own kernels, excluding the
+all-gather wait and host DST), per step as the reference's Eq. 9 (sim.cpp:478-485).
+
+At N = 1 the line also carries measured sub-records: C2 (configs[1], one 32K packed layer),
+C5 (configs[4], one 128K sequence, GQA 32/8, keep 0.1) and C1 (configs[0], 4K, H8, d64, B64,
+keep 0.25, forward latency beside the CPU oracle on the same input).
 """
 from __future__ import annotations
 
@@ -32,26 +41,28 @@ sys.path.insert(0, ROOT)
 
 METRIC = "max-over-ranks sparse-attn step ms & useful TFLOPS at 1/2/4/8 B200 vs CPU ref"
 CFG = dict(tokens=32768, heads=32, head_dim=128, block=128, keep_lo=0.05, keep_hi=0.5, seed=42)
+C3_DIST = dict(short_weight=0.6, short_log_mean=float(np.log(2048)), short_log_sigma=0.0,
+               long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
+COST_TABLE = os.path.join(ROOT, "profiles", "b200_cost_table_h32_d128_b128.csv")
 
 
 def peaks():
-    """(bf16 TF/s, HBM GB/s, source). The roofline kernel runs inside a multi-millisecond step
-    repeated back to back, so the SUSTAINED bf16 figure of MEASURED_PEAKS.json is the
-    denominator (the burst figure applies to a kernel timed alone)."""
+    """MEASURED_PEAKS.json: (burst bf16 TF/s, sustained bf16 TF/s, sustained clock MHz, HBM GB/s, source).
+    The roofline denominator is the BURST figure: the timed windows are ~0.1-1 s after idle, and
+    the sustained figure was taken at a lower power-capped clock than these kernels run at."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        if "bf16_tflops_sustained" in p:
-            return float(p["bf16_tflops_sustained"]), float(p["hbm_gbs"]), "measured sustained"
-        return float(p["bf16_tflops"]), float(p["hbm_gbs"]), "measured burst"
+        return (float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                p.get("clocks_under_load", {}).get("sm_mhz_median"), float(p["hbm_gbs"]), "measured")
     except Exception:
-        return 1590.0, 6650.0, "fallback"
+        return 1590.0, 1400.0, 1300.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def workload(rank: int):
+def c2_workload(rank: int):
     """C2 micro-batch of 32768 tokens: the SURVEY.md section 8(d) example composition
     [12288, 8192, 4096, 2048 x 4] packed with cu_seqlens, and per-sequence keep ratios
-    U[0.05, 0.5] seeded by rank (so ranks carry different sparse work)."""
+    U[0.05, 0.5] seeded by rank."""
     lens = [12288, 8192, 4096, 2048, 2048, 2048, 2048]
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     rng = np.random.default_rng(CFG["seed"] + 7919 * rank)
@@ -61,10 +72,12 @@ def workload(rank: int):
     return cu, k_seq
 
 
-def useful_flops(cu, B, idx, cnt, d):
-    """(fwd, bwd) useful FLOPs: 4*d*sum(e_ij) and 10*d*sum(e_ij) over q heads, where e_ij is the
-    number of unmasked score entries of pair (i, j): r_i * c_j off the diagonal and
-    r_i (r_i + 1) / 2 on the causal diagonal."""
+workload = c2_workload  # tools/ import the old name
+
+
+def pair_entries(cu, B, idx, cnt):
+    """sum over selection rows of e_ij (unmasked score entries of pair (i, j)): r_i * c_j off the
+    diagonal, r_i (r_i + 1) / 2 on it; and the executed-tile count."""
     cu = np.asarray(cu, np.int64)
     nb = (np.diff(cu) + B - 1) // B
     blk = np.concatenate([[0], np.cumsum(nb)])
@@ -79,7 +92,15 @@ def useful_flops(cu, B, idx, cnt, d):
     r = rows[None, :, None]
     diag = sel == local[None, :, None]
     e = np.where(valid, np.where(diag, r * (r + 1) // 2, r * kv_rows), 0).sum(dtype=np.int64)
-    return 4.0 * d * float(e), 10.0 * d * float(e)
+    return float(e), float(valid.sum())
+
+
+def useful_flops(cu, B, idx, cnt, d, hq=None):
+    """(fwd, bwd) useful FLOPs: 4*d*sum(e_ij) and 10*d*sum(e_ij) over q heads. idx/cnt rows are
+    per selection head; with group-shared selection (hsel < hq) each row serves hq / hsel heads."""
+    e, _ = pair_entries(cu, B, idx, cnt)
+    mult = (hq // idx.shape[0]) if hq else 1
+    return 4.0 * d * e * mult, 10.0 * d * e * mult
 
 
 class ClockSampler:
@@ -131,22 +152,24 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-C2_WORKLOAD = ("C2: 32K-token packed varlen micro-batch per rank ([12288, 8192, 4096, 2048x4], SURVEY 8d), "
-               "32 heads MHA, d128, B128, per-sequence keep U[0.05,0.5], scorer+profile+selector+fwd+bwd")
+C2_LABEL = ("C2: 32K-token packed varlen micro-batch ([12288, 8192, 4096, 2048x4], SURVEY 8d), 32 heads MHA, d128, "
+            "B128, per-sequence keep U[0.05,0.5], scorer+profile+selector+fwd+bwd, one layer")
 
 
-def c3_workload(world: int, layers: int, table_src: str) -> str:
-    """The C3 workload label, shared by our arm and the CPU reference arm."""
-    return (f"C3: 40% 32K / 60% 2K global batch (reference generator, seed 42, gbs={5 * world}), "
-            f"SAB plan mbs=5 (one packed micro-batch per rank), {layers} layers, per-layer DST "
-            f"(Mean anchor, p=0.1, global scope, coverage base, {table_src}) on the generator's "
-            "routing profiles (all-gathered), GPU block scores for selection, 32 heads MHA, d128, B128, "
-            "scorer+allgather+DST+selector+fwd+bwd")
+def c3_label(world: int, layers: int, table_src: str) -> str:
+    return (f"C3: 40% 32K / 60% 2K global batch (reference generator, seed 42, gbs={5 * world}), SAB plan mbs=5 "
+            f"(one packed micro-batch per rank), {layers} layers, planted block-routing Q/K (generator pre-sort "
+            f"routing draws), closed-loop per-layer DST from the GPU coverage profiles (Mean anchor, p=0.1, global "
+            f"scope, coverage base, {table_src}), 32 heads MHA, d128, B128, "
+            "scorer+profile D2H+allgather+DST+selector+fwd+bwd")
 
 
-def cost_table_source() -> str:
-    tpath = os.path.join(ROOT, "profiles", "b200_cost_table_h32_d128_b128.csv")
-    return "GPU-measured cost table" if os.path.exists(tpath) else "synthetic cost table"
+def cost_table():
+    from paper_2604_13847_b200.host import api
+
+    if os.path.exists(COST_TABLE):
+        return api().load_table(COST_TABLE)[0], "GPU-measured cost table " + os.path.relpath(COST_TABLE, ROOT)
+    return api().synthesize_table(block_size=CFG["block"]), "synthetic cost table"
 
 
 def host_cores() -> int:
@@ -158,16 +181,24 @@ def host_cores() -> int:
         return max(1, os.cpu_count() or 1)
 
 
-def c3_rank0_layer0(world, layers):
-    """Rank 0's packed micro-batch of the C3 global batch (SAB plan on the same cost table as the
-    GPU arm) and its layer-0 DST keep count per sequence (the pooled host DST, bit-identical to
-    what every GPU rank decides)."""
-    from paper_2604_13847_b200 import dp
+def c3_global_batch(world: int, seed: int, layers: int = 1, sorted_: bool = True):
+    """C3: the reference workload generator's 40% 32K / 60% 2K bimodal mix, gbs = 5 * dp ->
+    (lengths, per-sample per-layer routing profiles)."""
     from paper_2604_13847_b200.host import api
 
+    lengths, profiles = api().generate_samples(5 * world, layers, CFG["block"], seed=seed, dist=C3_DIST,
+                                               sorted=sorted_)
+    return np.asarray(lengths), profiles
+
+
+def c3_rank0_layer0(world, layers):
+    """CPU-arm sample: rank 0's packed micro-batch of the C3 global batch (same SAB plan and cost
+    table as the GPU arm) and a layer-0 keep count per sequence from the pooled host DST over the
+    generator's routing profiles (the GPU arm's closed-loop counts come from its own scores)."""
+    from paper_2604_13847_b200 import dp
+
     lengths_all, profiles_all = c3_global_batch(world, CFG["seed"], layers)
-    tpath = os.path.join(ROOT, "profiles", "b200_cost_table_h32_d128_b128.csv")
-    table = api().load_table(tpath)[0] if os.path.exists(tpath) else api().synthesize_table(block_size=CFG["block"])
+    table, _ = cost_table()
     bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=table)
     pooled = []
     for r in range(world):
@@ -181,28 +212,24 @@ def c3_rank0_layer0(world, layers):
     return cu, np.minimum(int(k_final[0][0]), nb).astype(np.int32)
 
 
+def _bf16_np(rng, shape):
+    return (rng.standard_normal(shape).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference has no CPU attention; the CPU arm is this repo's
     oracle port of the path (oracle/sb_oracle.c, fp64, all host threads) on a bounded sample of
-    the same workload (q head 0 of rank 0's micro-batch: 1/32 of a step), scaled per unit."""
+    the same workload (q head 0 of rank 0's micro-batch: 1/32 of a layer), scaled per unit."""
     if rank != 0:
         return
     from oracle import device as orc
 
-    c3 = world > 1 or args.workload == "c3"
-    if c3:
-        cu, k_seq = c3_rank0_layer0(world, args.layers)
-    else:
-        cu, k_seq = workload(0)
+    c3 = args.workload == "c3"
+    cu, k_seq = c3_rank0_layer0(world, args.layers) if c3 else c2_workload(0)
     T, D, B = int(cu[-1]), CFG["head_dim"], CFG["block"]
     rng = np.random.default_rng(1)
-
-    def bf(shape):
-        return (rng.standard_normal(shape).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
-
-    q, k, v, do = bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D))
+    q, k, v, do = (_bf16_np(rng, (T, 1, D)) for _ in range(4))
     threads = orc.set_threads(host_cores())
-    blk, tri = orc.layout(cu, B)
     scale = 1.0 / math.sqrt(D)
     times, flops = [], None
     budget_s, start, warm_done = args.ref_budget_s, time.perf_counter(), 0
@@ -235,11 +262,12 @@ def run_reference_arm(args, rank, world):
     value = flops / (ms * 1e-3) / 1e12
     sample = (f"q head 0 of 32, {'layer 0 (DST keep count)' if c3 else 'one layer'}, of rank 0's {T}-token "
               f"micro-batch ({len(cu) - 1} seqs): scorer, profile, selector, fwd, bwd")
-    workload_txt = c3_workload(world, args.layers, cost_table_source()) if c3 else C2_WORKLOAD
+    _, table_src = cost_table()
+    label = c3_label(world, args.layers, table_src) if c3 else C2_LABEL
     line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_txt, "sample": "CPU port: " + sample, "warmup_run": warm_done,
+            "config": {"workload": label, "sample": "CPU port: " + sample, "warmup_run": warm_done,
                        "steps_timed": len(times), "budget_s": budget_s},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -266,16 +294,124 @@ class Marker:
         return out
 
 
-def c3_global_batch(world: int, seed: int, layers: int = 1):
-    """C3: the reference workload generator's 40% 32K / 60% 2K bimodal mix
-    (distribution={bimodal, short_weight 0.6, ln 2048 / ln 32768, sigma 0}, default
-    concentration), gbs = 5 * dp -> (lengths, per-sample per-layer routing profiles)."""
-    from paper_2604_13847_b200.host import api
+def time_fn(torch, fn, steps, warmup=3):
+    """Mean device ms of fn() over `steps` back-to-back calls after `warmup` (CUDA events)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
 
-    dist_spec = dict(short_weight=0.6, short_log_mean=float(np.log(2048)), short_log_sigma=0.0,
-                     long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
-    lengths, profiles = api().generate_samples(5 * world, layers, CFG["block"], seed=seed, dist=dist_spec)
-    return np.asarray(lengths), profiles
+
+def sub_c2(torch, ops, dev, steps, burst):
+    """C2 (configs[1]): one 32K packed layer, scorer -> profile -> selector -> fwd -> bwd."""
+    H, D, B = CFG["heads"], CFG["head_dim"], CFG["block"]
+    cu, k_seq = c2_workload(0)
+    T = int(cu[-1])
+    lay = ops.VarlenLayout.build(cu, B, device=dev)
+    g = torch.Generator(device=dev).manual_seed(CFG["seed"])
+    q, k, v, do = (torch.randn((T, H, D), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
+    kseq_d = torch.from_numpy(k_seq).to(dev)
+    k_max = int(k_seq.max())
+    scale = 1.0 / math.sqrt(D)
+    S = ops.block_scores(q, k, lay, scale)
+    idx, cnt = ops.topk_select(S, lay, kseq_d, k_max)
+    o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+    f_fwd, f_bwd = useful_flops(cu, B, idx.cpu().numpy(), cnt.cpu().numpy(), D)
+
+    def full():
+        S_ = ops.block_scores(q, k, lay, scale)
+        ops.coverage_profile(S_, lay)
+        i_, c_ = ops.topk_select(S_, lay, kseq_d, k_max)
+        o_, l_ = ops.sparse_attn_fwd(q, k, v, lay, i_, c_, scale)
+        ops.sparse_attn_bwd(q, k, v, o_, do, l_, lay, i_, c_, scale)
+
+    t_step = time_fn(torch, full, steps)
+    t_fwd = time_fn(torch, lambda: ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale), steps)
+    t_bwd = time_fn(torch, lambda: ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale), steps)
+    return {"workload": C2_LABEL, "ms_per_step": t_step, "useful_tflop": (f_fwd + f_bwd) / 1e12,
+            "tflops": (f_fwd + f_bwd) / (t_step * 1e-3) / 1e12,
+            "fwd_ms": t_fwd, "fwd_tflops": f_fwd / (t_fwd * 1e-3) / 1e12,
+            "fwd_frac_burst": f_fwd / (t_fwd * 1e-3) / 1e12 / burst,
+            "bwd_ms": t_bwd, "bwd_tflops": f_bwd / (t_bwd * 1e-3) / 1e12,
+            "bwd_frac_burst": f_bwd / (t_bwd * 1e-3) / 1e12 / burst}
+
+
+def sub_c5(torch, ops, dev, steps, burst, keep=0.1):
+    """C5 (configs[4]): one 131072-token sequence, GQA 32q / 8kv with group-shared selection,
+    keep 0.1 (k = ceil(0.1 * 1024) = 103), fwd + bwd."""
+    T, Hq, Hkv, D, B = 131072, 32, 8, 128, 128
+    cu = np.array([0, T], np.int32)
+    lay = ops.VarlenLayout.build(cu, B, device=dev)
+    g = torch.Generator(device=dev).manual_seed(CFG["seed"] + 5)
+    q = torch.randn((T, Hq, D), generator=g, device=dev).to(torch.bfloat16)
+    k, v = (torch.randn((T, Hkv, D), generator=g, device=dev).to(torch.bfloat16) for _ in range(2))
+    do = torch.randn((T, Hq, D), generator=g, device=dev).to(torch.bfloat16)
+    nb = T // B
+    kk = max(1, math.ceil(keep * nb))
+    scale = 1.0 / math.sqrt(D)
+    S = ops.block_scores(q, k, lay, scale)
+    idx, cnt = ops.topk_select(S, lay, torch.tensor([kk], dtype=torch.int32, device=dev), kk, group=Hq // Hkv)
+    o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+    f_fwd, f_bwd = useful_flops(cu, B, idx.cpu().numpy(), cnt.cpu().numpy(), D, hq=Hq)
+    t_fwd = time_fn(torch, lambda: ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale), steps)
+    t_bwd = time_fn(torch, lambda: ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale), steps)
+    del q, k, v, do, o, lse, S
+    return {"workload": f"C5: one 131072-token sequence, GQA 32q/8kv (group-shared selection), d128, B128, keep "
+                        f"{keep} (k={kk}), fwd + bwd", "useful_tflop": (f_fwd + f_bwd) / 1e12,
+            "ms_per_step": t_fwd + t_bwd, "tflops": (f_fwd + f_bwd) / ((t_fwd + t_bwd) * 1e-3) / 1e12,
+            "fwd_ms": t_fwd, "fwd_tflops": f_fwd / (t_fwd * 1e-3) / 1e12,
+            "fwd_frac_burst": f_fwd / (t_fwd * 1e-3) / 1e12 / burst,
+            "bwd_ms": t_bwd, "bwd_tflops": f_bwd / (t_bwd * 1e-3) / 1e12,
+            "bwd_frac_burst": f_bwd / (t_bwd * 1e-3) / 1e12 / burst}
+
+
+def sub_c1(torch, ops, dev, steps, with_cpu=True):
+    """C1 (configs[0]): single 4096-token sequence, 8 heads MHA, d64, B64, keep 0.25 (k = 16):
+    forward latency (the attention kernel alone and scorer + selector + fwd), beside the CPU
+    oracle on the same bf16 input (all 8 heads, all host threads)."""
+    T, H, D, B, kk = 4096, 8, 64, 64, 16
+    cu = np.array([0, T], np.int32)
+    lay = ops.VarlenLayout.build(cu, B, device=dev)
+    rng = np.random.default_rng(CFG["seed"] + 1)
+    qn, kn, vn = (_bf16_np(rng, (T, H, D)) for _ in range(3))
+    to_t = lambda a: torch.from_numpy(a.view(np.int16)).to(dev).view(torch.bfloat16)  # noqa: E731
+    q, k, v = to_t(qn), to_t(kn), to_t(vn)
+    scale = 1.0 / math.sqrt(D)
+    kseq = torch.tensor([kk], dtype=torch.int32, device=dev)
+    S = ops.block_scores(q, k, lay, scale)
+    idx, cnt = ops.topk_select(S, lay, kseq, kk)
+    f_fwd, _ = useful_flops(cu, B, idx.cpu().numpy(), cnt.cpu().numpy(), D)
+    e, tiles = pair_entries(cu, B, idx.cpu().numpy(), cnt.cpu().numpy())
+
+    def full():
+        S_ = ops.block_scores(q, k, lay, scale)
+        i_, c_ = ops.topk_select(S_, lay, kseq, kk)
+        ops.sparse_attn_fwd(q, k, v, lay, i_, c_, scale)
+
+    t_fwd = time_fn(torch, lambda: ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale), max(steps, 20))
+    t_full = time_fn(torch, full, max(steps, 20))
+    out = {"workload": "C1: one 4096-token sequence, 8 heads MHA, d64, B64, keep 0.25 (k=16), forward",
+           "useful_gflop": f_fwd / 1e9, "fwd_attn_ms": t_fwd, "fwd_attn_tflops": f_fwd / (t_fwd * 1e-3) / 1e12,
+           "scorer_selector_fwd_ms": t_full,
+           "executed_over_useful": tiles * 64 * 64 / e}
+    if with_cpu:
+        from oracle import device as orc
+
+        threads = orc.set_threads(host_cores())
+        cu_np = cu
+        sel_i, sel_c = idx.cpu().numpy(), cnt.cpu().numpy()
+        t0 = time.perf_counter()
+        orc.sparse_attn_fwd(qn, kn, vn, cu_np, B, sel_i, sel_c, scale)
+        dt = time.perf_counter() - t0
+        out["cpu_oracle"] = {"fwd_attn_ms": dt * 1e3, "cores": threads, "kind": "port",
+                             "sample": "the full C1 forward (all 8 heads), same bf16 input and selection"}
+    return out
 
 
 def main():
@@ -288,11 +424,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=None, choices=["c2", "c3"],
-                    help="c2 (default at 1 GPU): 32K packed, per-sequence keeps; c3 (default at >1 GPU): 40/60 "
-                         "32K/2K global batch, SAB plan + per-layer DST across ranks")
+    ap.add_argument("--workload", default="c3", choices=["c2", "c3"],
+                    help="c3 (default, every N): 40/60 32K/2K global batch, SAB plan + closed-loop per-layer DST "
+                         "across ranks; c2: the one-layer 32K packed micro-batch")
     ap.add_argument("--layers", type=int, default=36, help="c3: layers per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the N=1 C1 / C2 / C5 sub-records")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="--impl reference: wall-clock budget for the CPU arm (>= 1 warm-up + 1 timed step)")
     ap.add_argument("--profile-only", action="store_true", help="2 plain steps then exit (for ncu)")
@@ -302,15 +439,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    workload_kind = args.workload or ("c2" if world == 1 else "c3")
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
 
     import torch
     import torch.distributed as dist
 
-    from paper_2604_13847_b200 import dp, ops
-    from paper_2604_13847_b200.host import api
+    from paper_2604_13847_b200 import dp, ops, synth
 
     torch.cuda.set_device(local_rank)
     if world > 1:
@@ -318,37 +454,25 @@ def main():
     dev = torch.device("cuda", local_rank)
     H, D, B = CFG["heads"], CFG["head_dim"], CFG["block"]
     stream = torch.cuda.current_stream()
+    burst, sustained, sustained_mhz, hbm_peak, peak_src = peaks()
 
-    if workload_kind == "c2":
-        cu, k_seq = workload(rank)
-        config = {"workload": C2_WORKLOAD, "seqs_rank0": int(len(cu) - 1)}
-    else:
-        lengths_all, profiles_all = c3_global_batch(world, CFG["seed"], args.layers)
-        # GPU-measured cost table (profiler.py, committed under profiles/) when present, as SURVEY
-        # 8(f) item 1 intends; the reference's synthetic table otherwise.
-        tpath = os.path.join(ROOT, "profiles", "b200_cost_table_h32_d128_b128.csv")
-        table = api().load_table(tpath)[0] if os.path.exists(tpath) else api().synthesize_table(block_size=B)
-        table_src = cost_table_source()
-        bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=table)
-        mine = [int(lengths_all[i]) for i in bins[rank][0]]
-        cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
-        k_seq = None
-        config = {"workload": c3_workload(world, args.layers, table_src),
-                  "tokens_per_rank": [int(x) for x in np.array([sum(int(lengths_all[i]) for i in b[0]) for b in bins])]}
-    T = int(cu[-1])
-    lay = ops.VarlenLayout.build(cu, B, device=dev)
-    g = torch.Generator(device=dev).manual_seed(CFG["seed"] + rank)
-    q, k, v, do = (torch.randn((T, H, D), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
-    scale = 1.0 / math.sqrt(D)
-
-    if workload_kind == "c2":
+    runner = None
+    if args.workload == "c2":
+        cu, k_seq = c2_workload(rank)
+        config = {"workload": C2_LABEL, "seqs_rank0": int(len(cu) - 1)}
+        T = int(cu[-1])
+        lay = ops.VarlenLayout.build(cu, B, device=dev)
+        g = torch.Generator(device=dev).manual_seed(CFG["seed"] + rank)
+        q, k, v, do = (torch.randn((T, H, D), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
+        scale = 1.0 / math.sqrt(D)
         kseq_d = torch.from_numpy(k_seq).to(dev)
         k_max = int(k_seq.max())
-        grid = torch.tensor([1, 2, 3, 4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 56, 64], dtype=torch.int32,
-                            device=dev)
+        grid = torch.tensor([1, 2, 3, 4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 56, 64], dtype=torch.int32, device=dev)
 
         def step(mark=None, bufs=None):
             q_, k_, v_, do_ = bufs if bufs is not None else (q, k, v, do)
+            if mark:
+                mark("start")
             S = ops.block_scores(q_, k_, lay, scale)
             prof = ops.coverage_profile(S, lay)
             ops.coverage_at_grid(prof, lay, grid)
@@ -362,26 +486,46 @@ def main():
             if mark:
                 mark("bwd")
             return [(idx, cnt, o, (dq, dk, dv))]
+
+        busy_of = None
     else:
-        rng = np.random.default_rng(CFG["seed"])
-        layer_scales = np.exp(rng.uniform(-0.5, 1.0, size=args.layers))  # per-layer softmax temperature
-        routing = [[profiles_all[i][l] for i in bins[rank][0]] for l in range(args.layers)]
-        runner = dp.DPStep(dp.RankBatch(np.diff(cu), list(bins[rank][0]), lay), q, k, v, do, layer_scales, table,
-                           dp.DstSettings(), rank=rank, world=world, width=int(np.ceil(32768 / B)),
-                           routing_profiles=routing)
+        lengths_all, routing_all = c3_global_batch(world, CFG["seed"], args.layers, sorted_=False)
+        table, table_src = cost_table()
+        bins = dp.assign_rank_batches(lengths_all, world, 5, "sab", table=table)
+        ids = list(bins[rank][0])
+        mine = [int(lengths_all[i]) for i in ids]
+        cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
+        T = int(cu[-1])
+        lay = ops.VarlenLayout.build(cu, B, device=dev)
+        q, k, v, do = synth.planted_qkv(mine, [routing_all[i][0] for i in ids], H, H, D, B, seed=CFG["seed"] + rank,
+                                        device=dev)
+        layer_scales = synth.layer_scales(args.layers, CFG["seed"])
+        runner = dp.DPStep(dp.RankBatch(np.asarray(mine), ids, lay), q, k, v, do, layer_scales, table,
+                           dp.DstSettings(), rank=rank, world=world)
+        config = {"workload": c3_label(world, args.layers, table_src),
+                  "tokens_per_rank": [int(sum(int(lengths_all[i]) for i in b[0])) for b in bins],
+                  "members_rank0": [int(lengths_all[i]) for i in bins[0][0]]}
 
         def step(mark=None, bufs=None):
             if bufs is not None:
                 runner.q, runner.k, runner.v, runner.do = bufs
+            if mark:
+                mark("start")
             return runner.run(backward=True, mark=mark)
+
+        def busy_of():
+            return sum(a.elapsed_time(b) for a, b in runner.last["busy"])
 
     outs = step()
     torch.cuda.synchronize()
-    f_fwd = f_bwd = 0.0
-    for idx, cnt, *_ in outs:
-        a, b_ = useful_flops(cu, B, idx.cpu().numpy(), cnt.cpu().numpy(), D)
-        f_fwd, f_bwd = f_fwd + a, f_bwd + b_
-    f_step = f_fwd + f_bwd
+
+    def step_flops(outs_):
+        ff = fb = 0.0
+        for idx, cnt, *_ in outs_:
+            a, b_ = useful_flops(cu, B, idx.cpu().numpy(), cnt.cpu().numpy(), D, hq=H)
+            ff, fb = ff + a, fb + b_
+        return ff, fb
+
     if args.profile_only:
         step()
         torch.cuda.synchronize()
@@ -391,19 +535,21 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---- device-timed region: inputs resident in HBM (each >= 256 MB, larger than L2)
+    # ---- device-timed region: inputs resident in HBM (Q/K/V/dO >= 256 MB each, larger than L2)
     markers = [Marker(torch, stream) for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ops.launch_count()
+    step_outs, busy_pairs = [], []
     with ClockSampler(local_rank) as clk:
         time.sleep(0.3)  # let nvidia-smi start sampling
         t0.record(stream)
         for s_ in range(args.steps):
-            markers[s_]("start")
-            step(markers[s_])
+            step_outs.append(step(markers[s_]))
+            if runner is not None:
+                busy_pairs.append(list(runner.last["busy"]))
         t1.record(stream)
         torch.cuda.synchronize()
         launches = ops.launch_count() - launches0
@@ -412,16 +558,30 @@ def main():
         while time.perf_counter() - t_load < 1.2:
             step()
             torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    # Useful work per timed step (each step's own selections: closed-loop DST decides per step).
+    fl = [step_flops(o_) for o_ in step_outs]
+    f_fwd = statistics.mean(a for a, _ in fl)
+    f_bwd = statistics.mean(b for _, b in fl)
+    f_step = f_fwd + f_bwd
+    if busy_pairs:
+        busy = [sum(a.elapsed_time(b) for a, b in bp) for bp in busy_pairs]
+    else:
+        busy = [m.marks[0][1].elapsed_time(m.marks[-1][1]) for m in markers]
+    phase = {}
+    for m in markers:
+        for k_, v_ in m.durations().items():
+            phase[k_] = phase.get(k_, 0.0) + v_ / args.steps
+    sel_ms, fwd_ms, bwd_ms = phase.get("decided", 0.0), phase.get("fwd", 0.0), phase.get("bwd", 0.0)
     if world > 1:
         dist.barrier()
-    ms = t0.elapsed_time(t1) / args.steps
 
-    # ---- N > 1 (C3): the same step with the step-end gradient all-reduce of SURVEY 8(e),
-    # one stand-in bucket per layer (the layer's output-projection gradient, H*D x H*D bf16),
+    # ---- N > 1 (C3): the same step with the step-end gradient all-reduce of SURVEY 8(e), one
+    # stand-in bucket per layer (the layer's output-projection gradient, H*D x H*D bf16),
     # all-reduced on NCCL's stream overlapping the following layers. Reported beside the main
     # number, which (like the metric's max/mean) is measured before this barrier.
     grad_ar = None
-    if world > 1 and workload_kind == "c3":
+    if world > 1 and runner is not None:
         hidden = H * D
         buckets = [torch.zeros((hidden, hidden), dtype=torch.bfloat16, device=dev) for _ in range(args.layers)]
         runner.run(backward=True, grad_buckets=buckets)  # warm the NCCL path
@@ -440,18 +600,13 @@ def main():
                    "bytes_per_step": int(args.layers * hidden * hidden * 2),
                    "ms_per_step_with_allreduce": float(ar_ms[0]),
                    "overlap": "per-layer async NCCL all_reduce issued after that layer's backward"}
-    phase = {}
-    for m in markers:
-        for k_, v_ in m.durations().items():
-            phase[k_] = phase.get(k_, 0.0) + v_ / args.steps
-    sel_ms, fwd_ms, bwd_ms = phase.get("decided", 0.0), phase.get("fwd", 0.0), phase.get("bwd", 0.0)
 
     # ---- end-to-end region: every step copies its inputs in from pinned host memory and reads its
     # results (O, dQ, dK, dV of the last layer) back, through the same public calls. Double
     # buffered on separate copy streams: step i's H2D overlaps step i-1's kernels and step i-2's
     # D2H, as a training loop's data pipeline would.
     hin = [tuple(t.cpu().pin_memory() for t in (q, k, v, do)) for _ in range(2)]
-    hout = [tuple(torch.empty((T, H, D), dtype=torch.bfloat16).pin_memory() for _ in range(4)) for _ in range(2)]
+    hout = [tuple(torch.empty(t.shape, dtype=torch.bfloat16).pin_memory() for t in (q, q, k, v)) for _ in range(2)]
     dbuf = [(q, k, v, do), tuple(torch.empty_like(t) for t in (q, k, v, do))]
     h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     e2e_steps = max(2, min(args.steps, 6))
@@ -481,6 +636,8 @@ def main():
                     dst.copy_(src, non_blocking=True)
             keep = (keep + [res])[-2:]
         stream.wait_stream(d2h)
+        if runner is not None:
+            runner.q, runner.k, runner.v, runner.do = q, k, v, do
 
     pipelined(e2e_steps)  # warm: the caching allocator sizes its pool for the in-flight steps
     torch.cuda.synchronize()
@@ -493,64 +650,82 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    nbytes = 4 * T * H * D * 2
+    nbytes_in = sum(t.numel() * 2 for t in (q, k, v, do))
+    nbytes_out = sum(t.numel() * 2 for t in (q, q, k, v))  # O, dQ, dK, dV
 
-    # ---- max over ranks, whole-job aggregates
-    vals = torch.tensor([ms, e2e_ms, f_step], dtype=torch.float64, device=dev)
+    # ---- max over ranks, whole-job aggregates; busy-time balance per step (Eq. 9)
+    vals = torch.tensor([ms, e2e_ms, f_step] + busy, dtype=torch.float64, device=dev)
     if world > 1:
-        mx = vals.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        tot = vals.clone()
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        ms_max, e2e_max, flops_all = float(mx[0]), float(mx[1]), float(tot[2])
-        per_rank = [torch.zeros(3, dtype=torch.float64, device=dev) for _ in range(world)]
+        per_rank = [torch.zeros_like(vals) for _ in range(world)]
         dist.all_gather(per_rank, vals)
-        per_rank_ms = [float(x[0]) for x in per_rank]
-        per_rank_tflop = [float(x[2]) / 1e12 for x in per_rank]
+        pr = torch.stack(per_rank).cpu().numpy()
     else:
-        ms_max, e2e_max, flops_all, per_rank_ms, per_rank_tflop = ms, e2e_ms, f_step, [ms], [f_step / 1e12]
+        pr = vals.cpu().numpy()[None]
+    ms_max, e2e_max, flops_all = float(pr[:, 0].max()), float(pr[:, 1].max()), float(pr[:, 2].sum())
+    busy_mat = pr[:, 3:]  # [rank, step]
+    step_ratio = busy_mat.max(axis=0) / busy_mat.mean(axis=0)
+    busy_rank = busy_mat.mean(axis=1)
 
     if rank == 0:
-        bf16_peak, hbm_peak, peak_kind = peaks()
+        b_tflops = f_bwd / (bwd_ms * 1e-3) / 1e12 if bwd_ms else 0.0
+        f_tflops = f_fwd / (fwd_ms * 1e-3) / 1e12 if fwd_ms else 0.0
         if bwd_ms >= fwd_ms:
-            dom, dom_ms, dom_flops = "sb_sparse_attn_bwd (dkv+dq passes)", bwd_ms, f_bwd
+            dom, dom_tf = "sb_sparse_attn_bwd (prep + transpose + dK/dV + dQ passes)", b_tflops
         else:
-            dom, dom_ms, dom_flops = "sb_sparse_attn_fwd", fwd_ms, f_fwd
-        achieved = dom_flops / (dom_ms * 1e-3) / 1e12
-        traffic = None
+            dom, dom_tf = "sb_sparse_attn_fwd", f_tflops
+        traffic, traffic_note = None, None
         prof_path = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
         if os.path.exists(prof_path):
             try:
-                traffic = json.load(open(prof_path)).get(workload_kind, {}).get("dominant_traffic_bytes")
+                rec = json.load(open(prof_path)).get(args.workload, {})
+                traffic, traffic_note = rec.get("dominant_traffic_bytes"), rec.get("note")
             except Exception:
                 traffic = None
+        clocks = clk.summary()
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(cu, k_seq if k_seq is not None else np.maximum(1, (np.diff(cu) + B - 1) // B // 8))
+            cpu = cpu_baseline(cu, np.maximum(1, (np.diff(cu) + B - 1) // B // 8))
+        subs = None
+        if world == 1 and not args.no_sub:
+            subs = {"c2": sub_c2(torch, ops, dev, 5, burst), "c5_gqa_keep0.1": sub_c5(torch, ops, dev, 3, burst),
+                    "c1": sub_c1(torch, ops, dev, 20, with_cpu=not args.no_cpu_baseline)}
         value = flops_all / (ms_max * 1e-3) / 1e12
-        config.update({"tokens_per_rank" if workload_kind == "c2" else "tokens_rank0": T,
-                       "l2": "inputs 256 MB+ each > L2, no flush", "parallelism": f"dp{world}"})
+        config.update({"tokens_rank0": T, "l2": "inputs 256 MB+ each > L2, no flush", "parallelism": f"dp{world}",
+                       "layers": args.layers if runner is not None else 1})
+        k_fin = runner.last.get("k_final") if runner is not None else None
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": config,
-            "breakdown_ms_rank0": {"scorer_profile_exchange_dst_selector": sel_ms, "fwd": fwd_ms, "bwd": bwd_ms},
-            "per_rank_ms": per_rank_ms, "per_rank_useful_tflop": per_rank_tflop,
-            "max_over_mean": ms_max / statistics.mean(per_rank_ms),
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (planted block routing)" if runner else "synthetic",
+            "config": config,
+            "breakdown_ms_rank0": {"scorer_profile_exchange_dst": sel_ms, "selector_fwd": fwd_ms, "bwd": bwd_ms},
+            "busy_ms_per_rank": [float(x) for x in busy_rank],
+            "max_over_mean": float(busy_rank.max() / busy_rank.mean()),
+            "max_over_mean_worst_step": float(step_ratio.max()),
+            "balance_note": "per-rank busy time = CUDA events around the rank's own kernels (scorer pre-pass, "
+                            "layer loop), excluding the all-gather wait and host DST",
+            "per_rank_ms_wall": [float(x) for x in pr[:, 0]],
+            "per_rank_useful_tflop": [float(x) / 1e12 for x in pr[:, 2]],
             "useful_tflop_per_step": flops_all / 1e12,
-            "fwd_tflops_rank0": f_fwd / (fwd_ms * 1e-3) / 1e12 if fwd_ms else None,
-            "bwd_tflops_rank0": f_bwd / (bwd_ms * 1e-3) / 1e12 if bwd_ms else None,
-            "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16_peak,
-                         "unit": "TFLOP/s", "frac": achieved / bf16_peak, "traffic": traffic,
-                         "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json)"},
+            "fwd_tflops_rank0": f_tflops, "bwd_tflops_rank0": b_tflops,
+            "k_final_rank0": [int(x) for x in k_fin[0]] if k_fin is not None else None,
+            "roofline": {"bound": "tensor", "kernel": dom, "achieved": dom_tf, "peak": burst, "unit": "TFLOP/s",
+                         "frac": dom_tf / burst, "traffic": traffic, "traffic_note": traffic_note,
+                         "peak_source": f"{peak_src} burst bf16 dense (MEASURED_PEAKS.json)",
+                         "peak_sustained": sustained, "frac_sustained": dom_tf / sustained,
+                         "sustained_measured_at_mhz": sustained_mhz,
+                         "bench_sm_mhz": (clocks or {}).get("sm_mhz"),
+                         "achieved_def": "useful selected-block FLOPs of the phase (10*d*sum e_ij bwd, 4*d*sum "
+                                         "e_ij fwd, per q head) / its CUDA-event time on the launching stream"},
             "e2e": {"value": flops_all / (e2e_max * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_max,
-                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                    "h2d_bytes_per_step": nbytes_in, "d2h_bytes_per_step": nbytes_out,
                     "note": "every step: pinned H2D of its Q,K,V,dO and D2H of its O,dQ,dK,dV (last layer), "
                             "double-buffered on two copy streams overlapping the neighbouring steps' kernels"},
             "gpu_launches": int(launches),
             "grad_allreduce": grad_ar,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "cpu_baseline": cpu,
+            "sub": subs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -559,16 +734,12 @@ def main():
 
 
 def cpu_baseline(cu, k_seq):
-    """Oracle port (fp64 C, all host threads) on a bounded sample: q head 0 of 32, fwd+bwd."""
+    """Oracle port (fp64 C, all host threads) on a bounded sample: q head 0 of 32, one layer fwd+bwd."""
     from oracle import device as orc
 
     T, D, B = int(cu[-1]), CFG["head_dim"], CFG["block"]
     rng = np.random.default_rng(1)
-
-    def bf(shape):
-        return (rng.standard_normal(shape).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
-
-    q, k, v, do = bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D)), bf((T, 1, D))
+    q, k, v, do = (_bf16_np(rng, (T, 1, D)) for _ in range(4))
     threads = orc.set_threads(host_cores())
     _, tri = orc.layout(cu, B)
     S = rng.standard_normal((1, int(tri[-1]))).astype(np.float32)
@@ -580,7 +751,7 @@ def cpu_baseline(cu, k_seq):
     dt = time.perf_counter() - t0
     f, b = useful_flops(cu, B, idx, cnt, D)
     return {"value": (f + b) / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-            "sample": f"q head 0 of 32 (1/32 of the step's attention work), fwd+bwd, {dt:.1f} s",
+            "sample": f"q head 0 of 32 of rank 0's micro-batch, one layer fwd+bwd at keep ~1/8, {dt:.1f} s",
             "seconds": dt}
 
 

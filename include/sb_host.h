@@ -65,6 +65,22 @@ int SBH(tune_global_batch)(const int64_t* bins, int nx, const int* grid, int nk,
 int SBH(make_micro_batch)(int ns, const int64_t* lengths, int nl, const double* profiles,
                           const int64_t* off, double* out, int64_t cap, int64_t* out_off,
                           int64_t* out_length_descriptor);
+#ifndef SB_REF
+/* Extension, not in the reference (dst.hpp CoverageTable): the {x, k_base, C(K) per layer}
+ * workload estimate DP ranks all-gather instead of their profiles.
+ * coverage_table: out[g] = coverage(profile, grid[g]) for g < n_grid, out[n_grid] =
+ * coverage(profile, k_base). tune_global_batch_cov: tune_global_batch for one layer with
+ * cov[n_mb][n_dst_grid + 1] laid out as coverage_table writes it (k_base of micro-batch i
+ * in k_base[i]); member lengths (mem_len, offsets mem_off[n_mb + 1]) are read only when
+ * varlen_block_size > 0. Outputs as tune_global_batch. Decisions are bit-identical to
+ * tune_global_batch on the profiles the tables were made from. */
+int SBH(coverage_table)(const double* scores, int m, const int* grid, int n_grid, int k_base, double* out);
+int SBH(tune_global_batch_cov)(const int64_t* bins, int nx, const int* grid, int nk, const double* lat,
+                               int n_mb, const int64_t* x, const int* k_base, const double* cov,
+                               const int64_t* mem_len, const int64_t* mem_off, int varlen_block_size, int layer,
+                               double threshold_p, int anchor, const int* dst_grid, int n_dst_grid, int* out_i,
+                               double* out_d);
+#endif
 int SBH(coverage_budget)(const double* scores, int m, double target, int* out);
 int SBH(intrinsic_budget)(int nl, const double* profiles, const int64_t* off, const int* grid,
                           int ng, double target, int* out);

@@ -228,6 +228,73 @@ SB_EXPORT int SBH(tune_global_batch)(const int64_t* bins, int nx, const int* gri
   });
 }
 
+#ifndef SB_REF
+// Extension (dst.hpp CoverageTable): the per-rank exchange payload and the tuner over it.
+SB_EXPORT int SBH(coverage_table)(const double* scores, int m, const int* grid, int n_grid, int k_base,
+                                  double* out) {
+  return guarded([&] {
+    if (n_grid < 1) throw sb::ConfigError("coverage_table: empty budget grid");
+    const auto prof = make_profile(scores, 0, m);
+    for (int g = 0; g < n_grid; ++g) out[g] = sb::coverage(prof, grid[g]);
+    out[n_grid] = sb::coverage(prof, k_base);
+  });
+}
+
+SB_EXPORT int SBH(tune_global_batch_cov)(const int64_t* bins, int nx, const int* grid, int nk, const double* lat,
+                                         int n_mb, const int64_t* x, const int* k_base, const double* cov,
+                                         const int64_t* mem_len, const int64_t* mem_off, int varlen_block_size,
+                                         int layer, double threshold_p, int anchor, const int* dst_grid,
+                                         int n_dst_grid, int* out_i, double* out_d) {
+  return guarded([&] {
+    const auto table = make_table(bins, nx, grid, nk, lat);
+    sb::DstConfig cfg;
+    cfg.threshold_p = threshold_p;
+    cfg.anchor = anchor_of(anchor);
+    cfg.budget_grid.assign(dst_grid, dst_grid + n_dst_grid);
+    cfg.varlen_block_size = varlen_block_size;
+    sb::validate_dst_config(cfg);
+    if (varlen_block_size > 0 && (mem_len == nullptr || mem_off == nullptr))
+      throw sb::ConfigError("tune_global_batch_cov: varlen cost needs member lengths");
+    sb::GlobalBatch gb;
+    std::vector<sb::CoverageTable> tabs;
+    for (int i = 0; i < n_mb; ++i) {
+      sb::MicroBatch mb;
+      mb.length_descriptor = x[i];
+      if (mem_len != nullptr && mem_off != nullptr)
+        for (int64_t e = mem_off[i]; e < mem_off[i + 1]; ++e) {
+          sb::Sample smp;
+          smp.id = e;
+          smp.length = mem_len[e];
+          mb.samples.push_back(std::move(smp));
+        }
+      gb.micro_batches.push_back(std::move(mb));
+      gb.base_budgets.push_back(k_base[i]);
+      sb::CoverageTable t;
+      const double* row = cov + static_cast<std::size_t>(i) * static_cast<std::size_t>(n_dst_grid + 1);
+      t.budgets.assign(dst_grid, dst_grid + n_dst_grid);
+      t.values.assign(row, row + n_dst_grid);
+      t.budgets.push_back(k_base[i]);
+      t.values.push_back(row[n_dst_grid]);
+      tabs.push_back(std::move(t));
+    }
+    const auto res = sb::tune_global_batch_cov(gb, tabs, layer, cfg, table);
+    for (std::size_t i = 0; i < res.decisions.size(); ++i) {
+      const auto& d = res.decisions[i];
+      int* oi = out_i + 5 * i;
+      oi[0] = d.micro_batch_id;
+      oi[1] = d.k_base;
+      oi[2] = d.k_anchor;
+      oi[3] = d.k_final;
+      oi[4] = direction_code(d.direction);
+      double* od = out_d + 3 * i;
+      od[0] = d.coverage_drop;
+      od[1] = d.predicted_ms_base;
+      od[2] = d.predicted_ms_final;
+    }
+  });
+}
+#endif
+
 SB_EXPORT int SBH(make_micro_batch)(int ns, const int64_t* lengths, int nl,
                                     const double* profiles, const int64_t* off, double* out,
                                     int64_t cap, int64_t* out_off,

@@ -1225,6 +1225,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   const int32_t* order_kv_lpt = sched::build_order(sched::CostFromLists{tr_off, hq / hsel, kMaxKvCost, nb_total, hkv},
                                                    kv_items, ws + w.order_kv, st, "sb_sparse_attn_bwd/order_kv");
   // Round matching (sched.cuh) runs its rounds in sequence on one CTA, ~5.3 us per round of 148
+  // (both cost constants below were calibrated on B200)
   // items on B200; it wins ~6 % of the dK/dV pass where items are long (C5: -4 to -10 % bwd) and
   // loses where they are short (C2: 295 us of matching for ~110 us won). Use it only when 6 % of
   // the dK/dV upper-bound estimate (hq * NB * k_max q tiles at ~2.3 us, causal half) exceeds it.
@@ -1232,7 +1233,8 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   const double match_us = 5.3 * ((kv_items + grid_kv - 1) / grid_kv);
   const double dkv_est_us = static_cast<double>(hq) * nb_total * k_max * 2.3 / 2.0 / grid_kv;
   const int32_t* order_kv = order_kv_lpt;
-  if (match_us < 0.06 * dkv_est_us) {
+  // match_rounds_kernel keeps per-CTA state in 256-entry shared arrays: grid_kv <= 256 (B200: 148).
+  if (grid_kv <= sched::kMatchMaxGrid && match_us < 0.06 * dkv_est_us) {
     int32_t* matched = reinterpret_cast<int32_t*>(ws + w.order_kv_matched);
     sched::match_rounds_kernel<<<1, sched::kMatchThreads, 0, st>>>(sched::ListCost{tr_off, hq / hsel}, order_kv_lpt,
                                                                    kv_items, grid_kv, matched);
@@ -1310,6 +1312,10 @@ SB_API int sb_sparse_attn_bwd(const uint16_t* q, const uint16_t* k, const uint16
     if (nseq == 0 || nb_total == 0 || total_tokens == 0) return;
     sbk::require(q && k && v && o && d_o && lse && cu_seqlens && blk_off && idx && cnt && dq && dk && dv && workspace,
                  "null pointer");
+    sbk::require((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+                  reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(d_o) | reinterpret_cast<uintptr_t>(dq) |
+                  reinterpret_cast<uintptr_t>(dk) | reinterpret_cast<uintptr_t>(dv)) % 16 == 0,
+                 "q/k/v/o/dO/dQ/dK/dV must be 16-byte aligned");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint8_t* ws = static_cast<uint8_t*>(workspace);
 #define SB_BWD_CASE(DD, BB)                                                                                     \

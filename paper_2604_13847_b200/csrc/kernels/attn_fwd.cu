@@ -444,7 +444,8 @@ SB_API int sb_sparse_attn_fwd(const uint16_t* q, const uint16_t* k, const uint16
     sbk::require(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128");
     sbk::require(block_size == 64 || block_size == 128, "block_size must be 64 or 128");
     sbk::require(hq >= 1 && hkv >= 1 && hq % hkv == 0, "hq must be a positive multiple of hkv");
-    sbk::require(hsel >= 1 && hq % hsel == 0, "hsel must divide hq");
+    sbk::require(hsel >= hkv && hq % hsel == 0 && hsel % hkv == 0,
+                 "hsel must divide hq and be a multiple of hkv (each selection row maps to one kv head)");
     sbk::require(k_max >= 1, "k_max must be >= 1");
     if (nseq == 0 || nb_total == 0 || total_tokens == 0) return;
     sbk::require(q && k && v && cu_seqlens && blk_off && idx && cnt && o && lse && workspace, "null pointer");

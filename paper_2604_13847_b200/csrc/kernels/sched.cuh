@@ -140,10 +140,13 @@ int32_t* build_order(Key key, int n_items, void* ws, cudaStream_t st, const char
 // 1024 threads: thread (target = t & 255, chunk = t >> 8) counts its quarter of the pairwise
 // compares and adds them into the target's rank, so a round costs ~40 compares and 4 barriers.
 constexpr int kMatchThreads = 1024;
+constexpr int kMatchMaxGrid = 256;  // shared arrays below are sized per CTA of the consuming grid
 template <typename Cost>
 __global__ void __launch_bounds__(kMatchThreads) match_rounds_kernel(Cost cost, const int32_t* __restrict__ order,
                                                                      int n_items, int grid, int32_t* __restrict__ out) {
-  __shared__ int load[256], item_cost[256], item_id[256], cta_at[256], rank_cta[256], rank_item[256];
+  __shared__ int load[kMatchMaxGrid], item_cost[kMatchMaxGrid], item_id[kMatchMaxGrid], cta_at[kMatchMaxGrid],
+      rank_cta[kMatchMaxGrid], rank_item[kMatchMaxGrid];
+  if (grid > kMatchMaxGrid) __trap();  // host gates on grid <= kMatchMaxGrid (B200 has 148 SMs)
   const int t = threadIdx.x, tgt = t & 255, chunk = t >> 8;
   const int per = (grid + 3) / 4, u0 = chunk * per, u1 = min(grid, u0 + per);
   if (t < 256) load[t] = 0;

@@ -61,7 +61,9 @@ __global__ void __launch_bounds__(256) topk_select_warp_kernel(
   const int n = i + 1;
   if (n > kWarpRow) return;  // long rows: topk_select_kernel
   const int64_t tri = tri_off[nseq];
-  const int k = max(1, min(k_seq[s], n));
+  // k_seq is clamped to the row length and to the idx row stride k_max (a caller passing
+  // k_seq > k_max gets k_max blocks, never writes past its row).
+  const int k = max(1, min(min(k_seq[s], n), k_max));
   int32_t* out = idx + (static_cast<size_t>(g) * nbt + gi) * k_max;
   if (lane == 0) cnt[static_cast<size_t>(g) * nbt + gi] = k;
   const int m = force_diag ? n - 1 : n;     // candidate count
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(
   const int i = gi - blk_off[s];
   const int n = i + 1;
   if (n <= kWarpRow) return;  // short rows: topk_select_warp_kernel
-  const int k = max(1, min(k_seq[s], n));
+  const int k = max(1, min(min(k_seq[s], n), k_max));  // clamped as in topk_select_warp_kernel
   int32_t* out = idx + (static_cast<size_t>(g) * nbt + gi) * k_max;
   if (threadIdx.x == 0) cnt[static_cast<size_t>(g) * nbt + gi] = k;
 

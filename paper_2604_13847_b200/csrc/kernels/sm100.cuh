@@ -12,6 +12,7 @@
 
 #include <cuda.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace sbk {
 namespace sm100 {
@@ -59,12 +60,29 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait_sleep(bar, parity)) {
-  }
+// Debug builds (-DSB_MBAR_TIMEOUT_ITERS=N, `make debug`): a wait still incomplete after N polls
+// (each try_wait blocks for up to its suspend window) prints the CTA, thread, barrier and parity
+// and traps, so a pipeline hang surfaces as a launch error naming the stuck barrier instead of a
+// silent hang. One 32-bit counter: the register-capped softmax warps still fit.
+#ifdef SB_MBAR_TIMEOUT_ITERS
+static __device__ __noinline__ void mbar_timeout(uint64_t* bar, uint32_t parity) {
+  printf("sb: mbarrier wait timeout: block %d thread %d barrier smem+0x%x parity %u\n", blockIdx.x, threadIdx.x,
+         smem_u32(bar), parity);
+  __trap();
 }
+#define SB_WAIT_LOOP(TRY)                                                             \
+  for (uint32_t n_ = 0; !TRY(bar, parity);)                                           \
+    if (++n_ > static_cast<uint32_t>(SB_MBAR_TIMEOUT_ITERS)) mbar_timeout(bar, parity);
+#else
+#define SB_WAIT_LOOP(TRY) \
+  while (!TRY(bar, parity)) { \
+  }
+#endif
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { SB_WAIT_LOOP(mbar_try_wait_sleep) }
 // try_wait without a suspend-time hint (the hardware's default suspend window): for the
 // latency-critical softmax waits on a freshly committed S tile.
+// (No debug timeout here: the forward's softmax warps that use it sit at their 224-register cap.
+// Every pipeline they wait on is also waited on by a producer / issuer through mbar_wait.)
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }

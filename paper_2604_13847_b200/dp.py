@@ -70,44 +70,100 @@ def profiles_to_host(prof: torch.Tensor, lay: ops.VarlenLayout) -> List[np.ndarr
     return [p[s, :nb].copy() for s, nb in enumerate(lay.nb_per_seq)]
 
 
-def pack_estimate(lengths: np.ndarray, layer_profiles: List[List[np.ndarray]], width: int) -> torch.Tensor:
-    """Flatten one rank's workload estimate into a fixed-size fp64 vector for the all-gather:
-    [nseq, lengths..., then for every layer and member the nb entries zero-padded to width]."""
+@dataclass
+class RankEstimate:
+    """One micro-batch's workload estimate, everything the pooled DST reads:
+    the length descriptor x, the base budget and, per layer, the merged profile's coverage at the
+    budget grid plus at k_base (host CoverageTable). Member lengths ride along for the opt-in
+    varlen cost model only."""
+
+    x: int
+    k_base: int
+    cov: np.ndarray                 # [num_layers, len(grid) + 1] fp64
+    members: np.ndarray | None = None
+
+
+def rank_estimate(lengths, layer_profiles: List[List[np.ndarray]], cfg: DstSettings) -> RankEstimate:
+    """Local half of the exchange: merge this rank's member profiles exactly as the reference's
+    make_micro_batch (workload.cpp:64-99), take the coverage-mode base budget over all layers
+    (intrinsic_budget, workload.cpp:389-411; sim.cpp:321-326) and tabulate C(k) per layer.
+    layer_profiles[l][s] = member s's profile at layer l."""
+    h = api()
+    grid = np.asarray(cfg.budget_grid, np.int32)
     L = len(layer_profiles)
-    nseq = len(lengths)
-    out = np.zeros(1 + nseq + L * nseq * width, np.float64)
-    out[0] = nseq
-    out[1:1 + nseq] = lengths
-    pos = 1 + nseq
-    for l in range(L):
-        for s in range(nseq):
-            v = layer_profiles[l][s]
-            out[pos:pos + len(v)] = v
-            pos += width
+    per_member = [[layer_profiles[l][s] for l in range(L)] for s in range(len(lengths))]
+    x, merged = h.make_micro_batch(np.asarray(lengths, np.int64), per_member)
+    k_base = h.intrinsic_budget(merged, grid, cfg.coverage_target) if cfg.base_mode == "coverage" else cfg.base_budget
+    cov = np.stack([h.coverage_table(merged[l], grid, k_base) for l in range(L)]) if L else np.zeros((0, len(grid) + 1))
+    return RankEstimate(int(x), int(k_base), cov, np.asarray(lengths, np.int64))
+
+
+def pack_estimate(est: RankEstimate, num_layers: int, n_grid: int, max_members: int = 0) -> torch.Tensor:
+    """Fixed-size fp64 vector [x, k_base, n_members, members (padded to max_members), cov]. Every
+    field is an integer < 2^53 or a double, so the round trip is exact. The size depends only on
+    (num_layers, n_grid, max_members), which every rank knows: one all-gather, no size exchange."""
+    if est.cov.shape != (num_layers, n_grid + 1):
+        raise ValueError(f"coverage table shape {est.cov.shape} != {(num_layers, n_grid + 1)}")
+    mem = est.members if (max_members and est.members is not None) else np.zeros(0, np.int64)
+    if len(mem) > max_members:
+        raise ValueError(f"{len(mem)} members exceed max_members={max_members}")
+    out = np.zeros(3 + max_members + num_layers * (n_grid + 1), np.float64)
+    out[0], out[1], out[2] = est.x, est.k_base, len(mem)
+    out[3:3 + len(mem)] = mem
+    out[3 + max_members:] = est.cov.reshape(-1)
     return torch.from_numpy(out)
 
 
-def unpack_estimate(vec: np.ndarray, num_layers: int, width: int, block: int):
-    nseq = int(vec[0])
-    lengths = vec[1:1 + nseq].astype(np.int64)
-    pos = 1 + nseq
-    prof = []  # [seq][layer]
-    nbs = (lengths + block - 1) // block
-    per_layer = []
+def unpack_estimate(vec: np.ndarray, num_layers: int, n_grid: int, max_members: int = 0) -> RankEstimate:
+    n = int(vec[2])
+    members = vec[3:3 + n].astype(np.int64) if max_members else None
+    cov = vec[3 + max_members:3 + max_members + num_layers * (n_grid + 1)].reshape(num_layers, n_grid + 1).copy()
+    return RankEstimate(int(vec[0]), int(vec[1]), cov, members)
+
+
+def exchange_estimates(est: RankEstimate, num_layers: int, n_grid: int, world: int, group=None, device="cpu",
+                       max_members: int = 0) -> List[RankEstimate]:
+    """All-gather every rank's estimate -> the pooled list, rank-major (the reference's pooled
+    order, sim.cpp:357-369). 8 * (3 + max_members + L * (|K| + 1)) bytes per rank: 4.9 KB for 36
+    layers on the default 16-point grid, 74 KB on the dense 1..256 grid. NCCL on GPU tensors,
+    gloo on CPU."""
+    mine = pack_estimate(est, num_layers, n_grid, max_members)
+    if world == 1:
+        return [unpack_estimate(mine.numpy(), num_layers, n_grid, max_members)]
+    import torch.distributed as dist
+
+    buf = mine.to(device)
+    outs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf, group=group)
+    flat = torch.stack(outs).cpu().numpy()  # one D2H for all ranks
+    return [unpack_estimate(flat[r], num_layers, n_grid, max_members) for r in range(world)]
+
+
+def decide_budgets_cov(pooled: List[RankEstimate], table: ProfileTable, cfg: DstSettings, num_layers: int,
+                       varlen_block_size: int = 0):
+    """Pooled host DST from the exchanged estimates: k_final[rank][layer] and the decisions,
+    bit-identical to decide_budgets on the underlying profiles (tune_global_batch_cov)."""
+    h = api()
+    grid = np.asarray(cfg.budget_grid, np.int32)
+    xs = [e.x for e in pooled]
+    k_base = [e.k_base for e in pooled]
+    mem = [e.members for e in pooled] if varlen_block_size else None
+    k_final = np.zeros((len(pooled), num_layers), np.int32)
+    decisions = []
     for l in range(num_layers):
-        row = []
-        for s in range(nseq):
-            row.append(vec[pos:pos + nbs[s]].copy())
-            pos += width
-        per_layer.append(row)
-    for s in range(nseq):
-        prof.append([per_layer[l][s] for l in range(num_layers)])
-    return lengths, prof
+        ds = h.tune_global_batch_cov(table, xs, k_base, [e.cov[l] for e in pooled], layer=l,
+                                     threshold_p=cfg.threshold_p, anchor=cfg.anchor, budget_grid=grid,
+                                     member_lengths=mem, varlen_block_size=varlen_block_size)
+        for d in ds:
+            k_final[d.micro_batch_id, l] = d.k_final
+        decisions.extend(ds)
+    return k_final, decisions, np.asarray(k_base), np.asarray(xs)
 
 
 def decide_budgets(pooled, table: ProfileTable, cfg: DstSettings, num_layers: int):
-    """Host DST over the pooled micro-batches (rank-major): returns k_final[rank][layer] and the
-    decisions. pooled = list over ranks of (lengths, per-member per-layer profiles)."""
+    """Host DST over pooled micro-batch PROFILES (rank-major): the replay / parity form of
+    decide_budgets_cov (same decisions). pooled = list over ranks of (lengths, per-member
+    per-layer profiles)."""
     h = api()
     grid = np.asarray(cfg.budget_grid, np.int32)
     xs, merged, k_base = [], [], []
@@ -151,23 +207,22 @@ class DPStep:
 
     Layers share the synthetic Q/K/V/dO tensors but each layer uses its own softmax
     temperature (scale_l / sqrt(d)), so per-layer routing profiles -- and the tuner's per-layer
-    budgets -- differ as they do across real layers."""
+    budgets -- differ as they do across real layers. The tuner is closed-loop: its profiles
+    are this step's K4 coverage profiles of the GPU block scores (planted_qk() gives synthetic
+    Q/K whose block scores carry the reference generator's routing structure)."""
 
     def __init__(self, batch: RankBatch, q, k, v, do, layer_scales, table: ProfileTable, cfg: DstSettings,
-                 rank: int = 0, world: int = 1, group=None, width: int | None = None, routing_profiles=None,
-                 pooled_xs=None):
-        """routing_profiles (optional): per-layer, per-member RoutingProfiles to feed the tuner
-        instead of the GPU coverage profiles -- e.g. the reference workload generator's own
-        routing scores for these samples (workload.cpp:239-271), which carry the reference's
-        sparsity structure; synthetic N(0,1) activations give near-uniform block scores."""
+                 rank: int = 0, world: int = 1, group=None, pooled_xs=None, max_members: int = 0,
+                 varlen_block_size: int = 0):
         self.batch, self.q, self.k, self.v, self.do = batch, q, k, v, do
         self.layer_scales = list(layer_scales)
         self.table, self.cfg = table, cfg
         self.rank, self.world, self.group = rank, world, group
         self.d = q.shape[2]
+        self.sel_group = q.shape[1] // k.shape[1]  # GQA: group-shared selection (SURVEY App. B 4)
         self.block = batch.layout.block_size
-        self.width = width if width is not None else int(batch.layout.nb_max)
-        self.routing_profiles = routing_profiles
+        self.max_members = max(max_members, len(batch.lengths)) if varlen_block_size else 0
+        self.varlen_block_size = varlen_block_size
         self.last = {}
         # On-device DST (fixed-base mode, SURVEY.md 8(f) item 3): with every rank's micro-batch
         # summed length known (the SAB plan is deterministic on every rank), the host half
@@ -188,29 +243,35 @@ class DPStep:
                 grid=torch.tensor(list(cfg.budget_grid), dtype=torch.int32, device=dev))
 
     def scorer_pass(self):
-        """K1 + K2 + K4 for every layer (the scorer pre-pass coverage-mode budgets need)."""
+        """K1 + K2 + K4 for every layer (the scorer pre-pass coverage-mode budgets need) ->
+        (block scores per layer, device profiles [L, nseq, nb_max] fp64)."""
         lay = self.batch.layout
         qbar, kbar = ops.block_pool(self.q, lay), ops.block_pool(self.k, lay)
-        profs, scores = [], []
-        for s_l in self.layer_scales:
+        scores = []
+        profs = torch.empty((len(self.layer_scales), lay.nseq, max(1, lay.nb_max)), dtype=torch.float64,
+                            device=self.q.device)
+        for l, s_l in enumerate(self.layer_scales):
             S = ops.block_scores(self.q, self.k, lay, s_l / math.sqrt(self.d), qbar=qbar, kbar=kbar)
             scores.append(S)
-            if self.routing_profiles is None:
-                profs.append(ops.coverage_profile(S, lay))
-        return qbar, kbar, profs, scores
+            profs[l] = ops.coverage_profile(S, lay)
+        return scores, profs
 
-    def exchange(self, profs):
+    def local_estimate(self, profs: torch.Tensor) -> RankEstimate:
+        """One D2H of all layers' profiles, then the local merge + coverage tables."""
         lay = self.batch.layout
-        if self.routing_profiles is not None:
-            layer_profiles = self.routing_profiles
-        else:
-            layer_profiles = [profiles_to_host(p, lay) for p in profs]
-        return exchange_estimates(self.batch.lengths, layer_profiles, self.width, self.block, self.world, self.group,
-                                  self.q.device)
+        host = profs.cpu().numpy()
+        nb = lay.nb_per_seq
+        layer_profiles = [[host[l, s, :nb[s]].copy() for s in range(lay.nseq)] for l in range(host.shape[0])]
+        self.last_profiles = layer_profiles
+        return rank_estimate(self.batch.lengths, layer_profiles, self.cfg)
 
     def run(self, backward: bool = True, mark=None, grad_buckets=None):
         """mark(tag) (optional) is called at phase boundaries: 'decided' after the scorer
         pre-pass + exchange + DST, then 'fwd' / 'bwd' after each layer's kernels.
+
+        self.last['busy'] = (start, end) CUDA-event pairs bracketing this rank's own kernels
+        (scorer pre-pass; layer loop), excluding the all-gather wait and the host DST: the
+        per-rank busy time the imbalance metric uses (reference Eq. 9 over per-rank totals).
 
         grad_buckets (optional, one tensor per layer): the step-end gradient all-reduce of
         SURVEY.md section 8(e). The attention op has no parameters, so the caller passes a stand-in
@@ -221,10 +282,16 @@ class DPStep:
         lay = self.batch.layout
         if self.on_device:
             return self._run_on_device(backward, mark, grad_buckets)
-        qbar, kbar, profs, scores = self.scorer_pass()
-        pooled = self.exchange(profs)
-        k_final, decisions, k_base, xs = decide_budgets(pooled, self.table, self.cfg, len(self.layer_scales))
-        self.last = dict(k_final=k_final, decisions=decisions, k_base=k_base, xs=xs)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        scores, profs = self.scorer_pass()
+        ev[1].record()
+        est = self.local_estimate(profs)
+        L = len(self.layer_scales)
+        pooled = exchange_estimates(est, L, len(self.cfg.budget_grid), self.world, self.group, self.q.device,
+                                    self.max_members)
+        k_final, decisions, k_base, xs = decide_budgets_cov(pooled, self.table, self.cfg, L, self.varlen_block_size)
+        self.last = dict(k_final=k_final, decisions=decisions, k_base=k_base, xs=xs, estimate=est, pooled=pooled)
         if mark:
             mark("decided")
         nb = lay.nb_per_seq
@@ -233,11 +300,12 @@ class DPStep:
         k_all = np.minimum(k_final[self.rank][:, None], nb[None, :]).astype(np.int32)
         self._k_host = torch.from_numpy(k_all).pin_memory()
         k_dev = self._k_host.to(self.q.device, non_blocking=True)
+        ev[2].record()
         outs, works = [], []
         for l, s_l in enumerate(self.layer_scales):
             k_max = int(max(1, k_all[l].max()))
             scale = s_l / math.sqrt(self.d)
-            idx, cnt = ops.topk_select(scores[l], lay, k_dev[l], k_max)
+            idx, cnt = ops.topk_select(scores[l], lay, k_dev[l], k_max, group=self.sel_group)
             o, lse = ops.sparse_attn_fwd(self.q, self.k, self.v, lay, idx, cnt, scale)
             if mark:
                 mark("fwd")
@@ -252,6 +320,8 @@ class DPStep:
             # hold ~1.3 GB x 36 of activations); every layer keeps its selection.
             last = l == len(self.layer_scales) - 1
             outs.append((idx, cnt, o if last else None, grads if last else None))
+        ev[3].record()
+        self.last["busy"] = [(ev[0], ev[1]), (ev[2], ev[3])]
         for w_ in works:
             w_.wait()  # the compute stream waits for every bucket
         return outs
@@ -259,6 +329,8 @@ class DPStep:
     def _run_on_device(self, backward, mark, grad_buckets):
         """The step with K8 deciding each layer's keep count on the device (fixed-base mode)."""
         lay = self.batch.layout
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
         qbar, kbar = ops.block_pool(self.q, lay), ops.block_pool(self.k, lay)
         if mark:
             mark("decided")
@@ -272,7 +344,7 @@ class DPStep:
             k_final, _, k_seq = ops.dst_decide(prof, lay, dp_["mb_off"], dp_["k_base"], dp_["k_anchor"],
                                                dp_["bottleneck"], dp_["grid"], self.cfg.threshold_p)
             k_finals.append(k_final)
-            idx, cnt = ops.topk_select(S, lay, k_seq, k_max)
+            idx, cnt = ops.topk_select(S, lay, k_seq, k_max, group=self.sel_group)
             o, lse = ops.sparse_attn_fwd(self.q, self.k, self.v, lay, idx, cnt, scale)
             if mark:
                 mark("fwd")
@@ -287,27 +359,10 @@ class DPStep:
             # hold ~1.3 GB x 36 of activations); every layer keeps its selection.
             last = l == len(self.layer_scales) - 1
             outs.append((idx, cnt, o if last else None, grads if last else None))
+        ev[1].record()
         for w_ in works:
             w_.wait()
-        self.last = dict(k_final_device=k_finals)
+        self.last = dict(k_final_device=k_finals, busy=[(ev[0], ev[1])])
         return outs
 
 
-def exchange_estimates(lengths, layer_profiles, width: int, block: int, world: int, group=None, device="cpu"):
-    """All-gather every rank's workload estimate (micro-batch member lengths + per-layer member
-    profiles, a few KB) -> the pooled list, rank-major. NCCL on GPU tensors; gloo on CPU."""
-    import torch.distributed as dist
-
-    num_layers = len(layer_profiles)
-    mine = pack_estimate(np.asarray(lengths), layer_profiles, width)
-    if world == 1:
-        return [unpack_estimate(mine.numpy(), num_layers, width, block)]
-    size = torch.tensor([mine.numel()], dtype=torch.int64, device=device)
-    sizes = [torch.zeros_like(size) for _ in range(world)]
-    dist.all_gather(sizes, size, group=group)
-    n = int(max(int(x) for x in sizes))
-    buf = torch.zeros(n, dtype=torch.float64, device=device)
-    buf[:mine.numel()] = mine.to(device)
-    outs = [torch.zeros_like(buf) for _ in range(world)]
-    dist.all_gather(outs, buf, group=group)
-    return [unpack_estimate(o.cpu().numpy(), num_layers, width, block) for o in outs]

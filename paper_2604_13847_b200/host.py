@@ -193,6 +193,42 @@ class HostAPI:
                                 float(d[0]), float(d[1]), float(d[2])))
         return out
 
+    def coverage_table(self, scores, budget_grid, k_base: int) -> np.ndarray:
+        """Extension (dst.hpp CoverageTable): [coverage(scores, g) for g in grid] + [coverage(scores, k_base)]."""
+        s = _a(scores, np.float64)
+        grid = _a(budget_grid, np.int32)
+        out = np.zeros(len(grid) + 1, np.float64)
+        self._call("coverage_table", _p(s if s.size else np.zeros(1)), len(s), _p(grid), len(grid), int(k_base),
+                   _p(out))
+        return out
+
+    def tune_global_batch_cov(self, table: ProfileTable, x: Sequence[int], k_base: Sequence[int], cov,
+                              layer: int = 0, threshold_p: float = 0.1, anchor: str = "min", budget_grid=None,
+                              member_lengths: Sequence[Sequence[int]] | None = None,
+                              varlen_block_size: int = 0) -> List[Decision]:
+        """tune_global_batch over coverage tables cov[n_mb][len(grid) + 1] (coverage_table rows)
+        instead of profiles; bit-identical decisions."""
+        n = len(x)
+        xs, kb = _a(x, np.int64), _a(k_base, np.int32)
+        grid = _a(table.budget_grid if budget_grid is None else budget_grid, np.int32)
+        cv = _a(np.asarray(cov, np.float64).reshape(n, len(grid) + 1), np.float64)
+        ml = mo = None
+        if member_lengths is not None:
+            mo = _a(np.concatenate([[0], np.cumsum([len(m) for m in member_lengths])]), np.int64)
+            flat = [int(v) for m in member_lengths for v in m]
+            ml = _a(flat if flat else [0], np.int64)
+        oi = np.zeros(5 * n, np.int32)
+        od = np.zeros(3 * n, np.float64)
+        self._call("tune_global_batch_cov", *table.args(), n, _p(xs), _p(kb), _p(cv), None if ml is None else _p(ml),
+                   None if mo is None else _p(mo), int(varlen_block_size), layer, C.c_double(threshold_p),
+                   ANCHORS[anchor], _p(grid), len(grid), _p(oi), _p(od))
+        out = []
+        for i in range(n):
+            a, d = oi[5 * i:5 * i + 5], od[3 * i:3 * i + 3]
+            out.append(Decision(int(a[0]), layer, int(a[1]), int(a[2]), int(a[3]), DIRECTIONS[a[4]],
+                                float(d[0]), float(d[1]), float(d[2])))
+        return out
+
     # ---- workload.hpp ------------------------------------------------------------------
     def make_micro_batch(self, lengths: Sequence[int], profiles: Sequence[Sequence[np.ndarray]]):
         """profiles[s][l] -> (length_descriptor, merged[l])."""

@@ -68,9 +68,48 @@ def _stream():
 
 
 def _need_cuda(*ts):
+    dev = None
     for t in ts:
-        if t is not None and not t.is_cuda:
+        if t is None:
+            continue
+        if not t.is_cuda:
             raise RuntimeError("sparsebalance-b200 ops run on CUDA tensors only (no CPU fallback)")
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise ValueError(f"all tensors must be on one device ({dev} vs {t.device})")
+    if dev is not None and dev.index is not None and dev.index != torch.cuda.current_device():
+        # kernels launch on the current device's current stream
+        raise ValueError(f"tensors are on {dev} but the current CUDA device is {torch.cuda.current_device()} "
+                         "(use torch.cuda.device(...))")
+
+
+def _need(t, name: str, dtype, ndim: int | None = None, shape=None):
+    """The kernels read raw data_ptr()s as dense row-major arrays of `dtype`: reject anything
+    else (a strided view or an fp16/fp32 tensor would otherwise be misread silently)."""
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (got strides {tuple(t.stride())})")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must have {ndim} dims, got shape {tuple(t.shape)}")
+    if shape is not None:
+        for a, (got, want) in enumerate(zip(t.shape, shape)):
+            if want is not None and got != want:
+                raise ValueError(f"{name} dim {a} must be {want}, got shape {tuple(t.shape)}")
+
+
+def _need_qkv(q, k, v, lay: "VarlenLayout"):
+    _need(q, "q", torch.bfloat16, 3, (lay.total_tokens, None, None))
+    T, _, D = q.shape
+    _need(k, "k", torch.bfloat16, 3, (T, None, D))
+    if v is not None:
+        _need(v, "v", torch.bfloat16, 3, tuple(k.shape))
+
+
+def _need_sel(idx, cnt, lay: "VarlenLayout"):
+    _need(idx, "idx", torch.int32, 3, (None, lay.nb_total, None))
+    _need(cnt, "cnt", torch.int32, 2, (idx.shape[0], lay.nb_total))
 
 
 def launch_count() -> int:
@@ -127,6 +166,7 @@ class VarlenLayout:
 def block_pool(x: torch.Tensor, lay: VarlenLayout) -> torch.Tensor:
     """K1: Xbar [NB, H, D] fp32 = mean of the valid rows of each block."""
     _need_cuda(x)
+    _need(x, "x", torch.bfloat16, 3, (lay.total_tokens, None, None))
     T, H, D = x.shape
     out = torch.empty((lay.nb_total, H, D), dtype=torch.float32, device=x.device)
     _call("sb_block_pool", _ptr(x), _ptr(lay.cu_seqlens), _ptr(lay.blk_off), lay.nseq, lay.nb_total, H, D,
@@ -137,12 +177,15 @@ def block_pool(x: torch.Tensor, lay: VarlenLayout) -> torch.Tensor:
 def block_scores(q: torch.Tensor, k: torch.Tensor, lay: VarlenLayout, scale: float | None = None,
                  qbar: torch.Tensor | None = None, kbar: torch.Tensor | None = None) -> torch.Tensor:
     """K1+K2: S [Hq, TRI] fp32, S[h][row(s,i)][j] = scale * <Qbar_i, Kbar_j>, j <= i."""
-    _need_cuda(q, k)
+    _need_cuda(q, k, qbar, kbar)
+    _need_qkv(q, k, None, lay)
     Hq, D = q.shape[1], q.shape[2]
     Hkv = k.shape[1]
     scale = 1.0 / math.sqrt(D) if scale is None else scale
     qbar = block_pool(q, lay) if qbar is None else qbar
     kbar = block_pool(k, lay) if kbar is None else kbar
+    _need(qbar, "qbar", torch.float32, 3, (lay.nb_total, Hq, D))
+    _need(kbar, "kbar", torch.float32, 3, (lay.nb_total, Hkv, D))
     S = torch.empty((Hq, max(1, lay.tri_total)), dtype=torch.float32, device=q.device)
     _call("sb_block_scores", _ptr(qbar), _ptr(kbar), _ptr(lay.blk_off), _ptr(lay.tri_off), lay.nseq, lay.nb_max, Hq,
           Hkv, D, C.c_float(scale), _ptr(S), _stream())
@@ -153,9 +196,12 @@ def topk_select(scores: torch.Tensor, lay: VarlenLayout, k_seq: torch.Tensor, k_
                 force_diag: bool = True):
     """K3: (idx [Hsel, NB, k_max] int32 ascending, -1 padded; cnt [Hsel, NB] int32)."""
     _need_cuda(scores, k_seq)
+    _need(scores, "scores", torch.float32, 2, (None, max(1, lay.tri_total)))
     Hs = scores.shape[0]
     hsel = Hs // group
     k_seq = k_seq.to(torch.int32).contiguous()
+    if k_seq.numel() != lay.nseq:
+        raise ValueError(f"k_seq must have one entry per sequence ({lay.nseq}), got {k_seq.numel()}")
     idx = torch.empty((hsel, lay.nb_total, k_max), dtype=torch.int32, device=scores.device)
     cnt = torch.empty((hsel, lay.nb_total), dtype=torch.int32, device=scores.device)
     _call("sb_topk_select", _ptr(scores), _ptr(lay.blk_off), _ptr(lay.tri_off), lay.nseq, lay.nb_total, lay.nb_max,
@@ -166,6 +212,7 @@ def topk_select(scores: torch.Tensor, lay: VarlenLayout, k_seq: torch.Tensor, k_
 def coverage_profile(scores: torch.Tensor, lay: VarlenLayout) -> torch.Tensor:
     """K4a: per-sequence routing profile [nseq, nb_max] fp64 (zero padded)."""
     _need_cuda(scores)
+    _need(scores, "scores", torch.float32, 2, (None, max(1, lay.tri_total)))
     Hs = scores.shape[0]
     ws = torch.empty(max(1, int(_lib().sb_coverage_profile_workspace_size(lay.tri_total, Hs, lay.nseq, lay.nb_max))),
                      dtype=torch.uint8, device=scores.device)
@@ -178,6 +225,7 @@ def coverage_profile(scores: torch.Tensor, lay: VarlenLayout) -> torch.Tensor:
 def coverage_at_grid(profile: torch.Tensor, lay: VarlenLayout, grid) -> torch.Tensor:
     """K4b: C[s][g] = coverage(profile_s, grid[g]) (reference dst.cpp:53-61 arithmetic)."""
     _need_cuda(profile)
+    _need(profile, "profile", torch.float64, 2, (lay.nseq, None))
     if isinstance(grid, torch.Tensor) and grid.is_cuda and grid.dtype == torch.int32:
         g = grid
     else:
@@ -194,6 +242,10 @@ def dst_decide(profile: torch.Tensor, lay: VarlenLayout, mb_off: torch.Tensor, k
     k_seq [nseq] int32 = min(k_final, nb_s)). All inputs device tensors; mb_off int32 [n_mb+1]
     partitions the layout's sequences into micro-batches."""
     _need_cuda(profile, mb_off, k_base, k_anchor, bottleneck, grid)
+    _need(profile, "profile", torch.float64, 2, (lay.nseq, None))
+    for t_, n_ in ((mb_off, "mb_off"), (k_base, "k_base"), (k_anchor, "k_anchor"), (bottleneck, "bottleneck"),
+                   (grid, "grid")):
+        _need(t_, n_, torch.int32, 1)
     n_mb = mb_off.numel() - 1
     k_final = torch.empty(n_mb, dtype=torch.int32, device=profile.device)
     drop = torch.empty(n_mb, dtype=torch.float64, device=profile.device)
@@ -207,6 +259,8 @@ def dst_decide(profile: torch.Tensor, lay: VarlenLayout, mb_off: torch.Tensor, k
 def sparse_attn_fwd(q, k, v, lay: VarlenLayout, idx, cnt, scale: float | None = None):
     """K5: (O [T, Hq, D] bf16, LSE [Hq, T] fp32 natural log)."""
     _need_cuda(q, k, v, idx, cnt)
+    _need_qkv(q, k, v, lay)
+    _need_sel(idx, cnt, lay)
     T, Hq, D = q.shape
     Hkv = k.shape[1]
     hsel, _, k_max = idx.shape
@@ -224,6 +278,12 @@ def sparse_attn_fwd(q, k, v, lay: VarlenLayout, idx, cnt, scale: float | None = 
 def sparse_attn_bwd(q, k, v, o, do, lse, lay: VarlenLayout, idx, cnt, scale: float | None = None):
     """K6: (dQ, dK, dV) bf16."""
     _need_cuda(q, k, v, o, do, lse, idx, cnt)
+    _need_qkv(q, k, v, lay)
+    _need_sel(idx, cnt, lay)
+    do = do.contiguous()  # autograd may hand a strided / expanded gradient
+    _need(o, "o", torch.bfloat16, 3, tuple(q.shape))
+    _need(do, "do", torch.bfloat16, 3, tuple(q.shape))
+    _need(lse, "lse", torch.float32, 2, (q.shape[1], q.shape[0]))
     T, Hq, D = q.shape
     Hkv = k.shape[1]
     hsel, _, k_max = idx.shape
@@ -231,7 +291,7 @@ def sparse_attn_bwd(q, k, v, o, do, lse, lay: VarlenLayout, idx, cnt, scale: flo
     ws_bytes = int(_lib().sb_sparse_attn_bwd_workspace_size(T, lay.nb_total, Hq, Hkv, D, hsel, k_max))
     ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=q.device)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-    _call("sb_sparse_attn_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(do.contiguous()), _ptr(lse),
+    _call("sb_sparse_attn_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(do), _ptr(lse),
           _ptr(lay.cu_seqlens), _ptr(lay.blk_off), lay.nseq, T, lay.nb_total, Hq, Hkv, D, lay.block_size, _ptr(idx),
           _ptr(cnt), hsel, k_max, C.c_float(scale), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), _stream())
     return dq, dk, dv

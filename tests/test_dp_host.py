@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 from paper_2604_13847_b200 import dp
 from paper_2604_13847_b200.host import api
 
-L, B = 3, 128
+L, B, MAXM = 3, 128, 4
 
 
 def rank_workload(rank):
@@ -37,9 +37,12 @@ def _worker(rank, world, port, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lengths, layer_profiles = rank_workload(rank)
-    pooled = dp.exchange_estimates(lengths, layer_profiles, width=256, block=B, world=world)
+    cfg = dp.DstSettings()
+    est = dp.rank_estimate(lengths, layer_profiles, cfg)
+    pooled = dp.exchange_estimates(est, L, len(cfg.budget_grid), world=world, max_members=MAXM)
+    assert [int(x) for x in pooled[rank].members] == [int(x) for x in lengths]
     table = api().synthesize_table(block_size=B)
-    k_final, decisions, k_base, xs = dp.decide_budgets(pooled, table, dp.DstSettings(), L)
+    k_final, decisions, k_base, xs = dp.decide_budgets_cov(pooled, table, cfg, L)
     out[rank] = (k_final.tolist(), [(d.micro_batch_id, d.layer_id, d.k_final, d.coverage_drop) for d in decisions],
                  k_base.tolist())
     dist.barrier()
@@ -92,10 +95,40 @@ def test_pooled_dst_matches_reference(ref):
 
 
 def test_pack_unpack_roundtrip():
+    """The exchanged estimate round-trips exactly, its size depends only on (L, |K|, max_members),
+    and an over-long member list is rejected instead of spilling into the next field."""
     lengths, layer_profiles = rank_workload(0)
-    vec = dp.pack_estimate(np.asarray(lengths), layer_profiles, 256).numpy()
-    got_len, got_prof = dp.unpack_estimate(vec, L, 256, B)
-    assert np.array_equal(got_len, lengths)
-    for s in range(len(lengths)):
-        for l in range(L):
-            assert np.array_equal(got_prof[s][l], layer_profiles[l][s])
+    cfg = dp.DstSettings()
+    est = dp.rank_estimate(lengths, layer_profiles, cfg)
+    G = len(cfg.budget_grid)
+    vec = dp.pack_estimate(est, L, G, MAXM).numpy()
+    assert vec.size == 3 + MAXM + L * (G + 1)
+    got = dp.unpack_estimate(vec, L, G, MAXM)
+    assert got.x == est.x and got.k_base == est.k_base
+    assert np.array_equal(got.members, lengths) and np.array_equal(got.cov, est.cov)
+    with pytest.raises(ValueError):
+        dp.pack_estimate(est, L, G, 1)
+    with pytest.raises(ValueError):
+        dp.pack_estimate(est, L + 1, G, MAXM)
+
+
+@pytest.mark.parametrize("anchor", ["min", "mean", "max"])
+@pytest.mark.parametrize("base_mode", ["coverage", "fixed"])
+def test_cov_exchange_decisions_equal_profile_decisions(anchor, base_mode):
+    """Deciding from the exchanged {x, k_base, C(K)} tables gives exactly the decisions of the
+    pooled PROFILES (decide_budgets -> tune_global_batch), fixed base off the grid included, on
+    the default and the dense 1..256 grids."""
+    table = api().synthesize_table(block_size=B)
+    for grid in (None, list(range(1, 257))):
+        cfg = dp.DstSettings(anchor=anchor, base_mode=base_mode, base_budget=37)
+        if grid is not None:
+            cfg.budget_grid = grid
+        ests, pooled = [], []
+        for r in range(4):
+            lengths, layer_profiles = rank_workload(r)
+            ests.append(dp.rank_estimate(lengths, layer_profiles, cfg))
+            pooled.append((np.asarray(lengths), [[layer_profiles[l][s] for l in range(L)] for s in range(len(lengths))]))
+        a = dp.decide_budgets(pooled, table, cfg, L)
+        b = dp.decide_budgets_cov(ests, table, cfg, L)
+        assert a[0].tolist() == b[0].tolist() and a[1] == b[1]
+        assert a[2].tolist() == b[2].tolist() and a[3].tolist() == b[3].tolist()

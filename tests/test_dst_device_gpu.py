@@ -87,8 +87,8 @@ def test_dpstep_on_device_matches_host_path():
         got = [int(t.item()) for t in dev_step.last["k_final_device"]]
         # host path over the same GPU profiles, the other ranks as single sequences
         host_step = dp.DPStep(batch, q, k, v, do, scales, table, cfg)
-        _, _, profs, _ = host_step.scorer_pass()
-        own = [dp.profiles_to_host(pr, lay) for pr in profs]
+        _, profs = host_step.scorer_pass()
+        own = [dp.profiles_to_host(profs[l], lay) for l in range(L)]
         pooled = [(np.asarray(lens), [[own[l][s] for l in range(L)] for s in range(len(lens))])]
         for x in others:
             nb = (x + B - 1) // B

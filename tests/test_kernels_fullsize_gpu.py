@@ -21,6 +21,39 @@ def _rand_bf16(shape, seed):
     return torch.randn(shape, generator=g, device="cuda").to(torch.bfloat16)
 
 
+def torch_topk_select(S, lay, k_seq, k_max, group):
+    """Independent restatement of the selector in torch: per selection row
+    (sum of the group's score rows), the diagonal plus the top-(min(k, i+1) - 1) earlier blocks
+    by (score desc, index asc) -- a stable descending sort keeps the lower index first on ties;
+    NaN ranks as -inf -- output ascending and -1 padded."""
+    Hs = S.shape[0]
+    hsel = Hs // group
+    Sg = S[:, :lay.tri_total].reshape(hsel, group, -1).sum(1) if group > 1 else S[:, :lay.tri_total]
+    nbt = lay.nb_total
+    idx = torch.full((hsel, nbt, k_max), -1, dtype=torch.int32, device=S.device)
+    cnt = torch.zeros((hsel, nbt), dtype=torch.int32, device=S.device)
+    blk, tri = lay.blk_off_host, lay.tri_off_host
+    for s in range(lay.nseq):
+        n = int(blk[s + 1] - blk[s])
+        if n == 0:
+            continue
+        ii, jj = torch.tril_indices(n, n, device=S.device)
+        full = torch.full((hsel, n, n), -math.inf, dtype=torch.float32, device=S.device)
+        full[:, ii, jj] = Sg[:, int(tri[s]):int(tri[s + 1])]
+        full = torch.nan_to_num(full, nan=-math.inf)
+        ar = torch.arange(n, device=S.device)
+        full[:, ar, ar] = -math.inf  # the diagonal is forced, not ranked
+        order = torch.sort(full, dim=2, descending=True, stable=True).indices
+        kk = int(min(k_seq[s], k_max))
+        for i in range(n):
+            want = max(1, min(kk, i + 1))
+            sel = torch.sort(order[:, i, :want - 1], dim=1).values if want > 1 else order[:, i, :0]
+            row = torch.cat([sel.to(torch.int32), torch.full((hsel, 1), i, dtype=torch.int32, device=S.device)], 1)
+            idx[:, int(blk[s]) + i, :want] = row
+            cnt[:, int(blk[s]) + i] = want
+    return idx, cnt
+
+
 def _run_and_check(cu, hq, hkv, d, B, hsel, k_seq, check_heads, seed):
     from paper_2604_13847_b200 import ops
 
@@ -48,6 +81,10 @@ def _run_and_check(cu, hq, hkv, d, B, hsel, k_seq, check_heads, seed):
         last = ic[:, blk[s] + i, want - 1]
         assert np.array_equal(last, np.broadcast_to(i, last.shape))  # diagonal last, ascending before it
     assert torch.isfinite(lse).all()
+    # Bit-exact selections against an independent torch top-k with the same tie rule.
+    ridx, rcnt = torch_topk_select(S, lay, k_seq, k_max, hq // hsel)
+    assert torch.equal(cnt, rcnt)
+    assert torch.equal(idx, ridx)
 
     ref, rdq, rdk, rdv = sparse_attention_ref(q, k, v, do, cu, B, idx, cnt, scale, check_heads, hsel)
     for h in check_heads:
@@ -82,19 +119,20 @@ def test_c3_rank_micro_batch():
 
 
 def test_c4_gqa_group_selection():
-    """C4: a 128K-token micro-batch of the mix ([32768 x 3, 2048 x 16]), GQA 4:1 (the 32q/8kv
-    ratio) with group-shared selection; kv head 0's whole group checked (dK, dV complete)."""
+    """C4: a 128K-token micro-batch of the mix ([32768 x 3, 2048 x 16]), BASELINE's GQA 32q / 8kv
+    with group-shared selection; kv heads 0 and 7 with their whole groups checked (dK, dV complete)."""
     lens = [32768] * 3 + [2048] * 16
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
-    _run_and_check(list(cu), 8, 2, 128, 128, 2, [16] * len(lens), [0, 1, 2, 3], 300)
+    _run_and_check(list(cu), 32, 8, 128, 128, 8, [16] * len(lens), [0, 1, 2, 3, 28, 29, 30, 31], 300)
 
 
-@pytest.mark.parametrize("keep", [0.05, 0.1])
+@pytest.mark.parametrize("keep", [0.05, 0.1, 0.25, 0.5])
 def test_c5_long_context(keep):
     """C5: a single 131072-token sequence (nb = 1024: selector rows up to 1024 candidates take
-    the CTA path), GQA 4:1 group selection, k = ceil(keep * 1024); kv head 0's group checked."""
+    the CTA path), BASELINE's GQA 32q / 8kv with group-shared selection, k = ceil(keep * 1024)
+    (52 / 103 / 256 / 512); kv head 0's whole group (q heads 0-3) checked, so its dK / dV too."""
     k = int(math.ceil(keep * 1024))
-    _run_and_check([0, 131072], 8, 2, 128, 128, 2, [k], [0, 1, 2, 3], 400)
+    _run_and_check([0, 131072], 32, 8, 128, 128, 8, [k], [0, 1, 2, 3], 400)
 
 
 @pytest.mark.parametrize("d,B", [(128, 128), (64, 64)])

@@ -93,12 +93,7 @@ def _ref(q, k, v, do, cu, B, idx, cnt, scale, heads, hsel, chunk, T, hq, hkv, d)
 
 
 def assert_close_bf16(got, ref, rel_fro, name=""):
-    """The bf16 rule of the device parity tests: max |err| <= 2e-2 * max(1, max|ref|) and a
-    relative Frobenius error below rel_fro."""
-    got = got.float()
-    ref = ref.float()
-    err = (got - ref).abs().max().item()
-    amax = ref.abs().max().item()
-    assert err <= 2e-2 * max(1.0, amax), (name, err, amax)
-    fro = ((got - ref).norm() / ref.norm().clamp(min=1e-12)).item()
-    assert fro < rel_fro, (name, fro)
+    """The bf16 rule of the device parity tests (tests/tolerance.py)."""
+    from tests.tolerance import check_bf16
+
+    return check_bf16(got, ref, name, rel_fro=rel_fro)
