@@ -60,7 +60,8 @@ int sb_block_scores(const float* qbar, const float* kbar, const int32_t* blk_off
                     const int64_t* tri_off, int nseq, int nb_max, int hq, int hkv, int head_dim,
                     float scale, float* scores, void* stream);
 
-/* K3: per selection row (hs, s, i): keep k = min(k_seq[s], i + 1) blocks. force_diag=1
+/* K3: per selection row (hs, s, i): keep k = max(1, min(k_seq[s], i + 1, k_max)) blocks (k_max is
+ * the idx row stride; a larger k_seq is clamped, never written past the row). force_diag=1
  * (causal MoBA): block i always, then the top-(k-1) of j < i; force_diag=0: top-k of j <= i.
  * Order: score descending, ties to the lower j; NaN ranks as -inf and -0.0 as +0.0.
  * group = Hs / Hsel score heads are summed (in head order, fp32) per selection row.

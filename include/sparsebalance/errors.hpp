@@ -9,6 +9,9 @@
 #include <stdexcept>
 #include <string>
 
+// Exported from libsparsebalance_b200.so (the library builds with -fvisibility=hidden): the
+// C++ API is part of the drop-in boundary.
+#pragma GCC visibility push(default)
 namespace sparsebalance {
 
 class ConfigError : public std::runtime_error {
@@ -17,3 +20,4 @@ class ConfigError : public std::runtime_error {
 };
 
 }  // namespace sparsebalance
+#pragma GCC visibility pop

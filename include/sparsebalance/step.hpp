@@ -18,6 +18,9 @@
 #include "sparsebalance/sab.hpp"
 #include "sparsebalance/workload.hpp"
 
+// Exported from libsparsebalance_b200.so (the library builds with -fvisibility=hidden): the
+// C++ API is part of the drop-in boundary.
+#pragma GCC visibility push(default)
 namespace sparsebalance {
 
 enum class Strategy { kBaseline, kDst, kSab, kLbb, kSabDst, kLbbDst };
@@ -61,3 +64,4 @@ StepPlan plan_step(std::span<const Sample> samples, Strategy strategy, const Ste
                    const ProfileTable& table, SparsityEstimator& est, int iter_index);
 
 }  // namespace sparsebalance
+#pragma GCC visibility pop

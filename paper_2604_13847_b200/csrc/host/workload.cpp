@@ -7,7 +7,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <fstream>
 #include <functional>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <string_view>
 #include <unordered_map>
 #include <unordered_set>
 
@@ -243,6 +249,61 @@ std::vector<Sample> generate_samples_unsorted(const LengthDistributionSpec& spec
                                               int num_layers, int block_size,
                                               std::uint64_t seed) {
   return generate_impl(spec, count, concentration, num_layers, block_size, seed, false);
+}
+
+namespace {
+
+std::string_view trim(std::string_view v) {
+  const auto ws = [](char c) { return c == ' ' || c == '\t' || c == '\r'; };
+  while (!v.empty() && ws(v.front())) v.remove_prefix(1);
+  while (!v.empty() && ws(v.back())) v.remove_suffix(1);
+  return v;
+}
+
+}  // namespace
+
+LengthDistributionSpec load_histogram(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw ConfigError("cannot open histogram file " + path);
+  LengthDistributionSpec spec;
+  spec.kind = LengthDistributionSpec::Kind::kHistogram;
+  std::string raw;
+  for (int line = 1; std::getline(in, raw); ++line) {
+    const std::string_view v = trim(raw);
+    if (v.empty() || v.front() == '#') continue;
+    const auto where = [&] { return path + ":" + std::to_string(line) + ": "; };
+    HistogramBin b;
+    char sep1 = 0, sep2 = 0;
+    std::istringstream fields{std::string(v)};
+    const bool ok = static_cast<bool>(fields >> b.lo >> sep1 >> b.hi >> sep2 >> b.frequency) && sep1 == ',' &&
+                    sep2 == ',' && (fields >> std::ws).eof();
+    if (!ok) throw ConfigError(where() + "expected 'lo,hi,frequency', got '" + raw + "'");
+    if (!(b.lo >= 1 && b.hi > b.lo)) throw ConfigError(where() + "bin bounds must satisfy 1 <= lo < hi");
+    if (!(b.frequency >= 0.0)) throw ConfigError(where() + "bin frequency must be >= 0");
+    spec.bins.push_back(b);
+  }
+  if (spec.bins.empty()) throw ConfigError("histogram file " + path + " has no bins");
+  spec.min_length = spec.bins[0].lo;
+  spec.max_length = spec.bins[0].hi - 1;
+  for (const HistogramBin& b : spec.bins) {
+    spec.min_length = std::min(spec.min_length, b.lo);
+    spec.max_length = std::max(spec.max_length, b.hi - 1);
+  }
+  validate_distribution(spec);
+  return spec;
+}
+
+void save_histogram(const std::vector<HistogramBin>& bins, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot write histogram file " + path);
+  out << "# lo_tokens,hi_tokens,frequency\n";
+  for (const HistogramBin& b : bins) {
+    char row[96];
+    std::snprintf(row, sizeof(row), "%lld,%lld,%.6f\n", static_cast<long long>(b.lo), static_cast<long long>(b.hi),
+                  b.frequency);
+    out << row;
+  }
+  if (!out) throw std::runtime_error("write failed for histogram file " + path);
 }
 
 GlobalBatch assemble_global_batch(std::span<const Sample> samples, const PackingPlan& plan,

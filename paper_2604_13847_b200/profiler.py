@@ -1,15 +1,21 @@
 """GPU cost-table profiler.
 
 Replaces the reference's synthetic stand-in for hardware profiling (`synthesize_table`,
-proj/core/src/profile_table.cpp:145-166) with measured latencies. For every (length x, budget k)
-cell of the grid it runs the real per-layer forward hot path (block scorer + top-k selector +
-sparse attention forward) on one packed sequence of x tokens with keep count k, times it with
-CUDA events (median of `reps`) and writes the reference CSV schema `x,k,latency_ms`
-(profile_table.cpp:168-182). load_table() then applies the same isotonic repair in k
-(profile_table.cpp:251-263). The simulator's convention is kept: the table holds the forward
-per-layer latency; backward = forward x fwd_bwd_ratio (sim.hpp:23).
+proj/core/src/profile_table.cpp:145-166) and its fixed backward ratio (`fwd_bwd_ratio` = 2.0,
+sim.hpp:23, applied in micro_batch_time, sim.cpp:88-98) with measured latencies. For every
+(length x, budget k) cell it runs one layer of the real hot path on one packed sequence of x
+tokens with keep count k and times, with CUDA events (median of `reps` windows),
 
-    python -m paper_2604_13847_b200.profiler --out b200_cost_table.csv
+  * fwd: block scorer (K1 + K2) + top-k selector (K3) + sparse attention forward (K5);
+  * bwd: sparse attention backward (K6, recompute from the saved LSE);
+
+and writes three CSVs in the reference schema `x,k,latency_ms` (profile_table.cpp:168-182):
+`<out>_fwd.csv`, `<out>_bwd.csv` and `<out>.csv` = fwd + bwd per layer, the per-layer training
+cost the tuner balances. load_table() applies the reference's isotonic repair in k to each
+(profile_table.cpp:251-263). GQA tables (--kv-heads < --heads) use group-shared selection.
+
+    python -m paper_2604_13847_b200.profiler --out profiles/b200_cost_table_h32_d128_b128
+    python -m paper_2604_13847_b200.profiler --kv-heads 8 --out profiles/b200_cost_table_h32kv8_d128_b128
 """
 from __future__ import annotations
 
@@ -23,34 +29,51 @@ from . import ops
 from .host import DEFAULT_BUDGET_GRID, DEFAULT_LENGTH_BINS, ProfileTable, api
 
 
-def measure_cell(q, k, v, lay, kk: int, reps: int, scale: float) -> float:
-    """Median over `reps` timed windows of the per-layer forward hot path; each window enqueues 8
-    layers back to back (as the step driver does) and divides, so the host's launch overhead
-    only counts where it exceeds the GPU work."""
+def measure_cell(q, k, v, do, lay, kk: int, reps: int, scale: float, group: int):
+    """(fwd ms, bwd ms) medians over `reps` timed windows; each window enqueues `n` layers back to
+    back (as the step driver does) and divides, so host launch overhead only counts where it
+    exceeds the GPU work. n shrinks for large cells so every cell costs ~ the same wall time."""
     k_seq = torch.full((lay.nseq,), kk, dtype=torch.int32, device=q.device)
     k_max = max(1, min(kk, lay.nb_max))
+    state = {}
 
-    def layer():
+    def fwd():
         S = ops.block_scores(q, k, lay, scale)
-        idx, cnt = ops.topk_select(S, lay, k_seq, k_max)
-        ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+        idx, cnt = ops.topk_select(S, lay, k_seq, k_max, group=group)
+        o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+        state.update(idx=idx, cnt=cnt, o=o, lse=lse)
 
-    layer()
+    def bwd():
+        ops.sparse_attn_bwd(q, k, v, state["o"], do, state["lse"], lay, state["idx"], state["cnt"], scale)
+
+    fwd()
+    bwd()
     torch.cuda.synchronize()
-    times = []
-    for _ in range(reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(8):
-            layer()
-        e1.record()
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1) / 8)
-    return float(np.median(times))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    fwd()
+    bwd()
+    b.record()
+    torch.cuda.synchronize()
+    n = int(max(1, min(8, 20.0 / max(1e-3, a.elapsed_time(b)))))
+    out = []
+    for fn in (fwd, bwd):
+        times = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(n):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / n)
+        out.append(float(np.median(times)))
+    return out[0], out[1]
 
 
-def profile_table(length_bins=None, budget_grid=None, heads=32, kv_heads=32, head_dim=128, block=128, reps=3,
-                  seed=0, device="cuda") -> ProfileTable:
+def profile_tables(length_bins=None, budget_grid=None, heads=32, kv_heads=32, head_dim=128, block=128, reps=3,
+                   seed=0, device="cuda"):
+    """-> (fwd, bwd, fwd + bwd) ProfileTables over the (length_bins x budget_grid) cells."""
     length_bins = list(DEFAULT_LENGTH_BINS if length_bins is None else length_bins)
     budget_grid = list(DEFAULT_BUDGET_GRID if budget_grid is None else budget_grid)
     g = torch.Generator(device=device).manual_seed(seed)
@@ -58,19 +81,34 @@ def profile_table(length_bins=None, budget_grid=None, heads=32, kv_heads=32, hea
     q = torch.randn((T, heads, head_dim), generator=g, device=device).to(torch.bfloat16)
     k = torch.randn((T, kv_heads, head_dim), generator=g, device=device).to(torch.bfloat16)
     v = torch.randn((T, kv_heads, head_dim), generator=g, device=device).to(torch.bfloat16)
+    do = torch.randn((T, heads, head_dim), generator=g, device=device).to(torch.bfloat16)
     scale = 1.0 / math.sqrt(head_dim)
-    lat = np.zeros((len(length_bins), len(budget_grid)))
+    group = heads // kv_heads
+    lf = np.zeros((len(length_bins), len(budget_grid)))
+    lb = np.zeros_like(lf)
     for xi, x in enumerate(length_bins):
         lay = ops.VarlenLayout.build([0, x], block, device=device)
-        qx, kx, vx = q[:x], k[:x], v[:x]
         for ki, kk in enumerate(budget_grid):
-            lat[xi, ki] = measure_cell(qx, kx, vx, lay, kk, reps, scale)
-    return ProfileTable(np.asarray(length_bins, np.int64), np.asarray(budget_grid, np.int32), lat)
+            lf[xi, ki], lb[xi, ki] = measure_cell(q[:x], k[:x], v[:x], do[:x], lay, kk, reps, scale, group)
+    bins = np.asarray(length_bins, np.int64)
+    grid = np.asarray(budget_grid, np.int32)
+    return ProfileTable(bins, grid, lf), ProfileTable(bins, grid, lb), ProfileTable(bins, grid, lf + lb)
+
+
+def write_tables(prefix: str, fwd: ProfileTable, bwd: ProfileTable, total: ProfileTable):
+    """Save the three tables with the reference writer and load them back through load_table
+    (isotonic repair in k); returns {path: repaired cell count}."""
+    h = api()
+    out = {}
+    for path, t in ((prefix + "_fwd.csv", fwd), (prefix + "_bwd.csv", bwd), (prefix + ".csv", total)):
+        h.save_table(t, path)
+        out[path] = h.load_table(path)[1]
+    return out
 
 
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
-    ap.add_argument("--out", required=True)
+    ap.add_argument("--out", required=True, help="path prefix: writes <out>.csv, <out>_fwd.csv, <out>_bwd.csv")
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--kv-heads", type=int, default=32)
     ap.add_argument("--head-dim", type=int, default=128)
@@ -78,12 +116,17 @@ def main():
     ap.add_argument("--max-x", type=int, default=262144)
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
+    if args.heads % args.kv_heads:
+        ap.error("--heads must be a multiple of --kv-heads")
+    prefix = args.out[:-4] if args.out.endswith(".csv") else args.out
     bins = [x for x in DEFAULT_LENGTH_BINS if x <= args.max_x]
-    t = profile_table(bins, None, args.heads, args.kv_heads, args.head_dim, args.block, args.reps)
-    h = api()
-    h.save_table(t, args.out)
-    loaded, repaired = h.load_table(args.out)
-    print(f"wrote {args.out}: {len(bins)} x {len(t.budget_grid)} cells, isotonic repair changed {repaired}")
+    fwd, bwd, tot = profile_tables(bins, None, args.heads, args.kv_heads, args.head_dim, args.block, args.reps)
+    rep = write_tables(prefix, fwd, bwd, tot)
+    ratio = bwd.latency_ms / np.maximum(fwd.latency_ms, 1e-9)
+    for p, r in rep.items():
+        print(f"wrote {p}: {len(bins)} x {len(fwd.budget_grid)} cells, isotonic repair changed {r}")
+    print(f"measured bwd/fwd ratio: min {ratio.min():.2f} median {np.median(ratio):.2f} max {ratio.max():.2f} "
+          f"(reference stand-in: 2.0, sim.hpp:23)")
 
 
 if __name__ == "__main__":
