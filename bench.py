@@ -43,6 +43,7 @@ METRIC = "max-over-ranks sparse-attn step ms & useful TFLOPS at 1/2/4/8 B200 vs 
 CFG = dict(tokens=32768, heads=32, head_dim=128, block=128, keep_lo=0.05, keep_hi=0.5, seed=42)
 C3_DIST = dict(short_weight=0.6, short_log_mean=float(np.log(2048)), short_log_sigma=0.0,
                long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
+FWD_TILE_M = {64: 128, 128: 128}  # query rows per forward UMMA tile at block size B (attn_fwd.cu)
 COST_TABLE = os.path.join(ROOT, "profiles", "b200_cost_table_h32_d128_b128.csv")
 
 
@@ -399,7 +400,8 @@ def sub_c1(torch, ops, dev, steps, with_cpu=True):
     out = {"workload": "C1: one 4096-token sequence, 8 heads MHA, d64, B64, keep 0.25 (k=16), forward",
            "useful_gflop": f_fwd / 1e9, "fwd_attn_ms": t_fwd, "fwd_attn_tflops": f_fwd / (t_fwd * 1e-3) / 1e12,
            "scorer_selector_fwd_ms": t_full,
-           "executed_over_useful": tiles * 64 * 64 / e}
+           # the forward kernel runs UMMA tiles of FWD_TILE_M query rows x B keys per pair
+           "fwd_tile_m": FWD_TILE_M[B], "executed_over_useful": tiles * FWD_TILE_M[B] * B / e}
     if with_cpu:
         from oracle import device as orc
 

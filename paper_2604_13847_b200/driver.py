@@ -11,6 +11,12 @@ top-k selector with the DST keep count of that (micro-batch, layer), clamped per
 sparse attention fwd -> bwd) timed with CUDA events, and the per-(rank, micro-batch) times are
 all-gathered.
 
+The tuner is closed-loop: its routing profiles are not the generator's but the K4 coverage
+profiles of the GPU block scores, measured by a scorer pre-pass over every layer on inputs that
+carry the generator's routing draws (synth.py), exchanged with one all-reduce, and written per
+iteration (gpu_profiles_<it>.npz) so the decisions can be replayed on the host and against the
+compiled reference bit for bit (tests/test_driver.py).
+
 It emits the reference's replay files per iteration, so a run can be replayed against the
 oracle:
   * iterations CSV with the reference's header and %.6f fields (report.cpp:55-74):
@@ -26,6 +32,7 @@ oracle:
 from __future__ import annotations
 
 import argparse
+import copy
 import math
 import os
 import time
@@ -33,7 +40,7 @@ import time
 import numpy as np
 import torch
 
-from . import ops
+from . import ops, synth
 from . import pp_projection as ppj
 from .host import DEFAULT_BUDGET_GRID, ProfileTable, api
 
@@ -77,7 +84,7 @@ class Driver:
     def __init__(self, strategy="sab_dst", gbs=16, mbs=2, layers=4, block=128, heads=32, kv_heads=32, head_dim=128,
                  seed=42, dist_spec=None, table: ProfileTable | None = None, anchor="mean", threshold_p=0.1,
                  dst_scope="global", base_mode="coverage", varlen_block_size=0, project_pp=0, rank=0, world=1,
-                 group=None, device="cuda"):
+                 group=None, device="cuda", dst_grid=None):
         self.h = api()
         self.strategy, self.gbs, self.mbs, self.layers, self.B = strategy, gbs, mbs, layers, block
         self.H, self.Hkv, self.D = heads, kv_heads, head_dim
@@ -88,6 +95,7 @@ class Driver:
         max_len = int((dist_spec or {}).get("max_length", 65536))
         self.est = self.h.make_estimator(self.h.default_bin_edges(max_len), budget_grid=self.grid)
         self.plan_kw = dict(anchor=anchor, threshold_p=threshold_p, dst_scope=dst_scope, base_mode=base_mode,
+                            dst_grid=dst_grid,
                             varlen_block_size=varlen_block_size)
         self._buf_T = 0
         self._warm = False
@@ -99,19 +107,26 @@ class Driver:
         # Per-layer softmax temperature, so layers differ as real layers do (fixed seed).
         self.layer_scales = np.exp(np.random.default_rng(seed).uniform(-0.5, 1.0, size=layers))
 
-    def _buffers(self, T: int):
-        if T > self._buf_T:
-            g = torch.Generator(device=self.device).manual_seed(self.seed + self.rank)
-            mk = lambda h: torch.randn((T, h, self.D), generator=g, device=self.device).to(torch.bfloat16)  # noqa: E731
-            self.q, self.k, self.v, self.do = mk(self.H), mk(self.Hkv), mk(self.Hkv), mk(self.H)
-            self._buf_T = T
-        return self.q[:T], self.k[:T], self.v[:T], self.do[:T]
+    def _inputs(self, ids, lengths, routing):
+        """Planted-routing Q/K/V/dO of one micro-batch (synth.py): member s's keys carry the
+        generator's pre-sort layer-0 routing draws, so the GPU block scores -- and the K4
+        profiles the tuner reads -- carry the generator's concentration."""
+        mem = [int(lengths[i]) for i in ids]
+        seed = self.seed + 7919 * self.rank + int(ids[0])
+        return synth.planted_qkv(mem, [routing[i][0] for i in ids], self.H, self.Hkv, self.D, self.B, seed,
+                                 device=self.device)
 
-    def _run_micro_batch(self, lengths: np.ndarray, budgets: np.ndarray) -> float:
-        cu = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
-        T = int(cu[-1])
-        lay = ops.VarlenLayout.build(cu, self.B, device=self.device)
-        q, k, v, do = self._buffers(T)
+    def _profile_pass(self, q, k, lay):
+        """Scorer pre-pass (K1 + K2 + K4) over every layer -> host profiles [layer][member]."""
+        qbar, kbar = ops.block_pool(q, lay), ops.block_pool(k, lay)
+        profs = torch.empty((self.layers, lay.nseq, max(1, lay.nb_max)), dtype=torch.float64, device=self.device)
+        for l in range(self.layers):
+            scale = float(self.layer_scales[l]) / math.sqrt(self.D)
+            profs[l] = ops.coverage_profile(ops.block_scores(q, k, lay, scale, qbar=qbar, kbar=kbar), lay)
+        return profs
+
+    def _run_micro_batch(self, inputs, lay, budgets: np.ndarray):
+        q, k, v, do = inputs
         nb = lay.nb_per_seq
         k_all = torch.from_numpy(np.minimum(budgets[:, None], nb[None, :]).astype(np.int32)).to(self.device)
         if not self._warm:  # first micro-batch: one untimed pass so allocator / module load stay out of the timing
@@ -139,18 +154,64 @@ class Driver:
             if ev is not None:
                 ev[2 * l + 2].record()
 
-    def iteration(self, it: int, decisions_csv=None, plan_json=None) -> dict:
-        lengths, profs = self.h.generate_samples(self.gbs, self.layers, self.B, seed=mix_seed(self.seed, it),
-                                                 dist=self.dist_spec)
+    def _gpu_profiles(self, lengths, routing, bins):
+        """Closed loop: this rank's micro-batches through the scorer pre-pass; every sample's
+        per-layer GPU profile assembled on every rank with one all-reduce (each sample's slot is
+        written by exactly one rank, the others add zeros: exact). -> (profiles[sample][layer],
+        per-micro-batch pre-pass ms, cached (inputs, layout) per micro-batch)."""
+        nb = (np.asarray(lengths, np.int64) + self.B - 1) // self.B
+        off = np.concatenate([[0], np.cumsum(nb * self.layers)])
+        flat = torch.zeros(int(off[-1]), dtype=torch.float64, device=self.device)
+        pre_ms, cache = [], []
+        for ids in bins[self.rank]:
+            cu = np.concatenate([[0], np.cumsum([int(lengths[i]) for i in ids])]).astype(np.int64)
+            lay = ops.VarlenLayout.build(cu, self.B, device=self.device)
+            inputs = self._inputs(ids, lengths, routing)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            profs = self._profile_pass(inputs[0], inputs[1], lay)
+            e1.record()
+            for s, i in enumerate(ids):
+                flat[int(off[i]):int(off[i + 1])] = profs[:, s, :nb[i]].reshape(-1)
+            cache.append((inputs, lay))
+            pre_ms.append((e0, e1))
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(flat, group=self.group)
+        host = flat.cpu().numpy()
+        profiles = [[host[int(off[i]) + l * nb[i]:int(off[i]) + (l + 1) * nb[i]].copy() for l in range(self.layers)]
+                    for i in range(len(lengths))]
+        return profiles, [a.elapsed_time(b) for a, b in pre_ms], cache
+
+    def iteration(self, it: int, decisions_csv=None, plan_json=None, profiles_npz=None) -> dict:
+        lengths, routing = self.h.generate_samples(self.gbs, self.layers, self.B, seed=mix_seed(self.seed, it),
+                                                   dist=self.dist_spec, sorted=False)
+        ids = np.arange(self.gbs)
+        kw = dict(gbs=self.gbs, mbs=self.mbs, dp=self.world, num_layers=self.layers, table=self.table, iter_index=it,
+                  **self.plan_kw)
+        # 1) the batch plan does not read profiles (SAB / LBB plan from lengths + the estimator,
+        #    sequential from order): plan once on a scratch copy of the estimator to learn which
+        #    samples this rank owns, 2) score them on the GPU, 3) plan the step for real on the
+        #    GPU profiles (same plan, DST on measured routing; the estimator calibrates once).
+        scratch = copy.deepcopy(self.est)
+        gen_sorted = [[np.sort(p)[::-1] for p in r] for r in routing]
+        bins = self.h.plan_step(self.strategy, ids, lengths, gen_sorted, est=scratch, **kw)["micro_batch_bins"]
+        profiles, pre_ms, cache = self._gpu_profiles(lengths, routing, bins)
         t0 = time.perf_counter()
-        sp = self.h.plan_step(self.strategy, np.arange(self.gbs), lengths, profs, gbs=self.gbs, mbs=self.mbs,
-                              dp=self.world, num_layers=self.layers, table=self.table, est=self.est, iter_index=it,
-                              decisions_csv=decisions_csv, plan_json=plan_json, **self.plan_kw)
+        sp = self.h.plan_step(self.strategy, ids, lengths, profiles, est=self.est, decisions_csv=decisions_csv,
+                              plan_json=plan_json, **kw)
         host_ms = (time.perf_counter() - t0) * 1e3
-        rows = []  # per micro-batch: [total, fwd_0..fwd_{L-1}, bwd_0..bwd_{L-1}]
-        for m, ids in enumerate(sp["micro_batch_bins"][self.rank]):
-            tot, tf, tb = self._run_micro_batch(np.asarray(lengths)[ids], sp["budgets"][self.rank][m])
-            rows.append([tot] + tf + tb)
+        if sp["micro_batch_bins"] != bins:
+            raise RuntimeError("batch plan changed between the pre-plan and the step plan")
+        if profiles_npz is not None and self.rank == 0:
+            np.savez_compressed(profiles_npz, lengths=np.asarray(lengths), layers=self.layers,
+                                **{f"p{i}_{l}": profiles[i][l] for i in range(len(lengths)) for l in range(self.layers)})
+        rows = []  # per micro-batch: [total, fwd_0..fwd_{L-1}, bwd_0..bwd_{L-1}]; total includes the pre-pass
+        for m, (inputs, lay) in enumerate(cache):
+            tot, tf, tb = self._run_micro_batch(inputs, lay, sp["budgets"][self.rank][m])
+            rows.append([tot + pre_ms[m]] + tf + tb)
+        del cache
         if self.world > 1:
             import torch.distributed as dist
 
@@ -163,7 +224,7 @@ class Driver:
         mb_ms = [[r[0] for r in rr] for rr in all_rows]
         rec = summarize(mb_ms)
         rec.update(dst_overhead_ms=host_ms, avg_budget=sp["avg_budget"], mean_cov_drop=sp["mean_cov_drop"],
-                   mb_ms=mb_ms)
+                   mb_ms=mb_ms, budgets=sp["budgets"], decisions=sp["decisions"])
         if self.project_pp:
             L = self.layers
             cl = ppj.Cluster(pp=self.project_pp, layers_per_stage=L // self.project_pp, comm_ms=0.05, dp_sync_ms=0.0)
@@ -181,7 +242,8 @@ class Driver:
             files = {}
             if out_dir and self.rank == 0:
                 files = dict(decisions_csv=os.path.join(out_dir, f"decisions_{it}.csv"),
-                             plan_json=os.path.join(out_dir, f"plan_{it}.json"))
+                             plan_json=os.path.join(out_dir, f"plan_{it}.json"),
+                             profiles_npz=os.path.join(out_dir, f"gpu_profiles_{it}.npz"))
             records.append(self.iteration(it, **files))
         if out_dir and self.rank == 0:
             with open(os.path.join(out_dir, "iterations.csv"), "w") as f:
@@ -207,6 +269,8 @@ def main():
                                                    "the reference generator's default distribution")
     ap.add_argument("--table", default=None, help="cost table CSV (x,k,latency_ms), e.g. from profiler.py")
     ap.add_argument("--varlen", action="store_true", help="opt-in varlen-aware DST cost (predict_members at B)")
+    ap.add_argument("--dense-grid", action="store_true", help="DST budget grid 1..256 (SURVEY 7.3(5): the 1.05x "
+                                                                   "balance target) instead of the table's 16 points")
     ap.add_argument("--project-pp", type=int, default=0, help="also project a PP-stage 1F1B pipeline from the "
                                                               "measured per-layer times (pp_projection.py)")
     ap.add_argument("--heads", type=int, default=32, help="query heads")
@@ -231,6 +295,7 @@ def main():
     drv = Driver(args.strategy, gbs=args.gbs_per_rank * world, mbs=args.mbs, layers=args.layers, dist_spec=dist_spec,
                  table=table, varlen_block_size=128 if args.varlen else 0, project_pp=args.project_pp, rank=rank,
                  world=world, heads=args.heads, kv_heads=args.kv_heads,
+                 dst_grid=list(range(1, 257)) if args.dense_grid else None,
                  device=torch.device("cuda", local))
     recs = drv.run(args.iters, args.out)
     if rank == 0:

@@ -49,3 +49,16 @@ def test_driver_short_run(tmp_path):
     assert (tmp_path / "decisions_1.csv").read_text().startswith("iter,mb,layer,")
     assert (tmp_path / "plan_0.json").exists()
     assert len((tmp_path / "iterations_pp2.csv").read_text().splitlines()) == 3
+    # Closed loop: the decisions came from the GPU profiles; replaying them through the host
+    # planner (fresh estimator = iteration 0's state) reproduces the decisions bit for bit.
+    from paper_2604_13847_b200.host import api
+
+    z = np.load(tmp_path / "gpu_profiles_0.npz")
+    lengths = z["lengths"]
+    profiles = [[z[f"p{i}_{l}"] for l in range(2)] for i in range(len(lengths))]
+    h = api()
+    est = h.make_estimator(h.default_bin_edges(8192), budget_grid=drv.grid)
+    sp = h.plan_step("sab_dst", np.arange(4), lengths, profiles, gbs=4, mbs=1, dp=1, num_layers=2, table=drv.table,
+                     est=est, iter_index=0, **drv.plan_kw)
+    assert sp["decisions"] == recs[0]["decisions"]
+    assert np.array_equal(sp["budgets"], recs[0]["budgets"])
