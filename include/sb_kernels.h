@@ -112,6 +112,15 @@ int sb_sparse_attn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                        const int32_t* idx, const int32_t* cnt, int hsel, int k_max, float scale,
                        uint16_t* o, float* lse, void* workspace, void* stream);
 
+/* K5 with the bf16 rounding residual of O: o_res = bf16(O - bf16(O)) (NULL: not written). Fed to
+ * sb_sparse_attn_bwd_ex, it makes D = rowsum(dO * O) accurate to ~2^-16 instead of bf16 (dS on
+ * rows that attend few keys is a difference of nearly equal terms; see tests/tolerance.py). */
+int sb_sparse_attn_fwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                          const int32_t* cu_seqlens, const int32_t* blk_off, int nseq, int total_tokens,
+                          int nb_total, int hq, int hkv, int head_dim, int block_size,
+                          const int32_t* idx, const int32_t* cnt, int hsel, int k_max, float scale,
+                          uint16_t* o, uint16_t* o_res, float* lse, void* workspace, void* stream);
+
 /* K6 (+K7): dQ, dK, dV from dO with P recomputed from the saved LSE; D = rowsum(dO * O).
  * K/V gradients accumulate over the q heads of each GQA group and over every q block that
  * selected the key block (deterministic: a kv-major pass over the transposed selection).
@@ -125,6 +134,21 @@ int sb_sparse_attn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                        int block_size, const int32_t* idx, const int32_t* cnt, int hsel,
                        int k_max, float scale, uint16_t* dq, uint16_t* dk, uint16_t* dv,
                        void* workspace, void* stream);
+
+/* K6 with flags. SB_BWD_DETERMINISTIC selects the two-pass backward (dK/dV pass over the
+ * transposed selection, then a dQ pass; 7 UMMAs per pair; bit-identical run to run). Without it,
+ * D = B = 128 runs the fused single pass (5 UMMAs per pair; dQ partials TMA-reduce-added in fp32,
+ * so dQ is reproducible to fp32 summation order) and other shapes the two-pass kernels.
+ * sb_sparse_attn_bwd == sb_sparse_attn_bwd_ex(..., flags = 0). Same workspace size. */
+#define SB_BWD_DETERMINISTIC 1
+int sb_sparse_attn_bwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                          const uint16_t* o, const uint16_t* o_res /* may be NULL */,
+                          const uint16_t* d_o, const float* lse,
+                          const int32_t* cu_seqlens, const int32_t* blk_off, int nseq,
+                          int total_tokens, int nb_total, int hq, int hkv, int head_dim,
+                          int block_size, const int32_t* idx, const int32_t* cnt, int hsel,
+                          int k_max, float scale, uint16_t* dq, uint16_t* dk, uint16_t* dv,
+                          void* workspace, void* stream, int flags);
 
 /* Diagnostics: number of hot-path kernel launches issued by this library since load. */
 uint64_t sb_launch_count(void);

@@ -34,7 +34,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 __host__ __device__ constexpr uint32_t pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
 // ------------------------------------------------------------------------------------ prep
+// With ores (the forward's bf16 rounding residual of O), D = rowsum(dO * (O + O_res)): O to ~2^-16
+// instead of bf16, which keeps dS accurate on rows that attend few keys (there dP - D cancels).
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ d_o,
+                                                       const uint16_t* __restrict__ ores,
                                                        const float* __restrict__ lse, int total, int hq, int d, int tp,
                                                        float* __restrict__ lse2, float* __restrict__ dvec) {
   // Head h = blockIdx.y; consecutive threads walk consecutive tokens of that head, so the
@@ -64,6 +67,18 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const uint16_t* __restric
       acc0 = fmaf(__uint_as_float(wa0[e] & 0xffff0000u), __uint_as_float(wb0[e] & 0xffff0000u), acc0);
       acc1 = fmaf(__uint_as_float(wa1[e] << 16), __uint_as_float(wb1[e] << 16), acc1);
       acc1 = fmaf(__uint_as_float(wa1[e] & 0xffff0000u), __uint_as_float(wb1[e] & 0xffff0000u), acc1);
+    }
+    if (ores != nullptr) {
+      const uint4 c0 = __ldg(reinterpret_cast<const uint4*>(ores) + e0);
+      const uint4 c1 = __ldg(reinterpret_cast<const uint4*>(ores) + e1);
+      const uint32_t wc0[4] = {c0.x, c0.y, c0.z, c0.w}, wc1[4] = {c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc0 = fmaf(__uint_as_float(wc0[e] << 16), __uint_as_float(wb0[e] << 16), acc0);
+        acc0 = fmaf(__uint_as_float(wc0[e] & 0xffff0000u), __uint_as_float(wb0[e] & 0xffff0000u), acc0);
+        acc1 = fmaf(__uint_as_float(wc1[e] << 16), __uint_as_float(wb1[e] << 16), acc1);
+        acc1 = fmaf(__uint_as_float(wc1[e] & 0xffff0000u), __uint_as_float(wb1[e] & 0xffff0000u), acc1);
+      }
     }
     for (int off = (1 << tpr_log) >> 1; off; off >>= 1) {
       acc0 += __shfl_xor_sync(0xffffffffu, acc0, off);
@@ -1158,13 +1173,522 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
   }
 }
 
+// ------------------------------------------------------------------------------------ fused
+// Single-pass backward for D = B = 128: 5 UMMAs per (key block, q tile) pair instead of the
+// two-pass 7. Persistent over key-block items (hk, gj) like the dK/dV pass; per pair it also
+// forms the pair's dQ partial dS K in TMEM and TMA-reduce-adds it (cp.reduce.async.bulk.tensor,
+// fp32 add in L2) into an fp32 dQ accumulator, converted to bf16 by a final elementwise pass.
+// The accumulation order of dQ across key blocks is not fixed, so dQ is reproducible to fp32
+// rounding only; the two-pass path stays as the bit-deterministic mode.
+//
+// TMEM (512 columns): SP | dQ | dV | dK. SP holds the pair's two score tiles in turn (S^T and
+// dP^T; the math warps read the first before the second is issued) and then P^T | dS^T packed as
+// bf16, the A operands of dV += P^T dO and dK += dS^T Q. dQ = dS K reads dS from shared memory
+// (MN-major A), written into the pair's dO ring slot once dV has read dO; the same slot then
+// stages the fp32 dQ partial for the TMA reduce and is released to the producer after it.
+// An item's first pair computes dP^T before S^T, so the next key block's K load (single K
+// buffer: K is read by S^T and by dQ up to the item's last pair) overlaps that first dP^T.
+//   Issue order: A_g, [sp_free] B_g, [p_ready] dV_g, [ds_ready] dK_g, A_{g+1}, [dsm_ready, dq_free]
+//   dQ_g, [sp_free] B_{g+1}, ...   (A / B = S^T / dP^T, swapped on an item's first pair)
+// Warps 0..3 (one warpgroup, 96 registers): TMA producer, UMMA issuer, two idle; warps 4..11
+// (200 registers): two math warpgroups splitting every key row's query columns in halves.
+constexpr int kFusedThreads = 384;
+
+struct FusedCfg {
+  static constexpr int kTile = 2 * kM * 128;  // 128 rows x 128 bf16 columns (two SW128 chunks)
+  static constexpr int kAugOnes = kM * 32, kAug = kM * 32;
+  static constexpr int kSmemTiles = 2 * kTile + 2 * kTile + 2 * kTile + kAugOnes + 4 * kAug;  // K,V | Q[2] | dO[2] | aug
+  static constexpr int kSP = 0, kDQ = 128, kDV = 256, kDK = 384;
+  static constexpr uint32_t kCols = 512;
+  static constexpr int kSmemBytes = kSmemTiles + 1024 + 256;
+};
+
+struct FusedBars {
+  uint64_t k_full, k_empty, v_full, v_empty;
+  uint64_t q_full[2], q_empty[2], do_full[2], do_empty[2];
+  uint64_t sp_full, sp_free;            // UMMA <-> math: a score tile in SP / the first one read
+  uint64_t p_ready, ds_ready, dsm_ready;  // math -> UMMA: P^T, dS^T packed in SP; dS in smem
+  uint64_t dv_done;                     // UMMA -> math: dV_g read dO_g (the slot may take dS_g)
+  uint64_t dq_full, dq_free;            // UMMA <-> math: the pair's dQ partial in TMEM / read
+  uint64_t acc_done;                    // UMMA -> math: the item's dV / dK are final
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
+    const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+    const __grid_constant__ CUtensorMap tm_dqacc, const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off,
+    int nseq, int hq, int hkv, int hsel, const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent,
+    const float* __restrict__ lse2, const float* __restrict__ dvec, int tp, float scale, float scale_log2,
+    uint16_t* __restrict__ dk, uint16_t* __restrict__ dv, const int32_t* __restrict__ order, int n_items) {
+  constexpr int D = 128, B = 128;
+  using C = FusedCfg;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint8_t* k_smem = smem;
+  uint8_t* v_smem = smem + C::kTile;
+  uint8_t* q_smem = smem + 2 * C::kTile;    // [2]
+  uint8_t* do_smem = smem + 4 * C::kTile;   // [2]: dO_g, then dS_g, then the dQ_g partial staging
+  uint8_t* ones_smem = smem + 6 * C::kTile;
+  uint8_t* qaug_smem = ones_smem + C::kAugOnes;  // [2] -lse2 / scale_log2
+  uint8_t* daug_smem = qaug_smem + 2 * C::kAug;  // [2] -D
+  FusedBars* bars = reinterpret_cast<FusedBars*>(smem + C::kSmemTiles);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbt = blk_off[nseq];
+  const int grid = gridDim.x, cta = blockIdx.x;
+  const int sg = hq / hsel;
+  const float inv_scale_log2 = 1.0f / scale_log2;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->k_full, 1);
+    mbar_init(&bars->k_empty, 1);
+    mbar_init(&bars->v_full, 1);
+    mbar_init(&bars->v_empty, 1);
+    for (int st = 0; st < 2; ++st) {
+      mbar_init(&bars->q_full[st], 2);   // TMA expect_tx arrive + augmented-slice arrive
+      mbar_init(&bars->q_empty[st], 1);  // UMMA commit after dK
+      mbar_init(&bars->do_full[st], 2);
+      mbar_init(&bars->do_empty[st], 2);  // one per math warpgroup after its dQ reduce read the slot
+    }
+    mbar_init(&bars->sp_full, 1);
+    mbar_init(&bars->sp_free, 256);
+    mbar_init(&bars->p_ready, 256);
+    mbar_init(&bars->ds_ready, 256);
+    mbar_init(&bars->dsm_ready, 256);
+    mbar_init(&bars->dv_done, 1);
+    mbar_init(&bars->dq_full, 1);
+    mbar_init(&bars->dq_free, 256);
+    mbar_init(&bars->acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<C::kCols>(&bars->tmem_base);
+  {
+    uint4* z = reinterpret_cast<uint4*>(ones_smem);
+    for (int i = threadIdx.x; i < (C::kAugOnes + 4 * C::kAug) / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    for (int r = threadIdx.x; r < kM; r += blockDim.x)
+      *reinterpret_cast<uint2*>(ones_smem + aug_off(r)) = make_uint2(0x3F803F80u, 0x00003F80u);
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  auto pair_of = [&](const KvItem& w, int m, int& h, int& gi) {
+    const int ent = __ldg(tr_ent + w.e0 + m / sg);
+    const int hs = ent / nbt;
+    gi = ent - hs * nbt;
+    h = hs * sg + m % sg;
+  };
+
+  if (warp < 4) setmaxnreg_dec<96>();
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer (whole warp)
+    if (lane == 0) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      tma_prefetch(&tm_do);
+    }
+    int g = 0, t = 0;
+    auto load_q = [&](int gg, int h, int q0, int nq) {
+      const int st = gg & 1;
+      float nl[B / 32];
+#pragma unroll
+      for (int e = 0; e < B / 32; ++e) {
+        const int r = e * 32 + lane;
+        nl[e] = r < nq ? __ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+      }
+      mbar_wait(&bars->q_empty[st], ((gg >> 1) & 1) ^ 1);
+      if (lane == 0) {
+        mbar_expect_tx(&bars->q_full[st], C::kTile);
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d(q_smem + st * C::kTile + c * kM * 128, &tm_q, &bars->q_full[st], c * 64, h, q0);
+      }
+      uint8_t* qa = qaug_smem + st * C::kAug;
+#pragma unroll
+      for (int e = 0; e < B / 32; ++e)
+        *reinterpret_cast<uint2*>(qa + aug_off(e * 32 + lane)) = split3_bf16(-nl[e] * inv_scale_log2);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->q_full[st]);
+    };
+    auto load_do = [&](int gg, int h, int q0, int nq) {
+      const int st = gg & 1;
+      float nd[B / 32];
+#pragma unroll
+      for (int e = 0; e < B / 32; ++e) {
+        const int r = e * 32 + lane;
+        nd[e] = r < nq ? __ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+      }
+      mbar_wait(&bars->do_empty[st], ((gg >> 1) & 1) ^ 1);
+      if (lane == 0) {
+        mbar_expect_tx(&bars->do_full[st], C::kTile);
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d(do_smem + st * C::kTile + c * kM * 128, &tm_do, &bars->do_full[st], c * 64, h, q0);
+      }
+      uint8_t* da = daug_smem + st * C::kAug;
+#pragma unroll
+      for (int e = 0; e < B / 32; ++e) *reinterpret_cast<uint2*>(da + aug_off(e * 32 + lane)) = split3_bf16(-nd[e]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->do_full[st]);
+    };
+    for (int k = 0;; ++k) {
+      const int it = sched::snake_item(order, n_items, grid, cta, k);
+      if (it < 0) break;
+      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+      const int items = w.ne * sg;
+      if (items == 0) continue;
+      const int kv0 = w.seq0 + w.jl * B;
+      const int blk0 = w.gj - w.jl;
+      if (lane == 0) {  // V first: the item's first UMMA is dP^T
+        mbar_wait(&bars->v_empty, (t & 1) ^ 1);
+        mbar_expect_tx(&bars->v_full, C::kTile);
+        for (int c = 0; c < 2; ++c) tma_load_3d(v_smem + c * kM * 128, &tm_v, &bars->v_full, c * 64, w.hk, kv0);
+      }
+      for (int m = 0; m < items; ++m, ++g) {
+        int h, gi;
+        pair_of(w, m, h, gi);
+        const int q0 = w.seq0 + (gi - blk0) * B;
+        const int nq = min(B, w.seq_len - (gi - blk0) * B);
+        if (m == 0) {
+          load_do(g, h, q0, nq);
+          load_q(g, h, q0, nq);
+          if (lane == 0) {  // K after the first pair's dO / Q: the previous item's last dQ reads K
+            mbar_wait(&bars->k_empty, (t & 1) ^ 1);
+            mbar_expect_tx(&bars->k_full, C::kTile);
+            for (int c = 0; c < 2; ++c) tma_load_3d(k_smem + c * kM * 128, &tm_k, &bars->k_full, c * 64, w.hk, kv0);
+          }
+        } else {
+          load_q(g, h, q0, nq);
+          load_do(g, h, q0, nq);
+        }
+      }
+      ++t;
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ UMMA issuer (whole warp)
+    const uint32_t leader = elect_one();
+    constexpr uint32_t idesc_t = idesc_bf16_f32(kM, B, false, false);
+    constexpr uint32_t idesc_acc = idesc_bf16_f32(kM, D, false, true);
+    constexpr uint32_t idesc_dq = idesc_bf16_f32(kM, D, true, true);
+    const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem), ones_addr = smem_u32(ones_smem);
+    auto qa = [&](int gg) { return smem_u32(q_smem + (gg & 1) * C::kTile); };
+    auto da = [&](int gg) { return smem_u32(do_smem + (gg & 1) * C::kTile); };
+    auto issue_st = [&](int gg) {
+      mbar_wait(&bars->q_full[gg & 1], (gg >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
+        mma_ss(tmem + C::kSP, desc_sw128(k_addr + off, 16, 1024), desc_sw128(qa(gg) + off, 16, 1024), idesc_t, kk > 0,
+               leader);
+      }
+      mma_ss(tmem + C::kSP, desc_aug(ones_addr), desc_aug(smem_u32(qaug_smem + (gg & 1) * C::kAug)), idesc_t, 1u,
+             leader);
+      tc_commit(&bars->sp_full, leader);
+    };
+    auto issue_dpt = [&](int gg) {
+      mbar_wait(&bars->do_full[gg & 1], (gg >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
+        mma_ss(tmem + C::kSP, desc_sw128(v_addr + off, 16, 1024), desc_sw128(da(gg) + off, 16, 1024), idesc_t, kk > 0,
+               leader);
+      }
+      mma_ss(tmem + C::kSP, desc_aug(ones_addr), desc_aug(smem_u32(daug_smem + (gg & 1) * C::kAug)), idesc_t, 1u,
+             leader);
+      tc_commit(&bars->sp_full, leader);
+    };
+    int g = 0, t = 0;
+    bool a_issued = false;  // tile A of pair g already issued (at the end of pair g - 1)
+    KvItem w;
+    int k = 0;
+    auto next_item = [&](KvItem& out) -> bool {
+      for (;; ++k) {
+        const int it = sched::snake_item(order, n_items, grid, cta, k);
+        if (it < 0) return false;
+        out = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+        if (out.ne * sg > 0) {
+          ++k;
+          return true;
+        }
+      }
+    };
+    bool have = next_item(w);
+    while (have) {
+      const int items = w.ne * sg;
+      KvItem nx;
+      bool have_nx = false;
+      for (int m = 0; m < items; ++m, ++g) {
+        const bool last = m + 1 == items;
+        if (!a_issued) {  // only the CTA's very first pair: dP^T first
+          mbar_wait(&bars->v_full, t & 1);
+          issue_dpt(g);
+        }
+        a_issued = false;
+        // tile B
+        mbar_wait(&bars->sp_free, g & 1);
+        if (m == 0) {
+          mbar_wait(&bars->k_full, t & 1);
+          issue_st(g);
+        } else {
+          issue_dpt(g);
+        }
+        if (last) tc_commit(&bars->v_empty, leader);  // the item's last dP^T is issued
+        // dV_g += P^T dO_g  (TS: P^T packed at SP + hf*64 + [0, 32))
+        mbar_wait(&bars->p_ready, g & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < B / 16; ++kk)
+          mma_ts(tmem + C::kDV, tmem + C::kSP + (kk >> 2) * 64 + (kk & 3) * 8,
+                 desc_sw128(da(g) + kk * 2048, kM * 128, 1024), idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
+        tc_commit(&bars->dv_done, leader);
+        // dK_g += dS^T Q_g  (TS: dS^T packed at SP + hf*64 + [32, 64))
+        mbar_wait(&bars->ds_ready, g & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < B / 16; ++kk)
+          mma_ts(tmem + C::kDK, tmem + C::kSP + (kk >> 2) * 64 + 32 + (kk & 3) * 8,
+                 desc_sw128(qa(g) + kk * 2048, kM * 128, 1024), idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
+        tc_commit(&bars->q_empty[g & 1], leader);
+        // tile A of the next pair (overwrites SP after dV_g / dK_g read it: in-order pipe)
+        if (!last) {
+          issue_st(g + 1);
+          a_issued = true;
+        } else {
+          have_nx = next_item(nx);
+          if (have_nx) {
+            mbar_wait(&bars->v_full, (t + 1) & 1);
+            issue_dpt(g + 1);
+            a_issued = true;
+          }
+        }
+        // dQ_g = dS_g K  (SS: A = dS in the dO_g slot, MN-major; B = K MN-major)
+        mbar_wait(&bars->dsm_ready, g & 1);
+        if (g > 0) mbar_wait(&bars->dq_free, (g - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < B / 16; ++kk)
+          mma_ss(tmem + C::kDQ, desc_sw128(da(g) + kk * 2048, kM * 128, 1024),
+                 desc_sw128(k_addr + kk * 2048, kM * 128, 1024), idesc_dq, kk > 0 ? 1u : 0u, leader);
+        tc_commit(&bars->dq_full, leader);
+        if (last) {
+          tc_commit(&bars->acc_done, leader);
+          tc_commit(&bars->k_empty, leader);
+        }
+      }
+      ++t;
+      w = nx;
+      have = have_nx;
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ math + dQ reduce + dK/dV epilogue
+    setmaxnreg_inc<200>();
+    constexpr int HB = B / 2;
+    const int quarter = warp & 3;
+    const int hf = (warp - 4) >> 2;
+    const int c = quarter * 32 + lane;  // TMEM lane: key row (SP, dV, dK) / query row (dQ)
+    const uint32_t lf = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t sp = tmem + lf + C::kSP + hf * HB;
+    const bool elected = (c == 0);      // one thread per warpgroup issues its TMA reduces
+    int g = 0, t = 0;
+    int prev_h = 0, prev_q0 = 0;
+    // dQ partial of pair gg (query rows = TMEM lanes, this warpgroup's 64 columns) -> fp32 tiles
+    // through this warpgroup's half of the dO_gg slot -> TMA reduce-add into the accumulator.
+    auto reduce_dq = [&](int gg, int h, int q0) {
+      mbar_wait(&bars->dq_full, gg & 1);
+      tc_fence_after();
+      uint32_t v[2][32];
+      tmem_ld32(tmem + lf + C::kDQ + hf * HB, v[0]);
+      tmem_ld32(tmem + lf + C::kDQ + hf * HB + 32, v[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars->dq_free);
+      uint8_t* stg = do_smem + (gg & 1) * C::kTile + hf * (kM * 128);
+#pragma unroll
+      for (int rd = 0; rd < 2; ++rd) {
+        if (rd > 0) {
+          if (elected) bulk_wait_read();
+          named_bar_sync(1 + hf, 128);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<uint4*>(stg + c * 128 + ((u ^ (c & 7)) << 4)) =
+              make_uint4(v[rd][4 * u], v[rd][4 * u + 1], v[rd][4 * u + 2], v[rd][4 * u + 3]);
+        fence_proxy_async_smem();
+        named_bar_sync(1 + hf, 128);
+        if (elected) {
+          tma_reduce_add_3d(&tm_dqacc, stg, hf * HB + rd * 32, h, q0);
+          bulk_commit();
+        }
+      }
+      if (elected) {
+        bulk_wait_read();
+        mbar_arrive(&bars->do_empty[gg & 1]);
+      }
+    };
+    for (int k = 0;; ++k) {
+      const int it = sched::snake_item(order, n_items, grid, cta, k);
+      if (it < 0) break;
+      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+      const int items = w.ne * sg;
+      const int kv0 = w.seq0 + w.jl * B;
+      const int nkv = min(B, w.seq_len - w.jl * B);
+      const int blk0 = w.gj - w.jl;
+      for (int m = 0; m < items; ++m, ++g) {
+        int h, gi;
+        pair_of(w, m, h, gi);
+        const int il = gi - blk0;
+        const int q0 = w.seq0 + il * B;
+        const int nq = min(B, w.seq_len - il * B);
+        // Valid query columns r >= r_lo: r >= key row on the diagonal; none for key rows past the
+        // sequence end (their dS must be 0: dQ sums over every key row of the tile).
+        const int r_lo = c >= nkv ? B : (il == w.jl ? c : 0);
+        uint32_t ta[HB / 32][32], tb[HB / 32][32];
+        mbar_wait(&bars->sp_full, 0);  // tile A (completion 2g: parity 0)
+        tc_fence_after();
+#pragma unroll
+        for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, ta[c2]);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&bars->sp_free);
+        mbar_wait(&bars->sp_full, 1);  // tile B (completion 2g + 1)
+        tc_fence_after();
+#pragma unroll
+        for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, tb[c2]);
+        tmem_wait_ld();
+        // ta <- S^T, tb <- dP^T (an item's first pair arrives as A = dP^T, B = S^T): register
+        // swaps, no dynamic indexing of the register arrays.
+        if (m == 0) {
+#pragma unroll
+          for (int c2 = 0; c2 < HB / 32; ++c2)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const uint32_t x = ta[c2][e];
+              ta[c2][e] = tb[c2][e];
+              tb[c2][e] = x;
+            }
+        }
+        const auto& sv = ta;
+        const auto& dpv = tb;
+        float p[HB];
+        if (r_lo <= hf * HB && nq == B) {
+          dkv_p<HB, false>(sv, scale_log2, hf * HB, 0, B, p);
+        } else {
+          dkv_p<HB, true>(sv, scale_log2, hf * HB, r_lo, nq, p);
+        }
+        {
+          uint32_t pw[2][16];
+#pragma unroll
+          for (int e = 0; e < HB; e += 2) pw[e / 32][(e % 32) / 2] = pack_bf16x2(p[e], p[e + 1]);
+          tmem_st16(sp, pw[0]);
+          tmem_st16(sp + 16, pw[1]);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&bars->p_ready);
+        }
+        uint32_t dsw[HB / 2];
+#pragma unroll
+        for (int e = 0; e < HB; e += 2) {  // dS^T = P^T (dP^T - D): the UMMA already subtracted D
+          const f2 ds = fmul2(mk2(p[e], p[e + 1]),
+                              mk2(__uint_as_float(dpv[e / 32][e % 32]), __uint_as_float(dpv[e / 32][e % 32 + 1])));
+          dsw[e / 2] = pack_bf16x2(ds.x, ds.y);
+        }
+        {
+          uint32_t d0[16], d1[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            d0[e] = dsw[e];
+            d1[e] = dsw[16 + e];
+          }
+          tmem_st16(sp + 32, d0);
+          tmem_st16(sp + 48, d1);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&bars->ds_ready);
+        }
+        if (g > 0) reduce_dq(g - 1, prev_h, prev_q0);
+        // dS (bf16) into the dO_g slot as the MN-major A operand of dQ_g: chunk hf holds query
+        // columns [hf*64, hf*64 + 64) of every key row c (128-byte rows, SW128).
+        mbar_wait(&bars->dv_done, g & 1);
+        uint8_t* dsm = do_smem + (g & 1) * C::kTile + hf * (kM * 128) + c * 128;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<uint4*>(dsm + ((u ^ (c & 7)) << 4)) =
+              make_uint4(dsw[4 * u], dsw[4 * u + 1], dsw[4 * u + 2], dsw[4 * u + 3]);
+        fence_proxy_async_smem();
+        mbar_arrive(&bars->dsm_ready);
+        prev_h = h;
+        prev_q0 = q0;
+      }
+      // Epilogue: dV and dK * scale for the valid key rows (zeros if nobody selected the block).
+      if (items > 0) {
+        mbar_wait(&bars->acc_done, t & 1);
+        tc_fence_after();
+        ++t;
+      }
+      const bool store = c < nkv;
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const uint32_t col = (part == 0 ? C::kDV : C::kDK) + hf * (D / 2);
+        const float mul = part == 0 ? 1.0f : scale;
+        uint16_t* row = (part == 0 ? dv : dk) + (static_cast<size_t>(kv0 + c) * hkv + w.hk) * D + hf * (D / 2);
+#pragma unroll
+        for (int cc = 0; cc < D / 64; ++cc) {
+          uint32_t vv[32];
+          if (items > 0) {
+            tmem_ld32(tmem + lf + col + cc * 32, vv);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) vv[e] = 0u;
+          }
+          if (store) {
+            uint32_t w16[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              w16[e] = pack_bf16x2(__uint_as_float(vv[2 * e]) * mul, __uint_as_float(vv[2 * e + 1]) * mul);
+            store_64B(row + cc * 32, w16);
+          }
+        }
+      }
+      tc_fence_before();  // epilogue TMEM reads precede the next item's first dV / dK (ordered via p_ready)
+    }
+    if (g > 0) reduce_dq(g - 1, prev_h, prev_q0);
+    if (elected) bulk_wait_all();  // every dQ reduce has landed before the kernel ends
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::kCols>(tmem);
+  }
+}
+
+// dQ = bf16(acc * scale): 8 fp32 -> 8 bf16 (one 16-byte store) per thread and step.
+__global__ void __launch_bounds__(256) dq_convert_kernel(const float4* __restrict__ acc, size_t n8, float scale,
+                                                         uint4* __restrict__ dq) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float4 a = __ldg(acc + 2 * i), b = __ldg(acc + 2 * i + 1);
+    dq[i] = make_uint4(pack_bf16x2(a.x * scale, a.y * scale), pack_bf16x2(a.z * scale, a.w * scale),
+                       pack_bf16x2(b.x * scale, b.y * scale), pack_bf16x2(b.z * scale, b.w * scale));
+  }
+}
+
 // ------------------------------------------------------------------------------------ host
 constexpr int kMaxKvCost = 1023;  // longest-first order resolution (costs above share the top bin)
 unsigned long long* g_trace_bwd = nullptr;  // debug timeline buffer (sb_debug_set_trace_bwd)
 unsigned long long* g_trace_dq = nullptr;   // debug timeline buffer (sb_debug_set_trace_dq)
 
 struct BwdWorkspace {
-  size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, order_kv_matched, rec_q, total;
+  size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, order_kv_matched, rec_q, dqacc, total;
   int tp;
 };
 
@@ -1192,16 +1716,20 @@ BwdWorkspace bwd_layout(int total, int nb_total, int hq, int hkv, int hsel, int 
   off = align256(off + static_cast<size_t>(hkv) * nb_total * 4);
   w.rec_q = off;
   off = align256(off + sched::rec_workspace_bytes(hq * nb_total));
+  w.dqacc = off;  // fused path (D = 128): fp32 dQ accumulator [T][Hq][128]
+  off = align256(off + static_cast<size_t>(total) * hq * 128 * 4);
   w.total = off;
   return w;
 }
 
 template <int D, int B>
 void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o,
-                const float* lse, const int32_t* cu, const int32_t* blk_off, int nseq, int total, int nb_total, int hq,
+                const uint16_t* ores, const float* lse, const int32_t* cu, const int32_t* blk_off, int nseq, int total, int nb_total, int hq,
                 int hkv, const int32_t* idx, const int32_t* cnt, int hsel, int k_max, float scale, uint16_t* dq,
-                uint16_t* dk, uint16_t* dv, uint8_t* ws, cudaStream_t st) {
+                uint16_t* dk, uint16_t* dv, uint8_t* ws, cudaStream_t st, bool deterministic) {
   const BwdWorkspace w = bwd_layout(total, nb_total, hq, hkv, hsel, k_max);
+  constexpr bool kFusable = D == 128 && B == 128;
+  const bool fused = kFusable && !deterministic;
   float* lse2 = reinterpret_cast<float*>(ws + w.lse2);
   float* dvec = reinterpret_cast<float*>(ws + w.dvec);
   int32_t* tr_cnt = reinterpret_cast<int32_t*>(ws + w.tr_cnt);
@@ -1210,7 +1738,8 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   const float scale_log2 = scale * kLog2e;
   const int sms = sched::num_sms();
 
-  bwd_prep_kernel<<<dim3(std::max(1, sms * 8 / hq), hq), 256, 0, st>>>(o, d_o, lse, total, hq, D, w.tp, lse2, dvec);
+  bwd_prep_kernel<<<dim3(std::max(1, sms * 8 / hq), hq), 256, 0, st>>>(o, d_o, ores, lse, total, hq, D, w.tp, lse2,
+                                                                         dvec);
   launched("sb_sparse_attn_bwd/prep");
   const int kv_items = hkv * nb_total;
   const int rows_per_kv = hsel / hkv;
@@ -1240,6 +1769,29 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
                                                                    kv_items, grid_kv, matched);
     launched("sb_sparse_attn_bwd/order_kv_match");
     order_kv = matched;
+  }
+  if constexpr (kFusable) {
+    if (fused) {
+      float* dqacc = reinterpret_cast<float*>(ws + w.dqacc);
+      cuda_check(cudaMemsetAsync(dqacc, 0, static_cast<size_t>(total) * hq * D * 4, st), "sb_sparse_attn_bwd: dQ acc");
+      const CUtensorMap tq = make_thd_map(q, total, hq, D, kM);
+      const CUtensorMap tdo = make_thd_map(d_o, total, hq, D, kM);
+      const CUtensorMap tk = make_thd_map(k, total, hkv, D, kM);
+      const CUtensorMap tv = make_thd_map(v, total, hkv, D, kM);
+      const CUtensorMap tacc = make_thd_map_f32(dqacc, total, hq, D, kM);
+      cuda_check(cudaFuncSetAttribute(attn_bwd_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      FusedCfg::kSmemBytes),
+                 "sb_sparse_attn_bwd: smem attribute (fused)");
+      attn_bwd_fused_kernel<<<std::min(kv_items, sms), kFusedThreads, FusedCfg::kSmemBytes, st>>>(
+          tq, tk, tv, tdo, tacc, cu, blk_off, nseq, hq, hkv, hsel, tr_off, tr_ent, lse2, dvec, w.tp, scale, scale_log2,
+          dk, dv, order_kv, kv_items);
+      launched("sb_sparse_attn_bwd/fused");
+      const size_t n8 = static_cast<size_t>(total) * hq * D / 8;
+      dq_convert_kernel<<<std::max(1, std::min<int>(sms * 8, static_cast<int>((n8 + 255) / 256))), 256, 0, st>>>(
+          reinterpret_cast<const float4*>(dqacc), n8, scale, reinterpret_cast<uint4*>(dq));
+      launched("sb_sparse_attn_bwd/dq_convert");
+      return;
+    }
   }
   const int q_items = hq * nb_total;
   const int32_t* order_q = sched::build_order(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, q_items,
@@ -1297,11 +1849,11 @@ SB_API size_t sb_sparse_attn_bwd_workspace_size(int total_tokens, int nb_total, 
   return sbk::bwd_layout(total_tokens, nb_total, hq, hkv, hsel, k_max).total;
 }
 
-SB_API int sb_sparse_attn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o,
-                              const uint16_t* d_o, const float* lse, const int32_t* cu_seqlens, const int32_t* blk_off,
-                              int nseq, int total_tokens, int nb_total, int hq, int hkv, int head_dim, int block_size,
-                              const int32_t* idx, const int32_t* cnt, int hsel, int k_max, float scale, uint16_t* dq,
-                              uint16_t* dk, uint16_t* dv, void* workspace, void* stream) {
+SB_API int sb_sparse_attn_bwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o,
+                                 const uint16_t* o_res, const uint16_t* d_o, const float* lse, const int32_t* cu_seqlens, const int32_t* blk_off,
+                                 int nseq, int total_tokens, int nb_total, int hq, int hkv, int head_dim, int block_size,
+                                 const int32_t* idx, const int32_t* cnt, int hsel, int k_max, float scale, uint16_t* dq,
+                                 uint16_t* dk, uint16_t* dv, void* workspace, void* stream, int flags) {
   return sbk::abi_call([&] {
     sbk::require(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128");
     sbk::require(block_size == 64 || block_size == 128, "block_size must be 64 or 128");
@@ -1309,23 +1861,35 @@ SB_API int sb_sparse_attn_bwd(const uint16_t* q, const uint16_t* k, const uint16
     sbk::require(hsel >= hkv && hq % hsel == 0 && hsel % hkv == 0,
                  "hsel must divide hq and be a multiple of hkv (each selection row maps to one kv head)");
     sbk::require(k_max >= 1, "k_max must be >= 1");
+    sbk::require((flags & ~SB_BWD_DETERMINISTIC) == 0, "unknown flags");
     if (nseq == 0 || nb_total == 0 || total_tokens == 0) return;
     sbk::require(q && k && v && o && d_o && lse && cu_seqlens && blk_off && idx && cnt && dq && dk && dv && workspace,
                  "null pointer");
     sbk::require((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
                   reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(d_o) | reinterpret_cast<uintptr_t>(dq) |
-                  reinterpret_cast<uintptr_t>(dk) | reinterpret_cast<uintptr_t>(dv)) % 16 == 0,
-                 "q/k/v/o/dO/dQ/dK/dV must be 16-byte aligned");
+                  reinterpret_cast<uintptr_t>(dk) | reinterpret_cast<uintptr_t>(dv) |
+                  reinterpret_cast<uintptr_t>(workspace) | reinterpret_cast<uintptr_t>(o_res)) % 16 == 0,
+                 "q/k/v/o/o_res/dO/dQ/dK/dV/workspace must be 16-byte aligned");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint8_t* ws = static_cast<uint8_t*>(workspace);
+    const bool det = (flags & SB_BWD_DETERMINISTIC) != 0;
 #define SB_BWD_CASE(DD, BB)                                                                                     \
   if (head_dim == DD && block_size == BB)                                                                       \
-    return sbk::launch_bwd<DD, BB>(q, k, v, o, d_o, lse, cu_seqlens, blk_off, nseq, total_tokens, nb_total, hq, \
-                                   hkv, idx, cnt, hsel, k_max, scale, dq, dk, dv, ws, st);
+    return sbk::launch_bwd<DD, BB>(q, k, v, o, d_o, o_res, lse, cu_seqlens, blk_off, nseq, total_tokens, nb_total, hq, \
+                                   hkv, idx, cnt, hsel, k_max, scale, dq, dk, dv, ws, st, det);
     SB_BWD_CASE(128, 128)
     SB_BWD_CASE(128, 64)
     SB_BWD_CASE(64, 128)
     SB_BWD_CASE(64, 64)
 #undef SB_BWD_CASE
   });
+}
+
+SB_API int sb_sparse_attn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o,
+                              const uint16_t* d_o, const float* lse, const int32_t* cu_seqlens, const int32_t* blk_off,
+                              int nseq, int total_tokens, int nb_total, int hq, int hkv, int head_dim, int block_size,
+                              const int32_t* idx, const int32_t* cnt, int hsel, int k_max, float scale, uint16_t* dq,
+                              uint16_t* dk, uint16_t* dv, void* workspace, void* stream) {
+  return sb_sparse_attn_bwd_ex(q, k, v, o, nullptr, d_o, lse, cu_seqlens, blk_off, nseq, total_tokens, nb_total, hq, hkv,
+                               head_dim, block_size, idx, cnt, hsel, k_max, scale, dq, dk, dv, workspace, stream, 0);
 }

@@ -144,9 +144,9 @@ template <int D, int B>
 __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-    const int32_t* __restrict__ blk_off, int nseq, int total_tokens,
+    const __grid_constant__ CUtensorMap tm_ores, const int32_t* __restrict__ blk_off, int nseq, int total_tokens,
     int hq, int hkv, const int32_t* __restrict__ idx, int k_max, float scale_log2, uint16_t* __restrict__ out,
-    float* __restrict__ lse, const sched::ItemRec* __restrict__ recs, int n_items,
+    uint16_t* __restrict__ ores, float* __restrict__ lse, const sched::ItemRec* __restrict__ recs, int n_items,
     unsigned long long* __restrict__ trace) {
   using C = Fwd2Cfg<D, B>;
   // Debug timeline: CTA 0, per stream s and block g < 256: [s][g][slot] (slots: 0 QK issued,
@@ -292,6 +292,10 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
         if (store) {
           uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<size_t>(row0 + r) * hq + w.h) * D);
           for (int e = 0; e < D / 8; ++e) dst[e] = make_uint4(0, 0, 0, 0);
+          if (ores != nullptr) {
+            uint4* dr = reinterpret_cast<uint4*>(ores + (static_cast<size_t>(row0 + r) * hq + w.h) * D);
+            for (int e = 0; e < D / 8; ++e) dr[e] = make_uint4(0, 0, 0, 0);
+          }
           lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = -INFINITY;
         }
         continue;
@@ -343,6 +347,9 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bars->o_free[s]);  // O may be overwritten by the stream's next item
+      // O (and, when ores != nullptr, its bf16 rounding residual bf16(O - bf16(O)), from which the
+      // backward forms D = rowsum(dO * O) to ~2^-16 instead of bf16 precision).
+      const int parts = ores != nullptr ? 2 : 1;
       if (nrows == B) {
         // Full tile: one 64-column chunk at a time through the stream's SW128 staging slot and
         // a TMA store issued by thread r == 0 of the warpgroup (the slot is reused once the
@@ -350,37 +357,50 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
         uint8_t* stg = o_stage + s * C::kStageBytes;
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          if (r == 0) bulk_wait_read();
-          named_bar_sync(1 + s, 128);
-          if (r < B) {
+          for (int part = 0; part < parts; ++part) {
+            if (r == 0) bulk_wait_read();
+            named_bar_sync(1 + s, 128);
+            if (r < B) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int d0 = c * 64 + u * 8;
-              uint4 q4;
-              q4.x = pack_bf16x2(__uint_as_float(v[d0 / 32][d0 % 32]) * inv_l, __uint_as_float(v[d0 / 32][d0 % 32 + 1]) * inv_l);
-              q4.y = pack_bf16x2(__uint_as_float(v[d0 / 32][d0 % 32 + 2]) * inv_l, __uint_as_float(v[d0 / 32][d0 % 32 + 3]) * inv_l);
-              q4.z = pack_bf16x2(__uint_as_float(v[d0 / 32][d0 % 32 + 4]) * inv_l, __uint_as_float(v[d0 / 32][d0 % 32 + 5]) * inv_l);
-              q4.w = pack_bf16x2(__uint_as_float(v[d0 / 32][d0 % 32 + 6]) * inv_l, __uint_as_float(v[d0 / 32][d0 % 32 + 7]) * inv_l);
-              *reinterpret_cast<uint4*>(stg + r * 128 + ((u ^ (r & 7)) << 4)) = q4;
+              for (int u = 0; u < 8; ++u) {
+                const int d0 = c * 64 + u * 8;
+                float x[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  x[e] = __uint_as_float(v[(d0 + e) / 32][(d0 + e) % 32]) * inv_l;
+                  if (part) x[e] -= __bfloat162float(__float2bfloat16_rn(x[e]));
+                }
+                *reinterpret_cast<uint4*>(stg + r * 128 + ((u ^ (r & 7)) << 4)) =
+                    make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]),
+                               pack_bf16x2(x[6], x[7]));
+              }
             }
-          }
-          fence_proxy_async_smem();
-          named_bar_sync(1 + s, 128);
-          if (r == 0) {
-            tma_store_3d(&tm_o, stg, c * 64, w.h, row0);
-            bulk_commit();
+            fence_proxy_async_smem();
+            named_bar_sync(1 + s, 128);
+            if (r == 0) {
+              tma_store_3d(part ? &tm_ores : &tm_o, stg, c * 64, w.h, row0);
+              bulk_commit();
+            }
           }
         }
         if (store) lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = (m_run + log2f(l_run)) * 0.69314718055994531f;
       } else if (store) {  // the last (partial) tile of a sequence: a box would cross into the next
-        uint16_t* orow = out + (static_cast<size_t>(row0 + r) * hq + w.h) * D;
+        for (int part = 0; part < parts; ++part) {
+          uint16_t* orow = (part ? ores : out) + (static_cast<size_t>(row0 + r) * hq + w.h) * D;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t w16[16];
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t w16[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            w16[e] = pack_bf16x2(__uint_as_float(v[c][2 * e]) * inv_l, __uint_as_float(v[c][2 * e + 1]) * inv_l);
-          store_64B(orow + c * 32, w16);
+            for (int e = 0; e < 16; ++e) {
+              float a = __uint_as_float(v[c][2 * e]) * inv_l, b = __uint_as_float(v[c][2 * e + 1]) * inv_l;
+              if (part) {
+                a -= __bfloat162float(__float2bfloat16_rn(a));
+                b -= __bfloat162float(__float2bfloat16_rn(b));
+              }
+              w16[e] = pack_bf16x2(a, b);
+            }
+            store_64B(orow + c * 32, w16);
+          }
         }
         lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = (m_run + log2f(l_run)) * 0.69314718055994531f;
       }
@@ -402,7 +422,7 @@ unsigned long long* g_trace = nullptr;  // debug timeline buffer (sb_debug_set_t
 template <int D, int B>
 void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* cu, const int32_t* blk_off,
                 int nseq, int total, int nb_total, int hq, int hkv, const int32_t* idx, const int32_t* cnt, int hsel,
-                int k_max, float scale, uint16_t* o, float* lse, void* ws, cudaStream_t st) {
+                int k_max, float scale, uint16_t* o, uint16_t* ores, float* lse, void* ws, cudaStream_t st) {
   const int n_items = hq * nb_total;
   const int32_t* order = sched::build_order(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, n_items, ws, st,
                                             "sb_sparse_attn_fwd/order");
@@ -415,13 +435,14 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
   const CUtensorMap tk = make_thd_map(k, total, hkv, D, B);
   const CUtensorMap tv = make_thd_map(v, total, hkv, D, B);
   const CUtensorMap to = make_thd_map(o, total, hq, D, B);
+  const CUtensorMap tores = make_thd_map(ores != nullptr ? ores : o, total, hq, D, B);
   const int grid = std::min(n_items, sched::num_sms());
   using C2 = Fwd2Cfg<D, B>;
   auto k2 = attn_fwd2_kernel<D, B>;
   cuda_check(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::kSmemBytes),
              "sb_sparse_attn_fwd: smem attribute");
-  k2<<<grid, kThreads2, C2::kSmemBytes, st>>>(tq, tk, tv, to, blk_off, nseq, total, hq, hkv, idx, k_max,
-                                              scale * 1.4426950408889634f, o, lse, recs, n_items, g_trace);
+  k2<<<grid, kThreads2, C2::kSmemBytes, st>>>(tq, tk, tv, to, tores, blk_off, nseq, total, hq, hkv, idx, k_max,
+                                              scale * 1.4426950408889634f, o, ores, lse, recs, n_items, g_trace);
   launched("sb_sparse_attn_fwd");
 }
 
@@ -436,10 +457,11 @@ SB_API size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq, int k_max)
          sbk::sched::rec_workspace_bytes(nb_total * hq);
 }
 
-SB_API int sb_sparse_attn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* cu_seqlens,
-                              const int32_t* blk_off, int nseq, int total_tokens, int nb_total, int hq, int hkv,
-                              int head_dim, int block_size, const int32_t* idx, const int32_t* cnt, int hsel,
-                              int k_max, float scale, uint16_t* o, float* lse, void* workspace, void* stream) {
+SB_API int sb_sparse_attn_fwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* cu_seqlens,
+                                 const int32_t* blk_off, int nseq, int total_tokens, int nb_total, int hq, int hkv,
+                                 int head_dim, int block_size, const int32_t* idx, const int32_t* cnt, int hsel,
+                                 int k_max, float scale, uint16_t* o, uint16_t* o_res, float* lse, void* workspace,
+                                 void* stream) {
   return sbk::abi_call([&] {
     sbk::require(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128");
     sbk::require(block_size == 64 || block_size == 128, "block_size must be 64 or 128");
@@ -449,17 +471,26 @@ SB_API int sb_sparse_attn_fwd(const uint16_t* q, const uint16_t* k, const uint16
     sbk::require(k_max >= 1, "k_max must be >= 1");
     if (nseq == 0 || nb_total == 0 || total_tokens == 0) return;
     sbk::require(q && k && v && cu_seqlens && blk_off && idx && cnt && o && lse && workspace, "null pointer");
-    sbk::require((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) % 16 == 0,
-                 "q/k/v must be 16-byte aligned");
+    sbk::require((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+                  reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(o_res)) % 16 == 0,
+                 "q/k/v/o/o_res must be 16-byte aligned");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define SB_FWD_CASE(DD, BB)                                                                                      \
   if (head_dim == DD && block_size == BB)                                                                        \
     return sbk::launch_fwd<DD, BB>(q, k, v, cu_seqlens, blk_off, nseq, total_tokens, nb_total, hq, hkv, idx, cnt, \
-                                   hsel, k_max, scale, o, lse, workspace, st);
+                                   hsel, k_max, scale, o, o_res, lse, workspace, st);
     SB_FWD_CASE(128, 128)
     SB_FWD_CASE(128, 64)
     SB_FWD_CASE(64, 128)
     SB_FWD_CASE(64, 64)
 #undef SB_FWD_CASE
   });
+}
+
+SB_API int sb_sparse_attn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* cu_seqlens,
+                              const int32_t* blk_off, int nseq, int total_tokens, int nb_total, int hq, int hkv,
+                              int head_dim, int block_size, const int32_t* idx, const int32_t* cnt, int hsel,
+                              int k_max, float scale, uint16_t* o, float* lse, void* workspace, void* stream) {
+  return sb_sparse_attn_fwd_ex(q, k, v, cu_seqlens, blk_off, nseq, total_tokens, nb_total, hq, hkv, head_dim,
+                               block_size, idx, cnt, hsel, k_max, scale, o, nullptr, lse, workspace, stream);
 }

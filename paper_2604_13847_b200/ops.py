@@ -40,9 +40,13 @@ def _lib():
             "sb_sparse_attn_fwd_workspace_size": (sz, [i, i, i]),
             "sb_sparse_attn_fwd": (i, [_vp, _vp, _vp, _vp, _vp, i, i, i, i, i, i, i, _vp, _vp, i, i, f, _vp, _vp,
                                        _vp, _vp]),
+            "sb_sparse_attn_fwd_ex": (i, [_vp, _vp, _vp, _vp, _vp, i, i, i, i, i, i, i, _vp, _vp, i, i, f, _vp, _vp,
+                                          _vp, _vp, _vp]),
             "sb_sparse_attn_bwd_workspace_size": (sz, [i, i, i, i, i, i, i]),
             "sb_sparse_attn_bwd": (i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, i, i, i, i, i, i, i, _vp, _vp, i, i,
                                        f, _vp, _vp, _vp, _vp, _vp]),
+            "sb_sparse_attn_bwd_ex": (i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, i, i, i, i, i, i, i, _vp, _vp,
+                                          i, i, f, _vp, _vp, _vp, _vp, _vp, i]),
             "sb_launch_count": (C.c_uint64, []),
             "sb_last_error": (C.c_char_p, []),
         }
@@ -256,8 +260,10 @@ def dst_decide(profile: torch.Tensor, lay: VarlenLayout, mb_off: torch.Tensor, k
     return k_final, drop, k_seq
 
 
-def sparse_attn_fwd(q, k, v, lay: VarlenLayout, idx, cnt, scale: float | None = None):
-    """K5: (O [T, Hq, D] bf16, LSE [Hq, T] fp32 natural log)."""
+def sparse_attn_fwd(q, k, v, lay: VarlenLayout, idx, cnt, scale: float | None = None, residual: bool = True):
+    """K5: (O [T, Hq, D] bf16, LSE [Hq, T] fp32 natural log). With residual (default) the kernel also
+    writes O's bf16 rounding residual, attached as `lse.o_res`; sparse_attn_bwd then forms
+    D = rowsum(dO * O) from O + residual (accurate dQ on rows that attend few keys)."""
     _need_cuda(q, k, v, idx, cnt)
     _need_qkv(q, k, v, lay)
     _need_sel(idx, cnt, lay)
@@ -266,17 +272,25 @@ def sparse_attn_fwd(q, k, v, lay: VarlenLayout, idx, cnt, scale: float | None = 
     hsel, _, k_max = idx.shape
     scale = 1.0 / math.sqrt(D) if scale is None else scale
     o = torch.empty_like(q)
+    o_res = torch.empty_like(q) if residual else None
     lse = torch.empty((Hq, T), dtype=torch.float32, device=q.device)
     ws = torch.empty(max(16, int(_lib().sb_sparse_attn_fwd_workspace_size(lay.nb_total, Hq, k_max))),
                      dtype=torch.uint8, device=q.device)
-    _call("sb_sparse_attn_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(lay.cu_seqlens), _ptr(lay.blk_off), lay.nseq, T,
+    _call("sb_sparse_attn_fwd_ex", _ptr(q), _ptr(k), _ptr(v), _ptr(lay.cu_seqlens), _ptr(lay.blk_off), lay.nseq, T,
           lay.nb_total, Hq, Hkv, D, lay.block_size, _ptr(idx), _ptr(cnt), hsel, k_max, C.c_float(scale), _ptr(o),
-          _ptr(lse), _ptr(ws), _stream())
+          _ptr(o_res), _ptr(lse), _ptr(ws), _stream())
+    if o_res is not None:
+        lse.o_res = o_res
     return o, lse
 
 
-def sparse_attn_bwd(q, k, v, o, do, lse, lay: VarlenLayout, idx, cnt, scale: float | None = None):
-    """K6: (dQ, dK, dV) bf16."""
+SB_BWD_DETERMINISTIC = 1
+
+
+def sparse_attn_bwd(q, k, v, o, do, lse, lay: VarlenLayout, idx, cnt, scale: float | None = None,
+                    deterministic: bool = False, o_res=None):
+    """K6: (dQ, dK, dV) bf16. Default: the fused single pass for d = B = 128 (dQ reduce-added in
+    fp32, reproducible to summation order); deterministic=True: the bit-deterministic two-pass."""
     _need_cuda(q, k, v, o, do, lse, idx, cnt)
     _need_qkv(q, k, v, lay)
     _need_sel(idx, cnt, lay)
@@ -284,6 +298,10 @@ def sparse_attn_bwd(q, k, v, o, do, lse, lay: VarlenLayout, idx, cnt, scale: flo
     _need(o, "o", torch.bfloat16, 3, tuple(q.shape))
     _need(do, "do", torch.bfloat16, 3, tuple(q.shape))
     _need(lse, "lse", torch.float32, 2, (q.shape[1], q.shape[0]))
+    o_res = o_res if o_res is not None else getattr(lse, "o_res", None)
+    if o_res is not None:
+        _need_cuda(o_res)
+        _need(o_res, "o_res", torch.bfloat16, 3, tuple(q.shape))
     T, Hq, D = q.shape
     Hkv = k.shape[1]
     hsel, _, k_max = idx.shape
@@ -291,9 +309,10 @@ def sparse_attn_bwd(q, k, v, o, do, lse, lay: VarlenLayout, idx, cnt, scale: flo
     ws_bytes = int(_lib().sb_sparse_attn_bwd_workspace_size(T, lay.nb_total, Hq, Hkv, D, hsel, k_max))
     ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=q.device)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-    _call("sb_sparse_attn_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(do), _ptr(lse),
+    _call("sb_sparse_attn_bwd_ex", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(o_res), _ptr(do), _ptr(lse),
           _ptr(lay.cu_seqlens), _ptr(lay.blk_off), lay.nseq, T, lay.nb_total, Hq, Hkv, D, lay.block_size, _ptr(idx),
-          _ptr(cnt), hsel, k_max, C.c_float(scale), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), _stream())
+          _ptr(cnt), hsel, k_max, C.c_float(scale), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), _stream(),
+          SB_BWD_DETERMINISTIC if deterministic else 0)
     return dq, dk, dv
 
 
@@ -301,18 +320,18 @@ class SparseAttention(torch.autograd.Function):
     """Autograd wrapper: forward = K5, backward = K6 (recompute from the saved LSE)."""
 
     @staticmethod
-    def forward(ctx, q, k, v, lay, idx, cnt, scale):
+    def forward(ctx, q, k, v, lay, idx, cnt, scale, deterministic=False):
         o, lse = sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
         ctx.save_for_backward(q, k, v, o, lse, idx, cnt)
-        ctx.lay, ctx.scale = lay, scale
+        ctx.lay, ctx.scale, ctx.deterministic = lay, scale, deterministic
         return o
 
     @staticmethod
     def backward(ctx, do):
         q, k, v, o, lse, idx, cnt = ctx.saved_tensors
-        dq, dk, dv = sparse_attn_bwd(q, k, v, o, do, lse, ctx.lay, idx, cnt, ctx.scale)
-        return dq, dk, dv, None, None, None, None
+        dq, dk, dv = sparse_attn_bwd(q, k, v, o, do, lse, ctx.lay, idx, cnt, ctx.scale, ctx.deterministic)
+        return dq, dk, dv, None, None, None, None, None
 
 
-def sparse_attention(q, k, v, lay, idx, cnt, scale=None):
-    return SparseAttention.apply(q, k, v, lay, idx, cnt, scale)
+def sparse_attention(q, k, v, lay, idx, cnt, scale=None, deterministic=False):
+    return SparseAttention.apply(q, k, v, lay, idx, cnt, scale, deterministic)

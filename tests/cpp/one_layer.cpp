@@ -150,13 +150,14 @@ int main() {
   int64_t* dtri = dev_copy(tri);
   float *qbar, *kbar, *S, *lse;
   int32_t *idx, *cnt;
-  uint16_t *o, *gq, *gk, *gv;
+  uint16_t *o, *ores, *gq, *gk, *gv;
   CK(cudaMalloc(&qbar, size_t(nbt) * Hq * D * 4));
   CK(cudaMalloc(&kbar, size_t(nbt) * Hkv * D * 4));
   CK(cudaMalloc(&S, size_t(Hq) * std::max<int64_t>(1, trit) * 4));
   CK(cudaMalloc(&idx, size_t(Hq) * nbt * k_max * 4));
   CK(cudaMalloc(&cnt, size_t(Hq) * nbt * 4));
   CK(cudaMalloc(&o, q.size() * 2));
+  CK(cudaMalloc(&ores, q.size() * 2));
   CK(cudaMalloc(&lse, size_t(Hq) * T * 4));
   CK(cudaMalloc(&gq, q.size() * 2));
   CK(cudaMalloc(&gk, k.size() * 2));
@@ -170,10 +171,10 @@ int main() {
   SB(sb_block_pool(dk_in, dcu, dblk, nseq, nbt, Hkv, D, kBlock, kbar, st));
   SB(sb_block_scores(qbar, kbar, dblk, dtri, nseq, nbm, Hq, Hkv, D, scale, S, st));
   SB(sb_topk_select(S, dblk, dtri, nseq, nbt, nbm, Hq, 1, dks, k_max, 1, idx, cnt, st));
-  SB(sb_sparse_attn_fwd(dq_in, dk_in, dv_in, dcu, dblk, nseq, T, nbt, Hq, Hkv, D, kBlock, idx, cnt, Hq, k_max, scale,
-                        o, lse, wf, st));
-  SB(sb_sparse_attn_bwd(dq_in, dk_in, dv_in, o, ddo, lse, dcu, dblk, nseq, T, nbt, Hq, Hkv, D, kBlock, idx, cnt, Hq,
-                        k_max, scale, gq, gk, gv, wb, st));
+  SB(sb_sparse_attn_fwd_ex(dq_in, dk_in, dv_in, dcu, dblk, nseq, T, nbt, Hq, Hkv, D, kBlock, idx, cnt, Hq, k_max,
+                           scale, o, ores, lse, wf, st));
+  SB(sb_sparse_attn_bwd_ex(dq_in, dk_in, dv_in, o, ores, ddo, lse, dcu, dblk, nseq, T, nbt, Hq, Hkv, D, kBlock, idx, cnt,
+                           Hq, k_max, scale, gq, gk, gv, wb, st, 0));
   CK(cudaStreamSynchronize(st));
 
   // ---- oracle checks
