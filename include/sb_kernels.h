@@ -106,6 +106,10 @@ int sb_dst_decide(const double* profile, const int32_t* blk_off, const int32_t* 
  * (workspace: sb_sparse_attn_fwd_workspace_size() bytes for the work order).
  * Replaces: predict()-based attention latency in micro_batch_time (reference sim.cpp:88-98). */
 size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq, int k_max);
+/* Workspace for any block size, including 256 (the paper's MoBA B = 256): a
+ * B = 256 selection runs on the B = 128 kernels through an exact re-expression over 128-row /
+ * 128-key sub-tiles (expand256.cu), whose index lists live in this workspace. */
+size_t sb_sparse_attn_fwd_workspace_size_ex(int nseq, int nb_total, int hq, int hsel, int k_max, int block_size);
 int sb_sparse_attn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                        const int32_t* cu_seqlens, const int32_t* blk_off, int nseq, int total_tokens,
                        int nb_total, int hq, int hkv, int head_dim, int block_size,
@@ -127,6 +131,8 @@ int sb_sparse_attn_fwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* 
  * Replaces: fwd_bwd_ratio (reference sim.hpp:23, sim.cpp:97). */
 size_t sb_sparse_attn_bwd_workspace_size(int total_tokens, int nb_total, int hq, int hkv,
                                          int head_dim, int hsel, int k_max);
+size_t sb_sparse_attn_bwd_workspace_size_ex(int nseq, int total_tokens, int nb_total, int hq, int hkv,
+                                            int head_dim, int hsel, int k_max, int block_size);
 int sb_sparse_attn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                        const uint16_t* o, const uint16_t* d_o, const float* lse,
                        const int32_t* cu_seqlens, const int32_t* blk_off, int nseq,

@@ -1849,6 +1849,13 @@ SB_API size_t sb_sparse_attn_bwd_workspace_size(int total_tokens, int nb_total, 
   return sbk::bwd_layout(total_tokens, nb_total, hq, hkv, hsel, k_max).total;
 }
 
+SB_API size_t sb_sparse_attn_bwd_workspace_size_ex(int nseq, int total_tokens, int nb_total, int hq, int hkv,
+                                                   int head_dim, int hsel, int k_max, int block_size) {
+  if (block_size != 256) return sb_sparse_attn_bwd_workspace_size(total_tokens, nb_total, hq, hkv, head_dim, hsel, k_max);
+  return sbk::expand256_workspace_bytes(nseq, nb_total, hsel, k_max) +
+         sbk::bwd_layout(total_tokens, 2 * nb_total, hq, hkv, hsel, 2 * k_max).total;
+}
+
 SB_API int sb_sparse_attn_bwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o,
                                  const uint16_t* o_res, const uint16_t* d_o, const float* lse, const int32_t* cu_seqlens, const int32_t* blk_off,
                                  int nseq, int total_tokens, int nb_total, int hq, int hkv, int head_dim, int block_size,
@@ -1856,7 +1863,7 @@ SB_API int sb_sparse_attn_bwd_ex(const uint16_t* q, const uint16_t* k, const uin
                                  uint16_t* dk, uint16_t* dv, void* workspace, void* stream, int flags) {
   return sbk::abi_call([&] {
     sbk::require(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128");
-    sbk::require(block_size == 64 || block_size == 128, "block_size must be 64 or 128");
+    sbk::require(block_size == 64 || block_size == 128 || block_size == 256, "block_size must be 64, 128 or 256");
     sbk::require(hq >= 1 && hkv >= 1 && hq % hkv == 0, "hq must be a positive multiple of hkv");
     sbk::require(hsel >= hkv && hq % hsel == 0 && hsel % hkv == 0,
                  "hsel must divide hq and be a multiple of hkv (each selection row maps to one kv head)");
@@ -1873,6 +1880,17 @@ SB_API int sb_sparse_attn_bwd_ex(const uint16_t* q, const uint16_t* k, const uin
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     const bool det = (flags & SB_BWD_DETERMINISTIC) != 0;
+    if (block_size == 256) {  // workspace: sb_sparse_attn_bwd_workspace_size_ex
+      const sbk::Expanded256 e =
+          sbk::expand_selection_256(cu_seqlens, blk_off, nseq, nb_total, hsel, idx, cnt, k_max, ws, st);
+      if (head_dim == 128)
+        return sbk::launch_bwd<128, 128>(q, k, v, o, d_o, o_res, lse, cu_seqlens, e.blk_off, nseq, total_tokens,
+                                         e.nb_total, hq, hkv, e.idx, e.cnt, hsel, e.k_max, scale, dq, dk, dv,
+                                         ws + e.used, st, det);
+      return sbk::launch_bwd<64, 128>(q, k, v, o, d_o, o_res, lse, cu_seqlens, e.blk_off, nseq, total_tokens,
+                                      e.nb_total, hq, hkv, e.idx, e.cnt, hsel, e.k_max, scale, dq, dk, dv, ws + e.used,
+                                      st, det);
+    }
 #define SB_BWD_CASE(DD, BB)                                                                                     \
   if (head_dim == DD && block_size == BB)                                                                       \
     return sbk::launch_bwd<DD, BB>(q, k, v, o, d_o, o_res, lse, cu_seqlens, blk_off, nseq, total_tokens, nb_total, hq, \

@@ -457,6 +457,12 @@ SB_API size_t sb_sparse_attn_fwd_workspace_size(int nb_total, int hq, int k_max)
          sbk::sched::rec_workspace_bytes(nb_total * hq);
 }
 
+SB_API size_t sb_sparse_attn_fwd_workspace_size_ex(int nseq, int nb_total, int hq, int hsel, int k_max, int block_size) {
+  if (block_size != 256) return sb_sparse_attn_fwd_workspace_size(nb_total, hq, k_max);
+  return sbk::expand256_workspace_bytes(nseq, nb_total, hsel, k_max) +
+         sb_sparse_attn_fwd_workspace_size(2 * nb_total, hq, 2 * k_max);
+}
+
 SB_API int sb_sparse_attn_fwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* cu_seqlens,
                                  const int32_t* blk_off, int nseq, int total_tokens, int nb_total, int hq, int hkv,
                                  int head_dim, int block_size, const int32_t* idx, const int32_t* cnt, int hsel,
@@ -464,13 +470,24 @@ SB_API int sb_sparse_attn_fwd_ex(const uint16_t* q, const uint16_t* k, const uin
                                  void* stream) {
   return sbk::abi_call([&] {
     sbk::require(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128");
-    sbk::require(block_size == 64 || block_size == 128, "block_size must be 64 or 128");
+    sbk::require(block_size == 64 || block_size == 128 || block_size == 256, "block_size must be 64, 128 or 256");
     sbk::require(hq >= 1 && hkv >= 1 && hq % hkv == 0, "hq must be a positive multiple of hkv");
     sbk::require(hsel >= hkv && hq % hsel == 0 && hsel % hkv == 0,
                  "hsel must divide hq and be a multiple of hkv (each selection row maps to one kv head)");
     sbk::require(k_max >= 1, "k_max must be >= 1");
     if (nseq == 0 || nb_total == 0 || total_tokens == 0) return;
     sbk::require(q && k && v && cu_seqlens && blk_off && idx && cnt && o && lse && workspace, "null pointer");
+    if (block_size == 256) {  // workspace: sb_sparse_attn_fwd_workspace_size_ex
+      const cudaStream_t st256 = static_cast<cudaStream_t>(stream);
+      const sbk::Expanded256 e = sbk::expand_selection_256(cu_seqlens, blk_off, nseq, nb_total, hsel, idx, cnt, k_max,
+                                                           static_cast<uint8_t*>(workspace), st256);
+      void* ws128 = static_cast<uint8_t*>(workspace) + e.used;
+      if (head_dim == 128)
+        return sbk::launch_fwd<128, 128>(q, k, v, cu_seqlens, e.blk_off, nseq, total_tokens, e.nb_total, hq, hkv,
+                                         e.idx, e.cnt, hsel, e.k_max, scale, o, o_res, lse, ws128, st256);
+      return sbk::launch_fwd<64, 128>(q, k, v, cu_seqlens, e.blk_off, nseq, total_tokens, e.nb_total, hq, hkv, e.idx,
+                                      e.cnt, hsel, e.k_max, scale, o, o_res, lse, ws128, st256);
+    }
     sbk::require((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
                   reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(o_res)) % 16 == 0,
                  "q/k/v/o/o_res must be 16-byte aligned");

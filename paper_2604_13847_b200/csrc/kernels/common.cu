@@ -24,7 +24,7 @@ SB_API int sb_block_layout_host(const int32_t* cu, int nseq, int block_size, int
   return sbk::abi_call([&] {
     sbk::require(cu != nullptr && blk_off != nullptr && tri_off != nullptr, "null pointer");
     sbk::require(nseq >= 0, "nseq must be >= 0");
-    sbk::require(block_size == 64 || block_size == 128, "block_size must be 64 or 128");
+    sbk::require(block_size == 64 || block_size == 128 || block_size == 256, "block_size must be 64, 128 or 256");
     sbk::require(nseq == 0 || cu[0] == 0, "cu_seqlens[0] must be 0");
     blk_off[0] = 0;
     tri_off[0] = 0;

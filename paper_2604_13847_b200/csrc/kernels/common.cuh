@@ -74,6 +74,19 @@ __device__ __forceinline__ void store_64B(void* dst, const uint32_t (&w)[16]) {
   }
 }
 
+// Block size 256 on the B = 128 kernels (expand256.cu): the selection re-expressed over a padded
+// 128 layout (blk_off = 2 x the 256 one), nb_total and k_max doubled.
+struct Expanded256 {
+  int32_t* blk_off;
+  int32_t* idx;
+  int32_t* cnt;
+  int nb_total, k_max;
+  size_t used;  // workspace bytes taken from the front
+};
+size_t expand256_workspace_bytes(int nseq, int nb256, int hsel, int k_max);
+Expanded256 expand_selection_256(const int32_t* cu, const int32_t* blk_off256, int nseq, int nb256, int hsel,
+                                 const int32_t* idx, const int32_t* cnt, int k_max, uint8_t* ws, cudaStream_t st);
+
 // Sequence owning global block gi (binary search in blk_off[0..nseq]).
 __device__ __forceinline__ int seq_of_block(const int32_t* blk_off, int nseq, int gi) {
   int lo = 0, hi = nseq;  // blk_off[lo] <= gi < blk_off[hi]

@@ -122,7 +122,7 @@ SB_API int sb_block_pool(const uint16_t* x, const int32_t* cu_seqlens, const int
                          int nb_total, int heads, int head_dim, int block_size, float* xbar, void* stream) {
   return sbk::abi_call([&] {
     sbk::require(heads >= 1 && (head_dim == 64 || head_dim == 128), "heads >= 1 and head_dim in {64,128}");
-    sbk::require(block_size == 64 || block_size == 128, "block_size must be 64 or 128");
+    sbk::require(block_size == 64 || block_size == 128 || block_size == 256, "block_size must be 64, 128 or 256");
     if (nb_total == 0 || nseq == 0) return;
     sbk::require(x && cu_seqlens && blk_off && xbar, "null pointer");
     const dim3 grid(nb_total, (heads * head_dim / 8 + sbk::kPoolThreads - 1) / sbk::kPoolThreads);

@@ -318,3 +318,44 @@ def test_edge_layouts_end_to_end(cu, B):
     rdq, rdk, rdv = orc.sparse_attn_bwd(_bits(q), _bits(k), _bits(v), ro, _bits(do), rlse, cu, B, ic, cc, scale)
     for got, ref, name in ((o, ro, "o"), (dq, rdq, "dq"), (dk, rdk, "dk"), (dv, rdv, "dv")):
         check_bf16(got, ref, name)
+
+
+B256_CASES = [
+    ([0, 2048], 2, 2, 128, 0.5),                     # one sequence, 8 blocks
+    ([0, 1000, 1100, 2900, 4096], 4, 2, 128, 0.4),   # ragged: partial last blocks, a 100-token sequence
+    ([0, 700, 3000], 2, 1, 64, 1.0),                 # dense rows, d64
+]
+
+
+@pytest.mark.parametrize("cu,hq,hkv,d,keep", B256_CASES)
+def test_block_256_fwd_bwd_vs_oracle(cu, hq, hkv, d, keep):
+    """Block size 256 (the paper's MoBA setting; reference default config.hpp:21):
+    scorer -> selector at B = 256, attention through the exact 128-tile re-expression
+    (expand256.cu), fwd and bwd against the fp64 oracle run natively at B = 256."""
+    from paper_2604_13847_b200 import ops
+
+    B = 256
+    T = cu[-1]
+    q, k, v, do = _rand_bf16((T, hq, d), 81), _rand_bf16((T, hkv, d), 82), _rand_bf16((T, hkv, d), 83), \
+        _rand_bf16((T, hq, d), 84)
+    lay = _layout(cu, B)
+    scale = 1.0 / math.sqrt(d)
+    S = ops.block_scores(q, k, lay, scale)
+    rS = orc.block_scores(orc.block_pool(_bits(q), cu, B), orc.block_pool(_bits(k), cu, B), cu, B, scale)
+    np.testing.assert_allclose(S.cpu().numpy()[:, :lay.tri_total], rS[:, :lay.tri_total], rtol=1e-4,
+                               atol=1e-5 * np.abs(rS).max())
+    nb = lay.nb_per_seq
+    k_seq = np.maximum(1, np.ceil(keep * nb)).astype(np.int32)
+    idx, cnt = ops.topk_select(S, lay, torch.from_numpy(k_seq).cuda(), int(k_seq.max()))
+    ridx, rcnt = orc.topk_select(S.cpu().numpy(), cu, B, k_seq, int(k_seq.max()))
+    assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(cnt.cpu().numpy(), rcnt)
+    o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+    ic, cc = idx.cpu().numpy(), cnt.cpu().numpy()
+    ro, rlse = orc.sparse_attn_fwd(_bits(q), _bits(k), _bits(v), cu, B, ic, cc, scale)
+    check_bf16(o, ro, "o")
+    np.testing.assert_allclose(lse.cpu().numpy(), rlse, atol=2e-3, rtol=1e-4)
+    rdq, rdk, rdv = orc.sparse_attn_bwd(_bits(q), _bits(k), _bits(v), ro, _bits(do), rlse, cu, B, ic, cc, scale)
+    for det in (False, True):
+        dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale, deterministic=det)
+        for got, ref, name in ((dq, rdq, "dq"), (dk, rdk, "dk"), (dv, rdv, "dv")):
+            check_bf16(got, ref, f"{name} det={det}")
