@@ -3,18 +3,19 @@
 For an output tensor `got` (rows = (token, head) vectors of the last dim d) against its fp64 /
 fp32 reference `ref`:
   * max |got - ref| <= rel * max |ref|                    (relative to the tensor's scale; no floor)
-  * per row r with rms(ref_r) > sig * max_r rms(ref_r):
-        max_d |got_rd - ref_rd| <= rel * rms(ref_r)     (true relative check against each token's
-                                                         own gradient / output magnitude)
+  * per row r with ||ref_r|| > sig * max_r ||ref_r||:
+        ||got_r - ref_r|| <= rel * ||ref_r||             (true relative check of every token's own
+                                                         output / gradient vector)
   * ||got - ref||_F / ||ref||_F < rel_fro
 
 Why per row and not per element: every tensor-core attention backward rounds dS = P (dP - D) to
 bf16 before the dQ / dK GEMMs, and sum_j dS_ij = 0 per query row, so dQ / dK elements are sums
 with heavy cancellation. Rounding dS alone (an exact fp64 computation otherwise; 2000 rows x 768
-keys, d 128, N(0,1) data) gives 2.4 % elementwise relative error on elements above 5 % of the max,
-but 0.95 % of the row RMS at worst and 0.16 % relative Frobenius -- so the per-row rule at 2e-2
-keeps a 2x margin over the arithmetic any bf16 kernel must do, while a real defect (a wrong block,
-a lost column, a mis-scaled row) moves a row by far more than 2 % of its RMS.
+keys, d 128, N(0,1) data) gives 2.4 % elementwise relative error on elements above 5 % of the max
+-- a tail statistic over ~10^5 elements -- while each row's error vector is ~0.2-0.5 % of the row
+and the relative Frobenius error 0.16 %. The per-row relative L2 rule therefore keeps a wide margin
+over the arithmetic any bf16 kernel must do, while a real defect (a wrong or missing block, a lost
+column, a mis-scaled row) moves a row by far more than 2 %.
 """
 import numpy as np
 
@@ -23,7 +24,7 @@ SIG = 0.05
 
 
 def check_bf16(got, ref, name="", rel=REL, rel_fro=REL, sig=SIG):
-    """Returns (max abs err, worst per-row max-err / row RMS on significant rows, rel Fro)."""
+    """Returns (max abs err, worst per-row relative L2 error on significant rows, rel Fro)."""
     if hasattr(got, "detach"):
         got = got.detach().float().cpu().numpy()
     if hasattr(ref, "detach"):
@@ -38,10 +39,10 @@ def check_bf16(got, ref, name="", rel=REL, rel_fro=REL, sig=SIG):
     assert emax <= rel * amax + 1e-30, (name, "max err", emax, "max|ref|", amax)
     d = ref.shape[-1] if ref.ndim else 1
     rr, ee = ref.reshape(-1, d), err.reshape(-1, d)
-    rms = np.sqrt((rr * rr).mean(axis=1))
-    sig_rows = rms > sig * (rms.max() if rms.size else 0.0)
-    worst = float((ee[sig_rows].max(axis=1) / rms[sig_rows]).max()) if sig_rows.any() else 0.0
-    assert worst <= rel, (name, "per-row max err / row RMS", worst)
+    rn = np.linalg.norm(rr, axis=1)
+    sig_rows = rn > sig * (rn.max() if rn.size else 0.0)
+    worst = float((np.linalg.norm(ee[sig_rows], axis=1) / rn[sig_rows]).max()) if sig_rows.any() else 0.0
+    assert worst <= rel, (name, "per-row relative L2 error", worst)
     fro = float(np.linalg.norm(got - ref) / max(1e-30, np.linalg.norm(ref)))
     assert fro < rel_fro, (name, "rel Fro", fro)
     return emax, worst, fro
