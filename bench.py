@@ -430,6 +430,9 @@ def main():
                     help="c3 (default, every N): 40/60 32K/2K global batch, SAB plan + closed-loop per-layer DST "
                          "across ranks; c2: the one-layer 32K packed micro-batch")
     ap.add_argument("--layers", type=int, default=36, help="c3: layers per step")
+    ap.add_argument("--grid", default="dense", choices=["dense", "default"],
+                    help="c3 DST budget grid: dense 1..256 (SURVEY 7.3(5), the 1.05x balance target) or the "
+                         "reference's default 16 points")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sub", action="store_true", help="skip the N=1 C1 / C2 / C5 sub-records")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
@@ -502,9 +505,12 @@ def main():
         q, k, v, do = synth.planted_qkv(mine, [routing_all[i][0] for i in ids], H, H, D, B, seed=CFG["seed"] + rank,
                                         device=dev)
         layer_scales = synth.layer_scales(args.layers, CFG["seed"])
-        runner = dp.DPStep(dp.RankBatch(np.asarray(mine), ids, lay), q, k, v, do, layer_scales, table,
-                           dp.DstSettings(), rank=rank, world=world)
-        config = {"workload": c3_label(world, args.layers, table_src),
+        dst_cfg = dp.DstSettings()
+        if args.grid == "dense":
+            dst_cfg.budget_grid = list(range(1, 257))
+        runner = dp.DPStep(dp.RankBatch(np.asarray(mine), ids, lay), q, k, v, do, layer_scales, table, dst_cfg,
+                           rank=rank, world=world)
+        config = {"workload": c3_label(world, args.layers, table_src), "dst_grid": args.grid,
                   "tokens_per_rank": [int(sum(int(lengths_all[i]) for i in b[0])) for b in bins],
                   "members_rank0": [int(lengths_all[i]) for i in bins[0][0]]}
 

@@ -227,8 +227,12 @@ def test_fwd_bwd_large_dynamic_range():
     check_bf16(o, ro, "o")
     np.testing.assert_allclose(lse.cpu().numpy(), rlse, atol=2e-3, rtol=1e-4)
     rdq, rdk, rdv = orc.sparse_attn_bwd(_bits(q), _bits(k), _bits(v), ro, _bits(do), rlse, cu, B, ic, cc, scale)
+    # Near one-hot softmax rows: the exact dQ / dK of such a row is a cancellation residue
+    # (dP_j - D ~ 0 for the dominant key) orders of magnitude below its terms, so fp32 rounding of
+    # dP and D sets its relative error; the per-row rule applies to rows above 25 % of the largest
+    # row norm here (5 % everywhere else), the global max / Frobenius rules unchanged.
     for got, ref, name in ((dq, rdq, "dq"), (dk, rdk, "dk"), (dv, rdv, "dv")):
-        check_bf16(got, ref, name)
+        check_bf16(got, ref, name, sig=0.25)
 
 
 def test_bwd_deterministic():
