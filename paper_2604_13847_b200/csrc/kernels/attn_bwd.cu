@@ -1176,42 +1176,60 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
 // ------------------------------------------------------------------------------------ fused
 // Single-pass backward for D = B = 128: 5 UMMAs per (key block, q tile) pair instead of the
 // two-pass 7. Persistent over key-block items (hk, gj) like the dK/dV pass; per pair it also
-// forms the pair's dQ partial dS K in TMEM and TMA-reduce-adds it (cp.reduce.async.bulk.tensor,
-// fp32 add in L2) into an fp32 dQ accumulator, converted to bf16 by a final elementwise pass.
-// The accumulation order of dQ across key blocks is not fixed, so dQ is reproducible to fp32
-// rounding only; the two-pass path stays as the bit-deterministic mode.
+// forms the pair's dQ partial dS K in TMEM, which a dedicated warpgroup streams out through a
+// small shared-memory ring and TMA-reduce-adds (cp.reduce.async.bulk.tensor, fp32 add in L2) into
+// an fp32 dQ accumulator, converted to bf16 by a final elementwise pass. The accumulation order
+// of dQ across key blocks is not fixed, so dQ is reproducible to fp32 rounding only; the two-pass
+// path stays as the bit-deterministic mode (dK / dV here accumulate in a fixed order).
 //
 // TMEM (512 columns): SP | dQ | dV | dK. SP holds the pair's two score tiles in turn (S^T and
 // dP^T; the math warps read the first before the second is issued) and then P^T | dS^T packed as
-// bf16, the A operands of dV += P^T dO and dK += dS^T Q. dQ = dS K reads dS from shared memory
-// (MN-major A), written into the pair's dO ring slot once dV has read dO; the same slot then
-// stages the fp32 dQ partial for the TMA reduce and is released to the producer after it.
+// bf16, the A operands of dV += P^T dO and dK += dS^T Q. dQ = dS K reads dS from a dedicated
+// shared-memory tile (MN-major A); dP^T_{g+1} is issued after dQ_g, so its completion frees that
+// tile for dS_{g+1} with no extra barrier. dO is single-buffered (released after dV_g).
 // An item's first pair computes dP^T before S^T, so the next key block's K load (single K
 // buffer: K is read by S^T and by dQ up to the item's last pair) overlaps that first dP^T.
 //   Issue order: A_g, [sp_free] B_g, [p_ready] dV_g, [ds_ready] dK_g, A_{g+1}, [dsm_ready, dq_free]
 //   dQ_g, [sp_free] B_{g+1}, ...   (A / B = S^T / dP^T, swapped on an item's first pair)
-// Warps 0..3 (one warpgroup, 96 registers): TMA producer, UMMA issuer, two idle; warps 4..11
-// (200 registers): two math warpgroups splitting every key row's query columns in halves.
-constexpr int kFusedThreads = 384;
+// Warps: 0 TMA producer, 1 UMMA issuer, 2-3 idle (WG0, 72 registers); 4-11 two math warpgroups
+// splitting every key row's query columns in halves (184 registers); 12-15 the dQ reducer
+// (72 registers).
+constexpr int kFusedThreads = 512;
+constexpr int kRedCols = 16;    // fp32 dQ columns per TMA reduce box (64-byte rows, 64B swizzle)
+constexpr int kRedStages = 2;   // staging ring depth
 
 struct FusedCfg {
   static constexpr int kTile = 2 * kM * 128;  // 128 rows x 128 bf16 columns (two SW128 chunks)
-  static constexpr int kAugOnes = kM * 32, kAug = kM * 32;
-  static constexpr int kSmemTiles = 2 * kTile + 2 * kTile + 2 * kTile + kAugOnes + 4 * kAug;  // K,V | Q[2] | dO[2] | aug
+  static constexpr int kAug = kM * 32;
+  static constexpr int kStage = kM * kRedCols * 4;
+  // K | V | Q[2] | dO | dS | ones | qaug[2] | daug | dQ staging[kRedStages]
+  static constexpr int kSmemTiles = 6 * kTile + 4 * kAug + kRedStages * kStage;
   static constexpr int kSP = 0, kDQ = 128, kDV = 256, kDK = 384;
   static constexpr uint32_t kCols = 512;
   static constexpr int kSmemBytes = kSmemTiles + 1024 + 256;
 };
+static_assert(FusedCfg::kSmemBytes <= 232448, "fused backward shared memory");
 
 struct FusedBars {
   uint64_t k_full, k_empty, v_full, v_empty;
-  uint64_t q_full[2], q_empty[2], do_full[2], do_empty[2];
-  uint64_t sp_full, sp_free;            // UMMA <-> math: a score tile in SP / the first one read
-  uint64_t p_ready, ds_ready, dsm_ready;  // math -> UMMA: P^T, dS^T packed in SP; dS in smem
-  uint64_t dv_done;                     // UMMA -> math: dV_g read dO_g (the slot may take dS_g)
-  uint64_t dq_full, dq_free;            // UMMA <-> math: the pair's dQ partial in TMEM / read
-  uint64_t acc_done;                    // UMMA -> math: the item's dV / dK are final
+  uint64_t q_full[2], q_empty[2], do_full, do_empty;
+  uint64_t sp_full, sp_free;               // UMMA <-> math: a score tile in SP / the first one read
+  uint64_t p_ready, ds_ready, dsm_ready;   // math -> UMMA: P^T, dS^T packed in SP; dS in smem
+  uint64_t dq_full, dq_free;               // UMMA <-> reducer: the pair's dQ partial in TMEM / read
+  uint64_t acc_done;                       // UMMA -> math: the item's dV / dK are final
   uint32_t tmem_base;
+};
+
+// Pair decode shared by the roles: the m-th (q head, q block) pair of a key-block item.
+struct PairCursor {
+  const int32_t* tr_ent;
+  int nbt, sg;
+  __device__ __forceinline__ void get(const KvItem& w, int m, int& h, int& gi) const {
+    const int ent = __ldg(tr_ent + w.e0 + m / sg);
+    const int hs = ent / nbt;
+    gi = ent - hs * nbt;
+    h = hs * sg + m % sg;
+  }
 };
 
 __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
@@ -1228,11 +1246,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* k_smem = smem;
   uint8_t* v_smem = smem + C::kTile;
-  uint8_t* q_smem = smem + 2 * C::kTile;    // [2]
-  uint8_t* do_smem = smem + 4 * C::kTile;   // [2]: dO_g, then dS_g, then the dQ_g partial staging
+  uint8_t* q_smem = smem + 2 * C::kTile;   // [2]
+  uint8_t* do_smem = smem + 4 * C::kTile;
+  uint8_t* ds_smem = smem + 5 * C::kTile;  // dS_g, MN-major A operand of dQ_g
   uint8_t* ones_smem = smem + 6 * C::kTile;
-  uint8_t* qaug_smem = ones_smem + C::kAugOnes;  // [2] -lse2 / scale_log2
-  uint8_t* daug_smem = qaug_smem + 2 * C::kAug;  // [2] -D
+  uint8_t* qaug_smem = ones_smem + C::kAug;      // [2] -lse2 / scale_log2
+  uint8_t* daug_smem = qaug_smem + 2 * C::kAug;  // -D
+  uint8_t* red_smem = daug_smem + C::kAug;       // [kRedStages] dQ staging
   FusedBars* bars = reinterpret_cast<FusedBars*>(smem + C::kSmemTiles);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1240,6 +1260,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
   const int grid = gridDim.x, cta = blockIdx.x;
   const int sg = hq / hsel;
   const float inv_scale_log2 = 1.0f / scale_log2;
+  const PairCursor pc{tr_ent, nbt, sg};
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->k_full, 1);
@@ -1247,26 +1268,25 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
     mbar_init(&bars->v_full, 1);
     mbar_init(&bars->v_empty, 1);
     for (int st = 0; st < 2; ++st) {
-      mbar_init(&bars->q_full[st], 2);   // TMA expect_tx arrive + augmented-slice arrive
-      mbar_init(&bars->q_empty[st], 1);  // UMMA commit after dK
-      mbar_init(&bars->do_full[st], 2);
-      mbar_init(&bars->do_empty[st], 2);  // one per math warpgroup after its dQ reduce read the slot
+      mbar_init(&bars->q_full[st], 2);  // TMA expect_tx arrive + augmented-slice arrive
+      mbar_init(&bars->q_empty[st], 1);
     }
+    mbar_init(&bars->do_full, 2);
+    mbar_init(&bars->do_empty, 1);
     mbar_init(&bars->sp_full, 1);
     mbar_init(&bars->sp_free, 256);
     mbar_init(&bars->p_ready, 256);
     mbar_init(&bars->ds_ready, 256);
     mbar_init(&bars->dsm_ready, 256);
-    mbar_init(&bars->dv_done, 1);
     mbar_init(&bars->dq_full, 1);
-    mbar_init(&bars->dq_free, 256);
+    mbar_init(&bars->dq_free, 128);
     mbar_init(&bars->acc_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kCols>(&bars->tmem_base);
   {
     uint4* z = reinterpret_cast<uint4*>(ones_smem);
-    for (int i = threadIdx.x; i < (C::kAugOnes + 4 * C::kAug) / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < 4 * C::kAug / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     for (int r = threadIdx.x; r < kM; r += blockDim.x)
       *reinterpret_cast<uint2*>(ones_smem + aug_off(r)) = make_uint2(0x3F803F80u, 0x00003F80u);
@@ -1277,262 +1297,216 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  auto pair_of = [&](const KvItem& w, int m, int& h, int& gi) {
-    const int ent = __ldg(tr_ent + w.e0 + m / sg);
-    const int hs = ent / nbt;
-    gi = ent - hs * nbt;
-    h = hs * sg + m % sg;
-  };
-
-  if (warp < 4) setmaxnreg_dec<96>();
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer (whole warp)
-    if (lane == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      tma_prefetch(&tm_do);
-    }
-    int g = 0, t = 0;
-    auto load_q = [&](int gg, int h, int q0, int nq) {
-      const int st = gg & 1;
-      float nl[B / 32];
-#pragma unroll
-      for (int e = 0; e < B / 32; ++e) {
-        const int r = e * 32 + lane;
-        nl[e] = r < nq ? __ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
-      }
-      mbar_wait(&bars->q_empty[st], ((gg >> 1) & 1) ^ 1);
+  if (warp < 4) {
+    setmaxnreg_dec<72>();
+    if (warp == 0) {
+      // ---------------------------------------------------------- producer (whole warp)
       if (lane == 0) {
-        mbar_expect_tx(&bars->q_full[st], C::kTile);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d(q_smem + st * C::kTile + c * kM * 128, &tm_q, &bars->q_full[st], c * 64, h, q0);
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        tma_prefetch(&tm_do);
       }
-      uint8_t* qa = qaug_smem + st * C::kAug;
+      int g = 0, t = 0;
+      auto load_q = [&](int gg, int h, int q0, int nq) {
+        const int st = gg & 1;
+        float nl[B / 32];
 #pragma unroll
-      for (int e = 0; e < B / 32; ++e)
-        *reinterpret_cast<uint2*>(qa + aug_off(e * 32 + lane)) = split3_bf16(-nl[e] * inv_scale_log2);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->q_full[st]);
-    };
-    auto load_do = [&](int gg, int h, int q0, int nq) {
-      const int st = gg & 1;
-      float nd[B / 32];
-#pragma unroll
-      for (int e = 0; e < B / 32; ++e) {
-        const int r = e * 32 + lane;
-        nd[e] = r < nq ? __ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
-      }
-      mbar_wait(&bars->do_empty[st], ((gg >> 1) & 1) ^ 1);
-      if (lane == 0) {
-        mbar_expect_tx(&bars->do_full[st], C::kTile);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d(do_smem + st * C::kTile + c * kM * 128, &tm_do, &bars->do_full[st], c * 64, h, q0);
-      }
-      uint8_t* da = daug_smem + st * C::kAug;
-#pragma unroll
-      for (int e = 0; e < B / 32; ++e) *reinterpret_cast<uint2*>(da + aug_off(e * 32 + lane)) = split3_bf16(-nd[e]);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->do_full[st]);
-    };
-    for (int k = 0;; ++k) {
-      const int it = sched::snake_item(order, n_items, grid, cta, k);
-      if (it < 0) break;
-      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
-      const int items = w.ne * sg;
-      if (items == 0) continue;
-      const int kv0 = w.seq0 + w.jl * B;
-      const int blk0 = w.gj - w.jl;
-      if (lane == 0) {  // V first: the item's first UMMA is dP^T
-        mbar_wait(&bars->v_empty, (t & 1) ^ 1);
-        mbar_expect_tx(&bars->v_full, C::kTile);
-        for (int c = 0; c < 2; ++c) tma_load_3d(v_smem + c * kM * 128, &tm_v, &bars->v_full, c * 64, w.hk, kv0);
-      }
-      for (int m = 0; m < items; ++m, ++g) {
-        int h, gi;
-        pair_of(w, m, h, gi);
-        const int q0 = w.seq0 + (gi - blk0) * B;
-        const int nq = min(B, w.seq_len - (gi - blk0) * B);
-        if (m == 0) {
-          load_do(g, h, q0, nq);
-          load_q(g, h, q0, nq);
-          if (lane == 0) {  // K after the first pair's dO / Q: the previous item's last dQ reads K
-            mbar_wait(&bars->k_empty, (t & 1) ^ 1);
-            mbar_expect_tx(&bars->k_full, C::kTile);
-            for (int c = 0; c < 2; ++c) tma_load_3d(k_smem + c * kM * 128, &tm_k, &bars->k_full, c * 64, w.hk, kv0);
-          }
-        } else {
-          load_q(g, h, q0, nq);
-          load_do(g, h, q0, nq);
+        for (int e = 0; e < B / 32; ++e) {
+          const int r = e * 32 + lane;
+          nl[e] = r < nq ? __ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
         }
-      }
-      ++t;
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ UMMA issuer (whole warp)
-    const uint32_t leader = elect_one();
-    constexpr uint32_t idesc_t = idesc_bf16_f32(kM, B, false, false);
-    constexpr uint32_t idesc_acc = idesc_bf16_f32(kM, D, false, true);
-    constexpr uint32_t idesc_dq = idesc_bf16_f32(kM, D, true, true);
-    const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem), ones_addr = smem_u32(ones_smem);
-    auto qa = [&](int gg) { return smem_u32(q_smem + (gg & 1) * C::kTile); };
-    auto da = [&](int gg) { return smem_u32(do_smem + (gg & 1) * C::kTile); };
-    auto issue_st = [&](int gg) {
-      mbar_wait(&bars->q_full[gg & 1], (gg >> 1) & 1);
-      tc_fence_after();
+        mbar_wait(&bars->q_empty[st], ((gg >> 1) & 1) ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(&bars->q_full[st], C::kTile);
+          for (int c = 0; c < 2; ++c)
+            tma_load_3d(q_smem + st * C::kTile + c * kM * 128, &tm_q, &bars->q_full[st], c * 64, h, q0);
+        }
+        uint8_t* qa = qaug_smem + st * C::kAug;
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t off = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
-        mma_ss(tmem + C::kSP, desc_sw128(k_addr + off, 16, 1024), desc_sw128(qa(gg) + off, 16, 1024), idesc_t, kk > 0,
-               leader);
-      }
-      mma_ss(tmem + C::kSP, desc_aug(ones_addr), desc_aug(smem_u32(qaug_smem + (gg & 1) * C::kAug)), idesc_t, 1u,
-             leader);
-      tc_commit(&bars->sp_full, leader);
-    };
-    auto issue_dpt = [&](int gg) {
-      mbar_wait(&bars->do_full[gg & 1], (gg >> 1) & 1);
-      tc_fence_after();
+        for (int e = 0; e < B / 32; ++e)
+          *reinterpret_cast<uint2*>(qa + aug_off(e * 32 + lane)) = split3_bf16(-nl[e] * inv_scale_log2);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->q_full[st]);
+      };
+      auto load_do = [&](int gg, int h, int q0, int nq) {
+        float nd[B / 32];
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t off = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
-        mma_ss(tmem + C::kSP, desc_sw128(v_addr + off, 16, 1024), desc_sw128(da(gg) + off, 16, 1024), idesc_t, kk > 0,
-               leader);
-      }
-      mma_ss(tmem + C::kSP, desc_aug(ones_addr), desc_aug(smem_u32(daug_smem + (gg & 1) * C::kAug)), idesc_t, 1u,
-             leader);
-      tc_commit(&bars->sp_full, leader);
-    };
-    int g = 0, t = 0;
-    bool a_issued = false;  // tile A of pair g already issued (at the end of pair g - 1)
-    KvItem w;
-    int k = 0;
-    auto next_item = [&](KvItem& out) -> bool {
-      for (;; ++k) {
+        for (int e = 0; e < B / 32; ++e) {
+          const int r = e * 32 + lane;
+          nd[e] = r < nq ? __ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+        }
+        mbar_wait(&bars->do_empty, (gg & 1) ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(&bars->do_full, C::kTile);
+          for (int c = 0; c < 2; ++c) tma_load_3d(do_smem + c * kM * 128, &tm_do, &bars->do_full, c * 64, h, q0);
+        }
+#pragma unroll
+        for (int e = 0; e < B / 32; ++e)
+          *reinterpret_cast<uint2*>(daug_smem + aug_off(e * 32 + lane)) = split3_bf16(-nd[e]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->do_full);
+      };
+      for (int k = 0;; ++k) {
         const int it = sched::snake_item(order, n_items, grid, cta, k);
-        if (it < 0) return false;
-        out = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
-        if (out.ne * sg > 0) {
-          ++k;
-          return true;
+        if (it < 0) break;
+        const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+        const int items = w.ne * sg;
+        if (items == 0) continue;
+        const int kv0 = w.seq0 + w.jl * B;
+        const int blk0 = w.gj - w.jl;
+        if (lane == 0) {  // V first: the item's first UMMA is dP^T
+          tma_prefetch_l2_3d(&tm_k, 0, w.hk, kv0);
+          tma_prefetch_l2_3d(&tm_k, 64, w.hk, kv0);
+          mbar_wait(&bars->v_empty, (t & 1) ^ 1);
+          mbar_expect_tx(&bars->v_full, C::kTile);
+          for (int c = 0; c < 2; ++c) tma_load_3d(v_smem + c * kM * 128, &tm_v, &bars->v_full, c * 64, w.hk, kv0);
         }
-      }
-    };
-    bool have = next_item(w);
-    while (have) {
-      const int items = w.ne * sg;
-      KvItem nx;
-      bool have_nx = false;
-      for (int m = 0; m < items; ++m, ++g) {
-        const bool last = m + 1 == items;
-        if (!a_issued) {  // only the CTA's very first pair: dP^T first
-          mbar_wait(&bars->v_full, t & 1);
-          issue_dpt(g);
-        }
-        a_issued = false;
-        // tile B
-        mbar_wait(&bars->sp_free, g & 1);
-        if (m == 0) {
-          mbar_wait(&bars->k_full, t & 1);
-          issue_st(g);
-        } else {
-          issue_dpt(g);
-        }
-        if (last) tc_commit(&bars->v_empty, leader);  // the item's last dP^T is issued
-        // dV_g += P^T dO_g  (TS: P^T packed at SP + hf*64 + [0, 32))
-        mbar_wait(&bars->p_ready, g & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < B / 16; ++kk)
-          mma_ts(tmem + C::kDV, tmem + C::kSP + (kk >> 2) * 64 + (kk & 3) * 8,
-                 desc_sw128(da(g) + kk * 2048, kM * 128, 1024), idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
-        tc_commit(&bars->dv_done, leader);
-        // dK_g += dS^T Q_g  (TS: dS^T packed at SP + hf*64 + [32, 64))
-        mbar_wait(&bars->ds_ready, g & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < B / 16; ++kk)
-          mma_ts(tmem + C::kDK, tmem + C::kSP + (kk >> 2) * 64 + 32 + (kk & 3) * 8,
-                 desc_sw128(qa(g) + kk * 2048, kM * 128, 1024), idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
-        tc_commit(&bars->q_empty[g & 1], leader);
-        // tile A of the next pair (overwrites SP after dV_g / dK_g read it: in-order pipe)
-        if (!last) {
-          issue_st(g + 1);
-          a_issued = true;
-        } else {
-          have_nx = next_item(nx);
-          if (have_nx) {
-            mbar_wait(&bars->v_full, (t + 1) & 1);
-            issue_dpt(g + 1);
-            a_issued = true;
+        for (int m = 0; m < items; ++m, ++g) {
+          int h, gi;
+          pc.get(w, m, h, gi);
+          const int q0 = w.seq0 + (gi - blk0) * B;
+          const int nq = min(B, w.seq_len - (gi - blk0) * B);
+          if (m == 0) {
+            load_do(g, h, q0, nq);
+            load_q(g, h, q0, nq);
+            if (lane == 0) {  // K after the first pair's dO / Q: the previous item's last dQ reads K
+              mbar_wait(&bars->k_empty, (t & 1) ^ 1);
+              mbar_expect_tx(&bars->k_full, C::kTile);
+              for (int c = 0; c < 2; ++c) tma_load_3d(k_smem + c * kM * 128, &tm_k, &bars->k_full, c * 64, w.hk, kv0);
+            }
+          } else {
+            load_q(g, h, q0, nq);
+            load_do(g, h, q0, nq);
           }
         }
-        // dQ_g = dS_g K  (SS: A = dS in the dO_g slot, MN-major; B = K MN-major)
-        mbar_wait(&bars->dsm_ready, g & 1);
-        if (g > 0) mbar_wait(&bars->dq_free, (g - 1) & 1);
+        ++t;
+      }
+    } else if (warp == 1) {
+      // ---------------------------------------------------------- UMMA issuer (whole warp)
+      const uint32_t leader = elect_one();
+      constexpr uint32_t idesc_t = idesc_bf16_f32(kM, B, false, false);
+      constexpr uint32_t idesc_acc = idesc_bf16_f32(kM, D, false, true);
+      constexpr uint32_t idesc_dq = idesc_bf16_f32(kM, D, true, true);
+      const uint32_t k_addr = smem_u32(k_smem), v_addr = smem_u32(v_smem), ones_addr = smem_u32(ones_smem);
+      const uint32_t do_addr = smem_u32(do_smem), ds_addr = smem_u32(ds_smem);
+      auto qa = [&](int gg) { return smem_u32(q_smem + (gg & 1) * C::kTile); };
+      auto issue_st = [&](int gg) {
+        mbar_wait(&bars->q_full[gg & 1], (gg >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < B / 16; ++kk)
-          mma_ss(tmem + C::kDQ, desc_sw128(da(g) + kk * 2048, kM * 128, 1024),
-                 desc_sw128(k_addr + kk * 2048, kM * 128, 1024), idesc_dq, kk > 0 ? 1u : 0u, leader);
-        tc_commit(&bars->dq_full, leader);
-        if (last) {
-          tc_commit(&bars->acc_done, leader);
-          tc_commit(&bars->k_empty, leader);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
+          mma_ss(tmem + C::kSP, desc_sw128(k_addr + off, 16, 1024), desc_sw128(qa(gg) + off, 16, 1024), idesc_t,
+                 kk > 0, leader);
         }
+        mma_ss(tmem + C::kSP, desc_aug(ones_addr), desc_aug(smem_u32(qaug_smem + (gg & 1) * C::kAug)), idesc_t, 1u,
+               leader);
+        tc_commit(&bars->sp_full, leader);
+      };
+      auto issue_dpt = [&](int gg) {
+        mbar_wait(&bars->do_full, gg & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (kM * 128) + (kk & 3) * 32;
+          mma_ss(tmem + C::kSP, desc_sw128(v_addr + off, 16, 1024), desc_sw128(do_addr + off, 16, 1024), idesc_t,
+                 kk > 0, leader);
+        }
+        mma_ss(tmem + C::kSP, desc_aug(ones_addr), desc_aug(smem_u32(daug_smem)), idesc_t, 1u, leader);
+        tc_commit(&bars->sp_full, leader);
+      };
+      int g = 0, t = 0, k = 0;
+      bool a_issued = false;  // tile A of pair g already issued (at the end of pair g - 1)
+      auto next_item = [&](KvItem& out) -> bool {
+        for (;; ++k) {
+          const int it = sched::snake_item(order, n_items, grid, cta, k);
+          if (it < 0) return false;
+          out = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+          if (out.ne * sg > 0) {
+            ++k;
+            return true;
+          }
+        }
+      };
+      KvItem w;
+      bool have = next_item(w);
+      while (have) {
+        const int items = w.ne * sg;
+        KvItem nx;
+        bool have_nx = false;
+        for (int m = 0; m < items; ++m, ++g) {
+          const bool last = m + 1 == items;
+          if (!a_issued) {  // only the CTA's very first pair: dP^T first
+            mbar_wait(&bars->v_full, t & 1);
+            issue_dpt(g);
+          }
+          a_issued = false;
+          mbar_wait(&bars->sp_free, g & 1);  // tile B
+          if (m == 0) {
+            mbar_wait(&bars->k_full, t & 1);
+            issue_st(g);
+          } else {
+            issue_dpt(g);
+          }
+          if (last) tc_commit(&bars->v_empty, leader);  // the item's last dP^T is issued
+          mbar_wait(&bars->p_ready, g & 1);  // dV_g += P^T dO_g (TS: P^T packed at SP + hf*64 + [0, 32))
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < B / 16; ++kk)
+            mma_ts(tmem + C::kDV, tmem + C::kSP + (kk >> 2) * 64 + (kk & 3) * 8,
+                   desc_sw128(do_addr + kk * 2048, kM * 128, 1024), idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
+          tc_commit(&bars->do_empty, leader);
+          mbar_wait(&bars->ds_ready, g & 1);  // dK_g += dS^T Q_g (TS: dS^T packed at SP + hf*64 + [32, 64))
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < B / 16; ++kk)
+            mma_ts(tmem + C::kDK, tmem + C::kSP + (kk >> 2) * 64 + 32 + (kk & 3) * 8,
+                   desc_sw128(qa(g) + kk * 2048, kM * 128, 1024), idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
+          tc_commit(&bars->q_empty[g & 1], leader);
+          // tile A of the next pair (overwrites SP after dV_g / dK_g read it: in-order pipe)
+          if (!last) {
+            issue_st(g + 1);
+            a_issued = true;
+          } else {
+            have_nx = next_item(nx);
+            if (have_nx) {
+              mbar_wait(&bars->v_full, (t + 1) & 1);
+              issue_dpt(g + 1);
+              a_issued = true;
+            }
+          }
+          // dQ_g = dS_g K  (SS: A = dS MN-major; B = K MN-major)
+          mbar_wait(&bars->dsm_ready, g & 1);
+          if (g > 0) mbar_wait(&bars->dq_free, (g - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < B / 16; ++kk)
+            mma_ss(tmem + C::kDQ, desc_sw128(ds_addr + kk * 2048, kM * 128, 1024),
+                   desc_sw128(k_addr + kk * 2048, kM * 128, 1024), idesc_dq, kk > 0 ? 1u : 0u, leader);
+          tc_commit(&bars->dq_full, leader);
+          if (last) {
+            tc_commit(&bars->acc_done, leader);
+            tc_commit(&bars->k_empty, leader);
+          }
+        }
+        ++t;
+        w = nx;
+        have = have_nx;
       }
-      ++t;
-      w = nx;
-      have = have_nx;
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ math + dQ reduce + dK/dV epilogue
-    setmaxnreg_inc<200>();
+  } else if (warp < 12) {
+    // ------------------------------------------------------------ math + dK/dV epilogue
+    setmaxnreg_inc<184>();
     constexpr int HB = B / 2;
     const int quarter = warp & 3;
     const int hf = (warp - 4) >> 2;
-    const int c = quarter * 32 + lane;  // TMEM lane: key row (SP, dV, dK) / query row (dQ)
+    const int c = quarter * 32 + lane;  // TMEM lane: key row
     const uint32_t lf = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t sp = tmem + lf + C::kSP + hf * HB;
-    const bool elected = (c == 0);      // one thread per warpgroup issues its TMA reduces
     int g = 0, t = 0;
-    int prev_h = 0, prev_q0 = 0;
-    // dQ partial of pair gg (query rows = TMEM lanes, this warpgroup's 64 columns) -> fp32 tiles
-    // through this warpgroup's half of the dO_gg slot -> TMA reduce-add into the accumulator.
-    auto reduce_dq = [&](int gg, int h, int q0) {
-      mbar_wait(&bars->dq_full, gg & 1);
-      tc_fence_after();
-      uint32_t v[2][32];
-      tmem_ld32(tmem + lf + C::kDQ + hf * HB, v[0]);
-      tmem_ld32(tmem + lf + C::kDQ + hf * HB + 32, v[1]);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&bars->dq_free);
-      uint8_t* stg = do_smem + (gg & 1) * C::kTile + hf * (kM * 128);
-#pragma unroll
-      for (int rd = 0; rd < 2; ++rd) {
-        if (rd > 0) {
-          if (elected) bulk_wait_read();
-          named_bar_sync(1 + hf, 128);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          *reinterpret_cast<uint4*>(stg + c * 128 + ((u ^ (c & 7)) << 4)) =
-              make_uint4(v[rd][4 * u], v[rd][4 * u + 1], v[rd][4 * u + 2], v[rd][4 * u + 3]);
-        fence_proxy_async_smem();
-        named_bar_sync(1 + hf, 128);
-        if (elected) {
-          tma_reduce_add_3d(&tm_dqacc, stg, hf * HB + rd * 32, h, q0);
-          bulk_commit();
-        }
-      }
-      if (elected) {
-        bulk_wait_read();
-        mbar_arrive(&bars->do_empty[gg & 1]);
-      }
-    };
     for (int k = 0;; ++k) {
       const int it = sched::snake_item(order, n_items, grid, cta, k);
       if (it < 0) break;
@@ -1543,9 +1517,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
       const int blk0 = w.gj - w.jl;
       for (int m = 0; m < items; ++m, ++g) {
         int h, gi;
-        pair_of(w, m, h, gi);
+        pc.get(w, m, h, gi);
         const int il = gi - blk0;
-        const int q0 = w.seq0 + il * B;
         const int nq = min(B, w.seq_len - il * B);
         // Valid query columns r >= r_lo: r >= key row on the diagonal; none for key rows past the
         // sequence end (their dS must be 0: dQ sums over every key row of the tile).
@@ -1575,13 +1548,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
               tb[c2][e] = x;
             }
         }
-        const auto& sv = ta;
-        const auto& dpv = tb;
         float p[HB];
         if (r_lo <= hf * HB && nq == B) {
-          dkv_p<HB, false>(sv, scale_log2, hf * HB, 0, B, p);
+          dkv_p<HB, false>(ta, scale_log2, hf * HB, 0, B, p);
         } else {
-          dkv_p<HB, true>(sv, scale_log2, hf * HB, r_lo, nq, p);
+          dkv_p<HB, true>(ta, scale_log2, hf * HB, r_lo, nq, p);
         }
         {
           uint32_t pw[2][16];
@@ -1597,7 +1568,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
 #pragma unroll
         for (int e = 0; e < HB; e += 2) {  // dS^T = P^T (dP^T - D): the UMMA already subtracted D
           const f2 ds = fmul2(mk2(p[e], p[e + 1]),
-                              mk2(__uint_as_float(dpv[e / 32][e % 32]), __uint_as_float(dpv[e / 32][e % 32 + 1])));
+                              mk2(__uint_as_float(tb[e / 32][e % 32]), __uint_as_float(tb[e / 32][e % 32 + 1])));
           dsw[e / 2] = pack_bf16x2(ds.x, ds.y);
         }
         {
@@ -1613,19 +1584,16 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
           tc_fence_before();
           mbar_arrive(&bars->ds_ready);
         }
-        if (g > 0) reduce_dq(g - 1, prev_h, prev_q0);
-        // dS (bf16) into the dO_g slot as the MN-major A operand of dQ_g: chunk hf holds query
-        // columns [hf*64, hf*64 + 64) of every key row c (128-byte rows, SW128).
-        mbar_wait(&bars->dv_done, g & 1);
-        uint8_t* dsm = do_smem + (g & 1) * C::kTile + hf * (kM * 128) + c * 128;
+        // dS (bf16) as the MN-major A operand of dQ_g: chunk hf holds query columns
+        // [hf*64, hf*64 + 64) of every key row c (128-byte rows, SW128). dQ_{g-1} has read the
+        // tile: it was issued before dP^T_g, whose completion (tile B / A above) we waited for.
+        uint8_t* dsm = ds_smem + hf * (kM * 128) + c * 128;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           *reinterpret_cast<uint4*>(dsm + ((u ^ (c & 7)) << 4)) =
               make_uint4(dsw[4 * u], dsw[4 * u + 1], dsw[4 * u + 2], dsw[4 * u + 3]);
         fence_proxy_async_smem();
         mbar_arrive(&bars->dsm_ready);
-        prev_h = h;
-        prev_q0 = q0;
       }
       // Epilogue: dV and dK * scale for the valid key rows (zeros if nobody selected the block).
       if (items > 0) {
@@ -1660,7 +1628,58 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
       }
       tc_fence_before();  // epilogue TMEM reads precede the next item's first dV / dK (ordered via p_ready)
     }
-    if (g > 0) reduce_dq(g - 1, prev_h, prev_q0);
+  } else {
+    // ------------------------------------------------------------ dQ reducer (warps 12..15)
+    // Per pair: the 128 x 128 fp32 dQ partial (TMEM lanes = query rows) in 32-column slices ->
+    // 16-column boxes through a kRedStages ring (64-byte rows, 64B swizzle) -> TMA reduce-add.
+    setmaxnreg_dec<72>();
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lf = static_cast<uint32_t>(quarter * 32) << 16;
+    const bool elected = r == 0;
+    int g = 0, n = 0;  // pair counter, staged box counter
+    for (int k = 0;; ++k) {
+      const int it = sched::snake_item(order, n_items, grid, cta, k);
+      if (it < 0) break;
+      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+      const int items = w.ne * sg;
+      const int blk0 = w.gj - w.jl;
+      for (int m = 0; m < items; ++m, ++g) {
+        int h, gi;
+        pc.get(w, m, h, gi);
+        const int q0 = w.seq0 + (gi - blk0) * B;
+        mbar_wait(&bars->dq_full, g & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int sl = 0; sl < D / 32; ++sl) {
+          uint32_t v[32];
+          tmem_ld32(tmem + lf + C::kDQ + sl * 32, v);
+          tmem_wait_ld();
+          if (sl == D / 32 - 1) {
+            tc_fence_before();
+            mbar_arrive(&bars->dq_free);  // the whole partial is in registers / staged
+          }
+#pragma unroll
+          for (int half = 0; half < 32 / kRedCols; ++half, ++n) {
+            uint8_t* stg = red_smem + (n % kRedStages) * C::kStage;
+            if (elected) bulk_wait_read<kRedStages - 1>();  // this slot's previous box has been read
+            named_bar_sync(3, 128);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int e = half * kRedCols + 4 * u;
+              *reinterpret_cast<uint4*>(stg + r * 64 + ((u ^ ((r >> 1) & 3)) << 4)) =
+                  make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(3, 128);
+            if (elected) {
+              tma_reduce_add_3d(&tm_dqacc, stg, sl * 32 + half * kRedCols, h, q0);
+              bulk_commit();
+            }
+          }
+        }
+      }
+    }
     if (elected) bulk_wait_all();  // every dQ reduce has landed before the kernel ends
   }
   tc_fence_before();
@@ -1778,7 +1797,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
       const CUtensorMap tdo = make_thd_map(d_o, total, hq, D, kM);
       const CUtensorMap tk = make_thd_map(k, total, hkv, D, kM);
       const CUtensorMap tv = make_thd_map(v, total, hkv, D, kM);
-      const CUtensorMap tacc = make_thd_map_f32(dqacc, total, hq, D, kM);
+      const CUtensorMap tacc = make_thd_map_f32(dqacc, total, hq, D, kM, kRedCols);
       cuda_check(cudaFuncSetAttribute(attn_bwd_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       FusedCfg::kSmemBytes),
                  "sb_sparse_attn_bwd: smem attribute (fused)");

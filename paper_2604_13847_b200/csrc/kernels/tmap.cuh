@@ -47,18 +47,22 @@ inline CUtensorMap make_thd_map(const void* base, int total_tokens, int heads, i
 }
 
 // 3-D view {D, H, T} of a [T][H][D] fp32 tensor (the fused backward's dQ accumulator); box
-// {32, 1, rows} (128-byte rows), 128-byte swizzle, for TMA reduce-add tiles.
-inline CUtensorMap make_thd_map_f32(const void* base, int total_tokens, int heads, int head_dim, int box_rows) {
+// {box_cols, 1, rows} for TMA reduce-add tiles; 64-byte rows (16 columns) use the 64B swizzle.
+inline CUtensorMap make_thd_map_f32(const void* base, int total_tokens, int heads, int head_dim, int box_rows,
+                                    int box_cols = 16) {
   CUtensorMap map;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(head_dim), static_cast<cuuint64_t>(heads),
                               static_cast<cuuint64_t>(total_tokens)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(head_dim) * 4,
                                  static_cast<cuuint64_t>(heads) * head_dim * 4};
-  const cuuint32_t box[3] = {32, 1, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_cols), 1, static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapSwizzle swz = box_cols * 4 == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : box_cols * 4 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_32B;
   const CUresult r = encode_tiled_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims,
                                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                       swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (f32) failed: " + std::to_string(r));
   return map;
