@@ -1523,36 +1523,46 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
         // Valid query columns r >= r_lo: r >= key row on the diagonal; none for key rows past the
         // sequence end (their dS must be 0: dQ sums over every key row of the tile).
         const int r_lo = c >= nkv ? B : (il == w.jl ? c : 0);
+        // ta <- S^T, tb <- dP^T. Tiles arrive as A then B (sp_full completions 2g, 2g + 1); A is
+        // S^T except on an item's first pair (dP^T first). When S^T comes first its exponentials
+        // run while the UMMA computes dP^T.
         uint32_t ta[HB / 32][32], tb[HB / 32][32];
-        mbar_wait(&bars->sp_full, 0);  // tile A (completion 2g: parity 0)
-        tc_fence_after();
-#pragma unroll
-        for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, ta[c2]);
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(&bars->sp_free);
-        mbar_wait(&bars->sp_full, 1);  // tile B (completion 2g + 1)
-        tc_fence_after();
-#pragma unroll
-        for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, tb[c2]);
-        tmem_wait_ld();
-        // ta <- S^T, tb <- dP^T (an item's first pair arrives as A = dP^T, B = S^T): register
-        // swaps, no dynamic indexing of the register arrays.
-        if (m == 0) {
-#pragma unroll
-          for (int c2 = 0; c2 < HB / 32; ++c2)
-#pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const uint32_t x = ta[c2][e];
-              ta[c2][e] = tb[c2][e];
-              tb[c2][e] = x;
-            }
-        }
         float p[HB];
-        if (r_lo <= hf * HB && nq == B) {
-          dkv_p<HB, false>(ta, scale_log2, hf * HB, 0, B, p);
+        auto exp_p = [&]() {
+          if (r_lo <= hf * HB && nq == B) {
+            dkv_p<HB, false>(ta, scale_log2, hf * HB, 0, B, p);
+          } else {
+            dkv_p<HB, true>(ta, scale_log2, hf * HB, r_lo, nq, p);
+          }
+        };
+        if (m > 0) {
+          mbar_wait(&bars->sp_full, 0);
+          tc_fence_after();
+#pragma unroll
+          for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, ta[c2]);
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(&bars->sp_free);
+          exp_p();
+          mbar_wait(&bars->sp_full, 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, tb[c2]);
+          tmem_wait_ld();
         } else {
-          dkv_p<HB, true>(ta, scale_log2, hf * HB, r_lo, nq, p);
+          mbar_wait(&bars->sp_full, 0);
+          tc_fence_after();
+#pragma unroll
+          for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, tb[c2]);
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(&bars->sp_free);
+          mbar_wait(&bars->sp_full, 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, ta[c2]);
+          tmem_wait_ld();
+          exp_p();
         }
         {
           uint32_t pw[2][16];
