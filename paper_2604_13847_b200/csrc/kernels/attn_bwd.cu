@@ -1394,7 +1394,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
       const uint32_t do_addr = smem_u32(do_smem), ds_addr = smem_u32(ds_smem);
       auto qa = [&](int gg) { return smem_u32(q_smem + (gg & 1) * C::kTile); };
       auto issue_st = [&](int gg) {
-        mbar_wait(&bars->q_full[gg & 1], (gg >> 1) & 1);
+        mbar_wait_spin(&bars->q_full[gg & 1], (gg >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -1407,7 +1407,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
         tc_commit(&bars->sp_full, leader);
       };
       auto issue_dpt = [&](int gg) {
-        mbar_wait(&bars->do_full, gg & 1);
+        mbar_wait_spin(&bars->do_full, gg & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -1440,26 +1440,26 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
         for (int m = 0; m < items; ++m, ++g) {
           const bool last = m + 1 == items;
           if (!a_issued) {  // only the CTA's very first pair: dP^T first
-            mbar_wait(&bars->v_full, t & 1);
+            mbar_wait_spin(&bars->v_full, t & 1);
             issue_dpt(g);
           }
           a_issued = false;
-          mbar_wait(&bars->sp_free, g & 1);  // tile B
+          mbar_wait_spin(&bars->sp_free, g & 1);  // tile B
           if (m == 0) {
-            mbar_wait(&bars->k_full, t & 1);
+            mbar_wait_spin(&bars->k_full, t & 1);
             issue_st(g);
           } else {
             issue_dpt(g);
           }
           if (last) tc_commit(&bars->v_empty, leader);  // the item's last dP^T is issued
-          mbar_wait(&bars->p_ready, g & 1);  // dV_g += P^T dO_g (TS: P^T packed at SP + hf*64 + [0, 32))
+          mbar_wait_spin(&bars->p_ready, g & 1);  // dV_g += P^T dO_g (TS: P^T packed at SP + hf*64 + [0, 32))
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
             mma_ts(tmem + C::kDV, tmem + C::kSP + (kk >> 2) * 64 + (kk & 3) * 8,
                    desc_sw128(do_addr + kk * 2048, kM * 128, 1024), idesc_acc, (m > 0 || kk > 0) ? 1u : 0u, leader);
           tc_commit(&bars->do_empty, leader);
-          mbar_wait(&bars->ds_ready, g & 1);  // dK_g += dS^T Q_g (TS: dS^T packed at SP + hf*64 + [32, 64))
+          mbar_wait_spin(&bars->ds_ready, g & 1);  // dK_g += dS^T Q_g (TS: dS^T packed at SP + hf*64 + [32, 64))
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
@@ -1473,14 +1473,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
           } else {
             have_nx = next_item(nx);
             if (have_nx) {
-              mbar_wait(&bars->v_full, (t + 1) & 1);
+              mbar_wait_spin(&bars->v_full, (t + 1) & 1);
               issue_dpt(g + 1);
               a_issued = true;
             }
           }
           // dQ_g = dS_g K  (SS: A = dS MN-major; B = K MN-major)
-          mbar_wait(&bars->dsm_ready, g & 1);
-          if (g > 0) mbar_wait(&bars->dq_free, (g - 1) & 1);
+          mbar_wait_spin(&bars->dsm_ready, g & 1);
+          if (g > 0) mbar_wait_spin(&bars->dq_free, (g - 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < B / 16; ++kk)
@@ -1536,7 +1536,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
           }
         };
         if (m > 0) {
-          mbar_wait(&bars->sp_full, 0);
+          mbar_wait_spin(&bars->sp_full, 0);
           tc_fence_after();
 #pragma unroll
           for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, ta[c2]);
@@ -1544,20 +1544,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
           tc_fence_before();
           mbar_arrive(&bars->sp_free);
           exp_p();
-          mbar_wait(&bars->sp_full, 1);
+          mbar_wait_spin(&bars->sp_full, 1);
           tc_fence_after();
 #pragma unroll
           for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, tb[c2]);
           tmem_wait_ld();
         } else {
-          mbar_wait(&bars->sp_full, 0);
+          mbar_wait_spin(&bars->sp_full, 0);
           tc_fence_after();
 #pragma unroll
           for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, tb[c2]);
           tmem_wait_ld();
           tc_fence_before();
           mbar_arrive(&bars->sp_free);
-          mbar_wait(&bars->sp_full, 1);
+          mbar_wait_spin(&bars->sp_full, 1);
           tc_fence_after();
 #pragma unroll
           for (int c2 = 0; c2 < HB / 32; ++c2) tmem_ld32(sp + c2 * 32, ta[c2]);
