@@ -433,8 +433,8 @@ def main():
     ap.add_argument("--grid", default="dense", choices=["dense", "default"],
                     help="c3 DST budget grid: dense 1..256 (SURVEY 7.3(5), the 1.05x balance target) or the "
                          "reference's default 16 points")
-    ap.add_argument("--bwd", default="fused", choices=["fused", "two-pass"],
-                    help="backward: fused single pass (d = B = 128) or the bit-deterministic two-pass")
+    ap.add_argument("--bwd", default="two-pass", choices=["fused", "two-pass"],
+                    help="backward: the bit-deterministic two-pass (default) or the opt-in fused single pass")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sub", action="store_true", help="skip the N=1 C1 / C2 / C5 sub-records")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
@@ -511,7 +511,7 @@ def main():
         if args.grid == "dense":
             dst_cfg.budget_grid = list(range(1, 257))
         runner = dp.DPStep(dp.RankBatch(np.asarray(mine), ids, lay), q, k, v, do, layer_scales, table, dst_cfg,
-                           rank=rank, world=world, deterministic=args.bwd == "two-pass")
+                           rank=rank, world=world, fused_bwd=args.bwd == "fused")
         config = {"workload": c3_label(world, args.layers, table_src), "dst_grid": args.grid, "bwd": args.bwd,
                   "tokens_per_rank": [int(sum(int(lengths_all[i]) for i in b[0])) for b in bins],
                   "members_rank0": [int(lengths_all[i]) for i in bins[0][0]]}

@@ -141,12 +141,16 @@ int sb_sparse_attn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                        int k_max, float scale, uint16_t* dq, uint16_t* dk, uint16_t* dv,
                        void* workspace, void* stream);
 
-/* K6 with flags. SB_BWD_DETERMINISTIC selects the two-pass backward (dK/dV pass over the
- * transposed selection, then a dQ pass; 7 UMMAs per pair; bit-identical run to run). Without it,
- * D = B = 128 runs the fused single pass (5 UMMAs per pair; dQ partials TMA-reduce-added in fp32,
- * so dQ is reproducible to fp32 summation order) and other shapes the two-pass kernels.
- * sb_sparse_attn_bwd == sb_sparse_attn_bwd_ex(..., flags = 0). Same workspace size. */
+/* K6 with flags. Default (flags = 0) and SB_BWD_DETERMINISTIC: the two-pass backward (dK/dV
+ * pass over the transposed selection, then a dQ pass; 7 UMMAs per pair; bit-identical run to
+ * run). SB_BWD_FUSED (d = B = 128 only; other shapes ignore it): the single pass with 5 UMMAs per
+ * pair whose dQ partials are TMA-reduce-added in fp32 (reproducible to summation order). On B200
+ * the fused pass is shared-memory-bandwidth bound (SS dQ operands + fp32 dQ staging: ~480 KB of
+ * shared-memory traffic per pair vs ~420 KB for both two-pass kernels together, K6) and
+ * measures slower, so it is opt-in. sb_sparse_attn_bwd == sb_sparse_attn_bwd_ex(..., flags = 0).
+ * Same workspace size. */
 #define SB_BWD_DETERMINISTIC 1
+#define SB_BWD_FUSED 2
 int sb_sparse_attn_bwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                           const uint16_t* o, const uint16_t* o_res /* may be NULL */,
                           const uint16_t* d_o, const float* lse,

@@ -1755,10 +1755,10 @@ template <int D, int B>
 void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o,
                 const uint16_t* ores, const float* lse, const int32_t* cu, const int32_t* blk_off, int nseq, int total, int nb_total, int hq,
                 int hkv, const int32_t* idx, const int32_t* cnt, int hsel, int k_max, float scale, uint16_t* dq,
-                uint16_t* dk, uint16_t* dv, uint8_t* ws, cudaStream_t st, bool deterministic) {
+                uint16_t* dk, uint16_t* dv, uint8_t* ws, cudaStream_t st, bool fused_requested) {
   const BwdWorkspace w = bwd_layout(total, nb_total, hq, hkv, hsel, k_max);
   constexpr bool kFusable = D == 128 && B == 128;
-  const bool fused = kFusable && !deterministic;
+  const bool fused = kFusable && fused_requested;
   float* lse2 = reinterpret_cast<float*>(ws + w.lse2);
   float* dvec = reinterpret_cast<float*>(ws + w.dvec);
   int32_t* tr_cnt = reinterpret_cast<int32_t*>(ws + w.tr_cnt);
@@ -1897,7 +1897,9 @@ SB_API int sb_sparse_attn_bwd_ex(const uint16_t* q, const uint16_t* k, const uin
     sbk::require(hsel >= hkv && hq % hsel == 0 && hsel % hkv == 0,
                  "hsel must divide hq and be a multiple of hkv (each selection row maps to one kv head)");
     sbk::require(k_max >= 1, "k_max must be >= 1");
-    sbk::require((flags & ~SB_BWD_DETERMINISTIC) == 0, "unknown flags");
+    sbk::require((flags & ~(SB_BWD_DETERMINISTIC | SB_BWD_FUSED)) == 0, "unknown flags");
+    sbk::require((flags & SB_BWD_DETERMINISTIC) == 0 || (flags & SB_BWD_FUSED) == 0,
+                 "SB_BWD_FUSED is not deterministic (dQ is reduce-added in fp32)");
     if (nseq == 0 || nb_total == 0 || total_tokens == 0) return;
     sbk::require(q && k && v && o && d_o && lse && cu_seqlens && blk_off && idx && cnt && dq && dk && dv && workspace,
                  "null pointer");
@@ -1908,7 +1910,7 @@ SB_API int sb_sparse_attn_bwd_ex(const uint16_t* q, const uint16_t* k, const uin
                  "q/k/v/o/o_res/dO/dQ/dK/dV/workspace must be 16-byte aligned");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint8_t* ws = static_cast<uint8_t*>(workspace);
-    const bool det = (flags & SB_BWD_DETERMINISTIC) != 0;
+    const bool det = (flags & SB_BWD_FUSED) != 0;  // fused requested (the default two-pass is deterministic)
     if (block_size == 256) {  // workspace: sb_sparse_attn_bwd_workspace_size_ex
       const sbk::Expanded256 e =
           sbk::expand_selection_256(cu_seqlens, blk_off, nseq, nb_total, hsel, idx, cnt, k_max, ws, st);

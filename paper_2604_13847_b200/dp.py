@@ -213,7 +213,7 @@ class DPStep:
 
     def __init__(self, batch: RankBatch, q, k, v, do, layer_scales, table: ProfileTable, cfg: DstSettings,
                  rank: int = 0, world: int = 1, group=None, pooled_xs=None, max_members: int = 0,
-                 varlen_block_size: int = 0, deterministic: bool = False):
+                 varlen_block_size: int = 0, fused_bwd: bool = False):
         self.batch, self.q, self.k, self.v, self.do = batch, q, k, v, do
         self.layer_scales = list(layer_scales)
         self.table, self.cfg = table, cfg
@@ -223,7 +223,7 @@ class DPStep:
         self.block = batch.layout.block_size
         self.max_members = max(max_members, len(batch.lengths)) if varlen_block_size else 0
         self.varlen_block_size = varlen_block_size
-        self.deterministic = deterministic  # backward: bit-deterministic two-pass instead of the fused pass
+        self.fused_bwd = fused_bwd  # backward: the opt-in fused single pass instead of the two-pass
         self.last = {}
         # On-device DST (fixed-base mode): with every rank's micro-batch
         # summed length known (the SAB plan is deterministic on every rank), the host half
@@ -311,7 +311,7 @@ class DPStep:
             if mark:
                 mark("fwd")
             grads = (ops.sparse_attn_bwd(self.q, self.k, self.v, o, self.do, lse, lay, idx, cnt, scale,
-                                         deterministic=self.deterministic) if backward else None)
+                                         fused=self.fused_bwd) if backward else None)
             if mark:
                 mark("bwd")
             if grad_buckets is not None and self.world > 1:
@@ -351,7 +351,7 @@ class DPStep:
             if mark:
                 mark("fwd")
             grads = (ops.sparse_attn_bwd(self.q, self.k, self.v, o, self.do, lse, lay, idx, cnt, scale,
-                                         deterministic=self.deterministic) if backward else None)
+                                         fused=self.fused_bwd) if backward else None)
             if mark:
                 mark("bwd")
             if grad_buckets is not None and self.world > 1:

@@ -288,12 +288,14 @@ def sparse_attn_fwd(q, k, v, lay: VarlenLayout, idx, cnt, scale: float | None = 
 
 
 SB_BWD_DETERMINISTIC = 1
+SB_BWD_FUSED = 2
 
 
 def sparse_attn_bwd(q, k, v, o, do, lse, lay: VarlenLayout, idx, cnt, scale: float | None = None,
-                    deterministic: bool = False, o_res=None):
-    """K6: (dQ, dK, dV) bf16. Default: the fused single pass for d = B = 128 (dQ reduce-added in
-    fp32, reproducible to summation order); deterministic=True: the bit-deterministic two-pass."""
+                    o_res=None, fused: bool = False):
+    """K6: (dQ, dK, dV) bf16. Default: the bit-deterministic two-pass backward. fused=True (d = B
+    = 128): the single pass with dQ reduce-added in fp32 (reproducible to summation order; opt-in,
+    it measures slower on B200, see sb_kernels.h)."""
     _need_cuda(q, k, v, o, do, lse, idx, cnt)
     _need_qkv(q, k, v, lay)
     _need_sel(idx, cnt, lay)
@@ -316,7 +318,7 @@ def sparse_attn_bwd(q, k, v, o, do, lse, lay: VarlenLayout, idx, cnt, scale: flo
     _call("sb_sparse_attn_bwd_ex", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(o_res), _ptr(do), _ptr(lse),
           _ptr(lay.cu_seqlens), _ptr(lay.blk_off), lay.nseq, T, lay.nb_total, Hq, Hkv, D, lay.block_size, _ptr(idx),
           _ptr(cnt), hsel, k_max, C.c_float(scale), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), _stream(),
-          SB_BWD_DETERMINISTIC if deterministic else 0)
+          SB_BWD_FUSED if fused else SB_BWD_DETERMINISTIC)
     return dq, dk, dv
 
 
@@ -324,18 +326,18 @@ class SparseAttention(torch.autograd.Function):
     """Autograd wrapper: forward = K5, backward = K6 (recompute from the saved LSE)."""
 
     @staticmethod
-    def forward(ctx, q, k, v, lay, idx, cnt, scale, deterministic=False):
+    def forward(ctx, q, k, v, lay, idx, cnt, scale, fused=False):
         o, lse = sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
         ctx.save_for_backward(q, k, v, o, lse, idx, cnt)
-        ctx.lay, ctx.scale, ctx.deterministic = lay, scale, deterministic
+        ctx.lay, ctx.scale, ctx.fused = lay, scale, fused
         return o
 
     @staticmethod
     def backward(ctx, do):
         q, k, v, o, lse, idx, cnt = ctx.saved_tensors
-        dq, dk, dv = sparse_attn_bwd(q, k, v, o, do, lse, ctx.lay, idx, cnt, ctx.scale, ctx.deterministic)
+        dq, dk, dv = sparse_attn_bwd(q, k, v, o, do, lse, ctx.lay, idx, cnt, ctx.scale, fused=ctx.fused)
         return dq, dk, dv, None, None, None, None, None
 
 
-def sparse_attention(q, k, v, lay, idx, cnt, scale=None, deterministic=False):
-    return SparseAttention.apply(q, k, v, lay, idx, cnt, scale, deterministic)
+def sparse_attention(q, k, v, lay, idx, cnt, scale=None, fused=False):
+    return SparseAttention.apply(q, k, v, lay, idx, cnt, scale, fused)

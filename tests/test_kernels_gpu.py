@@ -244,15 +244,15 @@ def test_bwd_deterministic():
     lay = _layout(cu, 128)
     idx, cnt = _selection(lay, 4, 0.5, 3)
     o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)
-    a = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, deterministic=True)
-    b = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, deterministic=True)
+    a = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
+    b = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
     for x, y in zip(a, b):
         assert torch.equal(x, y)
 
 
 def test_fused_bwd_vs_two_pass():
-    """d = B = 128: the fused single pass (default) against the deterministic two-pass on the same
-    inputs: dK / dV accumulate in TMEM in a fixed order (bit-identical run to run); dQ is
+    """d = B = 128: the opt-in fused single pass against the default deterministic two-pass on the
+    same inputs: dK / dV accumulate in TMEM in a fixed order (bit-identical run to run); dQ is
     reduce-added in fp32 across key blocks, so it agrees to fp32 summation order."""
     from paper_2604_13847_b200 import ops
 
@@ -263,9 +263,9 @@ def test_fused_bwd_vs_two_pass():
     lay = _layout(cu, 128)
     idx, cnt = _selection(lay, 2, 0.4, 5)
     o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)
-    f1 = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
-    f2 = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
-    det = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, deterministic=True)
+    f1 = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, fused=True)
+    f2 = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, fused=True)
+    det = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
     assert torch.equal(f1[1], f2[1]) and torch.equal(f1[2], f2[2])
     for a, b, name in zip(f1, det, ("dq", "dk", "dv")):
         a, b = a.float(), b.float()
@@ -359,7 +359,7 @@ def test_block_256_fwd_bwd_vs_oracle(cu, hq, hkv, d, keep):
     check_bf16(o, ro, "o")
     np.testing.assert_allclose(lse.cpu().numpy(), rlse, atol=2e-3, rtol=1e-4)
     rdq, rdk, rdv = orc.sparse_attn_bwd(_bits(q), _bits(k), _bits(v), ro, _bits(do), rlse, cu, B, ic, cc, scale)
-    for det in (False, True):
-        dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale, deterministic=det)
+    for fused in (False, True):
+        dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale, fused=fused)
         for got, ref, name in ((dq, rdq, "dq"), (dk, rdk, "dk"), (dv, rdv, "dv")):
-            check_bf16(got, ref, f"{name} det={det}")
+            check_bf16(got, ref, f"{name} fused={fused}")

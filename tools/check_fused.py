@@ -23,10 +23,10 @@ def run(cu, hq, hkv, keep, seed):
     o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
     torch.cuda.synchronize()
     t0 = time.time()
-    dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+    dq, dk, dv = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale, fused=True)
     torch.cuda.synchronize()
     print(f"fused bwd done in {time.time() - t0:.3f}s", flush=True)
-    dq2, dk2, dv2 = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale, deterministic=True)
+    dq2, dk2, dv2 = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
     torch.cuda.synchronize()
     ic, cc = idx.cpu().numpy(), cnt.cpu().numpy()
     ro, rlse = orc.sparse_attn_fwd(bits(q), bits(k), bits(v), cu, B, ic, cc, scale)
