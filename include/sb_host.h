@@ -80,6 +80,18 @@ int SBH(tune_global_batch_cov)(const int64_t* bins, int nx, const int* grid, int
                                const int64_t* mem_len, const int64_t* mem_off, int varlen_block_size, int layer,
                                double threshold_p, int anchor, const int* dst_grid, int n_dst_grid, int* out_i,
                                double* out_d);
+/* The same two steps batched for a DP rank / step: rank_estimate = make_micro_batch +
+ * (coverage-mode) intrinsic_budget + a coverage table per layer (profiles member-major,
+ * profiles[s * nl + l]; out_cov[nl][n_grid + 1]); tune_layers_cov = tune_global_batch_cov
+ * for layers 0..nl-1 (cov[n_mb][nl][n_dst_grid + 1] -> out_k_final[n_mb][nl], out_i[nl][n_mb][5],
+ * out_d[nl][n_mb][3]). */
+int SBH(rank_estimate)(int ns, const int64_t* lengths, int nl, const double* profiles, const int64_t* off,
+                       const int* grid, int n_grid, int coverage_mode, int base_budget, double coverage_target,
+                       int64_t* out_x, int* out_k_base, double* out_cov);
+int SBH(tune_layers_cov)(const int64_t* bins, int nx, const int* grid, int nk, const double* lat, int n_mb,
+                         const int64_t* x, const int* k_base, const double* cov, const int64_t* mem_len,
+                         const int64_t* mem_off, int varlen_block_size, int nl, double threshold_p, int anchor,
+                         const int* dst_grid, int n_dst_grid, int* out_k_final, int* out_i, double* out_d);
 #endif
 int SBH(coverage_budget)(const double* scores, int m, double target, int* out);
 int SBH(intrinsic_budget)(int nl, const double* profiles, const int64_t* off, const int* grid,

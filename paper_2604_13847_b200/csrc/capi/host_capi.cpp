@@ -240,6 +240,91 @@ SB_EXPORT int SBH(coverage_table)(const double* scores, int m, const int* grid, 
   });
 }
 
+// One DP rank's whole workload estimate in one call: make_micro_batch over the members'
+// per-layer profiles (member-major: profiles[s * nl + l] at off[...]), the base budget
+// (coverage mode: intrinsic_budget, else `base_budget`) and per layer the coverage table
+// out_cov[l][n_grid + 1] (grid points, then k_base).
+SB_EXPORT int SBH(rank_estimate)(int ns, const int64_t* lengths, int nl, const double* profiles, const int64_t* off,
+                                 const int* grid, int n_grid, int coverage_mode, int base_budget,
+                                 double coverage_target, int64_t* out_x, int* out_k_base, double* out_cov) {
+  return guarded([&] {
+    const auto mb = sb::make_micro_batch(make_samples(ns, nullptr, lengths, nl, profiles, off));
+    const std::span<const int> g(grid, static_cast<std::size_t>(n_grid));
+    const int kb = coverage_mode ? sb::intrinsic_budget(mb, g, coverage_target) : base_budget;
+    *out_x = mb.length_descriptor;
+    *out_k_base = kb;
+    for (int l = 0; l < nl; ++l) {
+      const auto t = sb::coverage_table(mb.merged_profiles[static_cast<std::size_t>(l)], g, kb);
+      double* row = out_cov + static_cast<std::size_t>(l) * static_cast<std::size_t>(n_grid + 1);
+      for (int i = 0; i < n_grid; ++i) row[i] = t.values[static_cast<std::size_t>(i)];
+      row[n_grid] = t.at(kb);
+    }
+  });
+}
+
+// tune_global_batch_cov for every layer at once: cov[n_mb][nl][n_dst_grid + 1];
+// out_k_final[n_mb][nl]; out_i[nl][n_mb][5] / out_d[nl][n_mb][3] as tune_global_batch's.
+SB_EXPORT int SBH(tune_layers_cov)(const int64_t* bins, int nx, const int* grid, int nk, const double* lat, int n_mb,
+                                   const int64_t* x, const int* k_base, const double* cov, const int64_t* mem_len,
+                                   const int64_t* mem_off, int varlen_block_size, int nl, double threshold_p,
+                                   int anchor, const int* dst_grid, int n_dst_grid, int* out_k_final, int* out_i,
+                                   double* out_d) {
+  return guarded([&] {
+    const auto table = make_table(bins, nx, grid, nk, lat);
+    sb::DstConfig cfg;
+    cfg.threshold_p = threshold_p;
+    cfg.anchor = anchor_of(anchor);
+    cfg.budget_grid.assign(dst_grid, dst_grid + n_dst_grid);
+    cfg.varlen_block_size = varlen_block_size;
+    sb::validate_dst_config(cfg);
+    if (varlen_block_size > 0 && (mem_len == nullptr || mem_off == nullptr))
+      throw sb::ConfigError("tune_layers_cov: varlen cost needs member lengths");
+    sb::GlobalBatch gb;
+    for (int i = 0; i < n_mb; ++i) {
+      sb::MicroBatch mb;
+      mb.length_descriptor = x[i];
+      if (mem_len != nullptr && mem_off != nullptr)
+        for (int64_t e = mem_off[i]; e < mem_off[i + 1]; ++e) {
+          sb::Sample smp;
+          smp.id = e;
+          smp.length = mem_len[e];
+          mb.samples.push_back(std::move(smp));
+        }
+      gb.micro_batches.push_back(std::move(mb));
+      gb.base_budgets.push_back(k_base[i]);
+    }
+    const std::size_t G = static_cast<std::size_t>(n_dst_grid) + 1;
+    std::vector<sb::CoverageTable> tabs(static_cast<std::size_t>(n_mb));
+    for (int l = 0; l < nl; ++l) {
+      for (int i = 0; i < n_mb; ++i) {
+        const double* row = cov + (static_cast<std::size_t>(i) * static_cast<std::size_t>(nl) +
+                                   static_cast<std::size_t>(l)) * G;
+        auto& t = tabs[static_cast<std::size_t>(i)];
+        t.budgets.assign(dst_grid, dst_grid + n_dst_grid);
+        t.values.assign(row, row + n_dst_grid);
+        t.budgets.push_back(k_base[i]);
+        t.values.push_back(row[n_dst_grid]);
+      }
+      const auto res = sb::tune_global_batch_cov(gb, tabs, l, cfg, table);
+      for (std::size_t i = 0; i < res.decisions.size(); ++i) {
+        const auto& d = res.decisions[i];
+        out_k_final[i * static_cast<std::size_t>(nl) + static_cast<std::size_t>(l)] = d.k_final;
+        const std::size_t o = static_cast<std::size_t>(l) * static_cast<std::size_t>(n_mb) + i;
+        int* oi = out_i + 5 * o;
+        oi[0] = d.micro_batch_id;
+        oi[1] = d.k_base;
+        oi[2] = d.k_anchor;
+        oi[3] = d.k_final;
+        oi[4] = direction_code(d.direction);
+        double* od = out_d + 3 * o;
+        od[0] = d.coverage_drop;
+        od[1] = d.predicted_ms_base;
+        od[2] = d.predicted_ms_final;
+      }
+    }
+  });
+}
+
 SB_EXPORT int SBH(tune_global_batch_cov)(const int64_t* bins, int nx, const int* grid, int nk, const double* lat,
                                          int n_mb, const int64_t* x, const int* k_base, const double* cov,
                                          const int64_t* mem_len, const int64_t* mem_off, int varlen_block_size,

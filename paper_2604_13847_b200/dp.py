@@ -86,16 +86,13 @@ class RankEstimate:
 def rank_estimate(lengths, layer_profiles: List[List[np.ndarray]], cfg: DstSettings) -> RankEstimate:
     """Local half of the exchange: merge this rank's member profiles exactly as the reference's
     make_micro_batch (workload.cpp:64-99), take the coverage-mode base budget over all layers
-    (intrinsic_budget, workload.cpp:389-411; sim.cpp:321-326) and tabulate C(k) per layer.
-    layer_profiles[l][s] = member s's profile at layer l."""
-    h = api()
-    grid = np.asarray(cfg.budget_grid, np.int32)
+    (intrinsic_budget, workload.cpp:389-411; sim.cpp:321-326) and tabulate C(k) per layer (one
+    native call). layer_profiles[l][s] = member s's profile at layer l."""
     L = len(layer_profiles)
     per_member = [[layer_profiles[l][s] for l in range(L)] for s in range(len(lengths))]
-    x, merged = h.make_micro_batch(np.asarray(lengths, np.int64), per_member)
-    k_base = h.intrinsic_budget(merged, grid, cfg.coverage_target) if cfg.base_mode == "coverage" else cfg.base_budget
-    cov = np.stack([h.coverage_table(merged[l], grid, k_base) for l in range(L)]) if L else np.zeros((0, len(grid) + 1))
-    return RankEstimate(int(x), int(k_base), cov, np.asarray(lengths, np.int64))
+    x, k_base, cov = api().rank_estimate(np.asarray(lengths, np.int64), per_member, cfg.budget_grid,
+                                         cfg.base_mode == "coverage", cfg.base_budget, cfg.coverage_target)
+    return RankEstimate(x, k_base, cov, np.asarray(lengths, np.int64))
 
 
 def pack_estimate(est: RankEstimate, num_layers: int, n_grid: int, max_members: int = 0) -> torch.Tensor:
@@ -141,23 +138,15 @@ def exchange_estimates(est: RankEstimate, num_layers: int, n_grid: int, world: i
 
 def decide_budgets_cov(pooled: List[RankEstimate], table: ProfileTable, cfg: DstSettings, num_layers: int,
                        varlen_block_size: int = 0):
-    """Pooled host DST from the exchanged estimates: k_final[rank][layer] and the decisions,
-    bit-identical to decide_budgets on the underlying profiles (tune_global_batch_cov)."""
-    h = api()
-    grid = np.asarray(cfg.budget_grid, np.int32)
-    xs = [e.x for e in pooled]
-    k_base = [e.k_base for e in pooled]
+    """Pooled host DST from the exchanged estimates (one native call for all layers): k_final
+    [rank][layer] and the decisions, bit-identical to decide_budgets on the underlying profiles
+    (tune_global_batch_cov)."""
     mem = [e.members for e in pooled] if varlen_block_size else None
-    k_final = np.zeros((len(pooled), num_layers), np.int32)
-    decisions = []
-    for l in range(num_layers):
-        ds = h.tune_global_batch_cov(table, xs, k_base, [e.cov[l] for e in pooled], layer=l,
-                                     threshold_p=cfg.threshold_p, anchor=cfg.anchor, budget_grid=grid,
-                                     member_lengths=mem, varlen_block_size=varlen_block_size)
-        for d in ds:
-            k_final[d.micro_batch_id, l] = d.k_final
-        decisions.extend(ds)
-    return k_final, decisions, np.asarray(k_base), np.asarray(xs)
+    cov = np.stack([e.cov for e in pooled]) if pooled else np.zeros((0, num_layers, len(cfg.budget_grid) + 1))
+    k_final, decisions = api().tune_layers_cov(table, [e.x for e in pooled], [e.k_base for e in pooled], cov,
+                                               cfg.budget_grid, threshold_p=cfg.threshold_p, anchor=cfg.anchor,
+                                               member_lengths=mem, varlen_block_size=varlen_block_size)
+    return k_final, decisions, np.asarray([e.k_base for e in pooled]), np.asarray([e.x for e in pooled])
 
 
 def decide_budgets(pooled, table: ProfileTable, cfg: DstSettings, num_layers: int):

@@ -229,6 +229,48 @@ class HostAPI:
                                 float(d[0]), float(d[1]), float(d[2])))
         return out
 
+    def rank_estimate(self, lengths, per_member_profiles, budget_grid, coverage_mode: bool = True,
+                      base_budget: int = 32, coverage_target: float = 0.9):
+        """Batched make_micro_batch + intrinsic_budget + per-layer coverage tables:
+        per_member_profiles[s][l] -> (x, k_base, cov [L, len(grid) + 1])."""
+        ns = len(lengths)
+        nl = len(per_member_profiles[0]) if ns else 0
+        flat, off = _flatten([p for m in per_member_profiles for p in m])
+        grid = _a(budget_grid, np.int32)
+        x, kb = C.c_int64(), C.c_int()
+        cov = np.zeros((nl, len(grid) + 1), np.float64)
+        self._call("rank_estimate", ns, _p(_a(lengths, np.int64)), nl, _p(flat), _p(off), _p(grid), len(grid),
+                   1 if coverage_mode else 0, int(base_budget), C.c_double(coverage_target), C.byref(x), C.byref(kb),
+                   _p(cov))
+        return int(x.value), int(kb.value), cov
+
+    def tune_layers_cov(self, table: ProfileTable, x, k_base, cov, budget_grid, threshold_p: float = 0.1,
+                        anchor: str = "min", member_lengths=None, varlen_block_size: int = 0):
+        """tune_global_batch_cov for every layer: cov [n_mb, L, len(grid) + 1] ->
+        (k_final [n_mb, L], decisions in layer-major order)."""
+        cov = _a(np.asarray(cov, np.float64), np.float64)
+        n, nl = cov.shape[0], cov.shape[1]
+        grid = _a(budget_grid, np.int32)
+        ml = mo = None
+        if member_lengths is not None:
+            mo = _a(np.concatenate([[0], np.cumsum([len(m) for m in member_lengths])]), np.int64)
+            flat = [int(v) for m in member_lengths for v in m]
+            ml = _a(flat if flat else [0], np.int64)
+        kf = np.zeros((n, nl), np.int32)
+        oi = np.zeros(5 * n * nl, np.int32)
+        od = np.zeros(3 * n * nl, np.float64)
+        self._call("tune_layers_cov", *table.args(), n, _p(_a(x, np.int64)), _p(_a(k_base, np.int32)), _p(cov),
+                   None if ml is None else _p(ml), None if mo is None else _p(mo), int(varlen_block_size), nl,
+                   C.c_double(threshold_p), ANCHORS[anchor], _p(grid), len(grid), _p(kf), _p(oi), _p(od))
+        out = []
+        for l in range(nl):
+            for i in range(n):
+                o = l * n + i
+                a, d = oi[5 * o:5 * o + 5], od[3 * o:3 * o + 3]
+                out.append(Decision(int(a[0]), l, int(a[1]), int(a[2]), int(a[3]), DIRECTIONS[a[4]], float(d[0]),
+                                    float(d[1]), float(d[2])))
+        return kf, out
+
     # ---- workload.hpp ------------------------------------------------------------------
     def make_micro_batch(self, lengths: Sequence[int], profiles: Sequence[Sequence[np.ndarray]]):
         """profiles[s][l] -> (length_descriptor, merged[l])."""
