@@ -420,6 +420,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
       if (items == 0) continue;
       const int kv0 = w.seq0 + w.jl * B;
       if (lane == 0) {
+        // L2 prefetch of the next non-empty item's K / V: short items (small keep counts) would
+        // otherwise expose a DRAM round trip at every item boundary (single K / V buffer).
+        for (int k2 = k + 1; k2 < k + 4; ++k2) {
+          const int it2 = sched::snake_item(order, n_items, grid, cta, k2);
+          if (it2 < 0) break;
+          const KvItem w2 = decode_kv(it2, cu, blk_off, nseq, nbt, tr_off);
+          if (w2.ne == 0) continue;
+          const int kv2 = w2.seq0 + w2.jl * B;
+          for (int c = 0; c < C::kChunks; ++c) {
+            tma_prefetch_l2_3d(&tm_k, c * 64, w2.hk, kv2);
+            tma_prefetch_l2_3d(&tm_v, c * 64, w2.hk, kv2);
+          }
+          break;
+        }
         mbar_wait(&bars->kv_empty, (t & 1) ^ 1);
         mbar_expect_tx(&bars->kv_full, 2 * C::kTileBytes);
         for (int c = 0; c < C::kChunks; ++c) {

@@ -208,6 +208,18 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
           const Item w = from_rec(rec, nbt, idx, k_max);
           if (w.n <= 0) continue;
           const int hk = w.h / (hq / hkv);
+          {  // L2 prefetch of this stream's next item's Q tile: its load waits for this item's last
+             // QK, so with few blocks per item a DRAM round trip would sit on the stream's chain
+            sched::RecCursor peek = cur;
+            for (int e = 0; e < 4; ++e) {
+              const sched::ItemRec nr = peek.next();
+              if (nr.it < 0) break;
+              if (nr.n <= 0) continue;
+              for (int c = 0; c < C::kChunks; ++c)
+                tma_prefetch_l2_3d(&tm_q, c * 64, nr.it / nbt, nr.seq0 + nr.loc * B);
+              break;
+            }
+          }
           mbar_wait_spin(&bars->q_empty[s], (q & 1) ^ 1);
           mbar_expect_tx(&bars->q_full[s], C::kQBytes);
           for (int c = 0; c < C::kChunks; ++c)

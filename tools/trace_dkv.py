@@ -6,7 +6,12 @@ from paper_2604_13847_b200 import ops
 import bench
 lib = ops._lib()
 lib.sb_debug_set_trace_bwd.argtypes = [ctypes.c_void_p]
-cu, k_seq = bench.workload(0)
+if os.environ.get("C3K"):  # C3 rank micro-batch [2048 x3, 32768, 2048] at a fixed keep count
+    lens = [2048, 2048, 2048, 32768, 2048]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    k_seq = np.minimum(int(os.environ["C3K"]), (np.array(lens) + 127) // 128).astype(np.int32)
+else:
+    cu, k_seq = bench.workload(0)
 T = int(cu[-1]); H, D, B = 32, 128, 128
 lay = ops.VarlenLayout.build(cu, B)
 g = torch.Generator(device="cuda").manual_seed(0)
