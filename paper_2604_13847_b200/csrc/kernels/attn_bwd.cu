@@ -139,6 +139,7 @@ __global__ void transpose_sel_kernel(const int32_t* __restrict__ idx, const int3
       key = hs * nbt + gi;
     }
     const uint32_t m = __ballot_sync(0xffffffffu, hit);
+    SB_DCHECK(!pass || !hit || found + __popc(m & ((1u << lane) - 1u)) < tr_off[w + 1] - tr_off[w]);
     if (pass && hit) dst[found + __popc(m & ((1u << lane) - 1u))] = key;
     found += __popc(m);
   }
@@ -748,6 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
             for (int e = 0; e < 32; ++e) v[e] = 0u;
           }
           if (store) {
+            SB_DCHECK(kv0 + c < cu[nseq]);
             uint32_t w16[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e)
@@ -1163,6 +1165,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         }
       } else {
         if (valid) {  // the last (partial) tile of a sequence: a box would cross into the next
+          SB_DCHECK(row0 + r < cu[nseq]);
 #pragma unroll
           for (int cc = 0; cc < D / 64; ++cc) {
             uint32_t w16[16];

@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
         }
         if (store) lse[static_cast<size_t>(w.h) * total_tokens + row0 + r] = (m_run + log2f(l_run)) * 0.69314718055994531f;
       } else if (store) {  // the last (partial) tile of a sequence: a box would cross into the next
+        SB_DCHECK(row0 + r < total_tokens);
         for (int part = 0; part < parts; ++part) {
           uint16_t* orow = (part ? ores : out) + (static_cast<size_t>(row0 + r) * hq + w.h) * D;
 #pragma unroll

@@ -87,6 +87,19 @@ size_t expand256_workspace_bytes(int nseq, int nb256, int hsel, int k_max);
 Expanded256 expand_selection_256(const int32_t* cu, const int32_t* blk_off256, int nseq, int nb256, int hsel,
                                  const int32_t* idx, const int32_t* cnt, int k_max, uint8_t* ws, cudaStream_t st);
 
+// Debug builds (`make debug`: -DSB_DEBUG_CHECKS) trap on a violated index invariant at the
+// kernels' global store sites (compute-sanitizer is not available on the B200 pool).
+#ifdef SB_DEBUG_CHECKS
+#define SB_DCHECK(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define SB_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 // Sequence owning global block gi (binary search in blk_off[0..nseq]).
 __device__ __forceinline__ int seq_of_block(const int32_t* blk_off, int nseq, int gi) {
   int lo = 0, hi = nseq;  // blk_off[lo] <= gi < blk_off[hi]

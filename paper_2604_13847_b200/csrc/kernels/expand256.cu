@@ -54,6 +54,7 @@ __global__ void expand_kernel(const int32_t* __restrict__ cu, const int32_t* __r
       }
     }
   }
+  SB_DCHECK(n <= 2 * k_max);
   cnt128[static_cast<size_t>(hs) * nb128 + ga] = n;
   for (int e = n; e < 2 * k_max; ++e) out[e] = -1;
 }

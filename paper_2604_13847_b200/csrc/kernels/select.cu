@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(256) topk_select_warp_kernel(
   // k_seq > k_max gets k_max blocks, never writes past its row).
   const int k = max(1, min(min(k_seq[s], n), k_max));
   int32_t* out = idx + (static_cast<size_t>(g) * nbt + gi) * k_max;
+  SB_DCHECK(k >= 1 && k <= k_max && gi < nbt);
   if (lane == 0) cnt[static_cast<size_t>(g) * nbt + gi] = k;
   const int m = force_diag ? n - 1 : n;     // candidate count
   const int want = force_diag ? k - 1 : k;  // candidates to keep
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(
   if (n <= kWarpRow) return;  // short rows: topk_select_warp_kernel
   const int k = max(1, min(min(k_seq[s], n), k_max));  // clamped as in topk_select_warp_kernel
   int32_t* out = idx + (static_cast<size_t>(g) * nbt + gi) * k_max;
+  SB_DCHECK(k >= 1 && k <= k_max && gi < nbt);
   if (threadIdx.x == 0) cnt[static_cast<size_t>(g) * nbt + gi] = k;
 
   const int m = force_diag ? n - 1 : n;   // candidate count
