@@ -3,10 +3,12 @@
 Replaces the reference's synthetic stand-in for hardware profiling (`synthesize_table`,
 proj/core/src/profile_table.cpp:145-166) and its fixed backward ratio (`fwd_bwd_ratio` = 2.0,
 sim.hpp:23, applied in micro_batch_time, sim.cpp:88-98) with measured latencies. For every
-(length x, budget k) cell it runs one layer of the real hot path on one packed sequence of x
-tokens with keep count k and times, with CUDA events (median of `reps` windows),
+(length x, budget k) cell it runs one layer of the real hot path on x tokens -- one sequence, or
+with --mix a packed micro-batch of the workload's length mix -- with keep count k (clamped per
+member) and times, with CUDA events (median of `reps` windows),
 
-  * fwd: block scorer (K1 + K2) + top-k selector (K3) + sparse attention forward (K5);
+  * fwd: block scorer (K1 + K2) + coverage profile (K4) + top-k selector (K3) + sparse attention
+    forward (K5);
   * bwd: sparse attention backward (K6, recompute from the saved LSE);
 
 and writes three CSVs in the reference schema `x,k,latency_ms` (profile_table.cpp:168-182):
@@ -16,6 +18,7 @@ cost the tuner balances. load_table() applies the reference's isotonic repair in
 
     python -m paper_2604_13847_b200.profiler --out profiles/b200_cost_table_h32_d128_b128
     python -m paper_2604_13847_b200.profiler --kv-heads 8 --out profiles/b200_cost_table_h32kv8_d128_b128
+    python -m paper_2604_13847_b200.profiler --mix 40/60 --out profiles/b200_cost_table_mix4060_h32_d128_b128
 """
 from __future__ import annotations
 
@@ -33,12 +36,13 @@ def measure_cell(q, k, v, do, lay, kk: int, reps: int, scale: float, group: int)
     """(fwd ms, bwd ms) medians over `reps` timed windows; each window enqueues `n` layers back to
     back (as the step driver does) and divides, so host launch overhead only counts where it
     exceeds the GPU work. n shrinks for large cells so every cell costs ~ the same wall time."""
-    k_seq = torch.full((lay.nseq,), kk, dtype=torch.int32, device=q.device)
+    k_seq = torch.from_numpy(np.minimum(kk, np.maximum(lay.nb_per_seq, 1)).astype(np.int32)).to(q.device)
     k_max = max(1, min(kk, lay.nb_max))
     state = {}
 
     def fwd():
         S = ops.block_scores(q, k, lay, scale)
+        ops.coverage_profile(S, lay)  # the tuner's profile (K4) is part of every layer of the closed-loop step
         idx, cnt = ops.topk_select(S, lay, k_seq, k_max, group=group)
         o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
         state.update(idx=idx, cnt=cnt, o=o, lse=lse)
@@ -71,9 +75,25 @@ def measure_cell(q, k, v, do, lay, kk: int, reps: int, scale: float, group: int)
     return out[0], out[1]
 
 
+def mix_lengths(x: int, long_len: int = 32768, short_len: int = 2048, long_frac: float = 0.4):
+    """A packed micro-batch of x tokens drawn from a long / short mix (the C3 / C4 workload: 40 %
+    32K / 60 % 2K by count): members appended long or short to keep the running long fraction at
+    long_frac, the last one truncated so the lengths sum to x exactly."""
+    out, n_long = [], 0
+    while sum(out) < x:
+        take_long = n_long / (len(out) + 1) < long_frac
+        n_long += take_long
+        out.append(min(long_len if take_long else short_len, x - sum(out)))
+    return out
+
+
 def profile_tables(length_bins=None, budget_grid=None, heads=32, kv_heads=32, head_dim=128, block=128, reps=3,
-                   seed=0, device="cuda"):
-    """-> (fwd, bwd, fwd + bwd) ProfileTables over the (length_bins x budget_grid) cells."""
+                   seed=0, device="cuda", mix=None):
+    """-> (fwd, bwd, fwd + bwd) ProfileTables over the (length_bins x budget_grid) cells. With
+    mix = (long_len, short_len, long_frac) every cell is a packed micro-batch of that mix
+    (mix_lengths) with the cell's keep count clamped per member, as the kernels run it; the
+    reference's predict(x = summed length, k) then prices packed micro-batches of that mix
+    directly. Without it, a cell is one sequence of x tokens (the reference's model)."""
     length_bins = list(DEFAULT_LENGTH_BINS if length_bins is None else length_bins)
     budget_grid = list(DEFAULT_BUDGET_GRID if budget_grid is None else budget_grid)
     g = torch.Generator(device=device).manual_seed(seed)
@@ -87,7 +107,8 @@ def profile_tables(length_bins=None, budget_grid=None, heads=32, kv_heads=32, he
     lf = np.zeros((len(length_bins), len(budget_grid)))
     lb = np.zeros_like(lf)
     for xi, x in enumerate(length_bins):
-        lay = ops.VarlenLayout.build([0, x], block, device=device)
+        lens = mix_lengths(x, *mix) if mix else [x]
+        lay = ops.VarlenLayout.build(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32), block, device=device)
         for ki, kk in enumerate(budget_grid):
             lf[xi, ki], lb[xi, ki] = measure_cell(q[:x], k[:x], v[:x], do[:x], lay, kk, reps, scale, group)
     bins = np.asarray(length_bins, np.int64)
@@ -115,12 +136,15 @@ def main():
     ap.add_argument("--block", type=int, default=128)
     ap.add_argument("--max-x", type=int, default=262144)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--mix", default=None, help="'40/60': cells are packed micro-batches of the 40%% 32K / 60%% 2K "
+                                                "mix (C3 / C4) instead of single sequences")
     args = ap.parse_args()
     if args.heads % args.kv_heads:
         ap.error("--heads must be a multiple of --kv-heads")
     prefix = args.out[:-4] if args.out.endswith(".csv") else args.out
     bins = [x for x in DEFAULT_LENGTH_BINS if x <= args.max_x]
-    fwd, bwd, tot = profile_tables(bins, None, args.heads, args.kv_heads, args.head_dim, args.block, args.reps)
+    mix = (32768, 2048, 0.4) if args.mix == "40/60" else None
+    fwd, bwd, tot = profile_tables(bins, None, args.heads, args.kv_heads, args.head_dim, args.block, args.reps, mix=mix)
     rep = write_tables(prefix, fwd, bwd, tot)
     ratio = bwd.latency_ms / np.maximum(fwd.latency_ms, 1e-9)
     for p, r in rep.items():

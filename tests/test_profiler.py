@@ -48,3 +48,15 @@ def test_profiler_measures_fwd_and_bwd(tmp_path):
     assert fwd.latency_ms[1, 2] > fwd.latency_ms[0, 0] and bwd.latency_ms[1, 2] > bwd.latency_ms[0, 0]
     rep = profiler.write_tables(str(tmp_path / "t"), fwd, bwd, tot)
     assert set(rep) == {str(tmp_path / "t_fwd.csv"), str(tmp_path / "t_bwd.csv"), str(tmp_path / "t.csv")}
+
+
+def test_mix_lengths():
+    """--mix cells: packed micro-batches of the 40 % 32K / 60 % 2K mix summing to x exactly."""
+    for x in (256, 2048, 32768, 49152, 71680, 143360, 262144):
+        m = profiler.mix_lengths(x)
+        assert sum(m) == x and all(0 < v <= 32768 for v in m)
+        if x >= 71680:
+            full = [v for v in m if v in (32768, 2048)]
+            frac = sum(v == 32768 for v in full) / len(full)
+            assert 0.3 <= frac <= 0.5, (x, m)
+    assert profiler.mix_lengths(71680) == [32768, 2048, 32768, 2048, 2048]
