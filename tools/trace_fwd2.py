@@ -6,7 +6,12 @@ from paper_2604_13847_b200 import ops
 import bench
 lib = ops._lib()
 lib.sb_debug_set_trace.argtypes = [ctypes.c_void_p]
-cu, k_seq = bench.workload(0)
+if os.environ.get("C3K"):  # C3 rank micro-batch [2048 x3, 32768, 2048] at a fixed keep count
+    lens = [2048, 2048, 2048, 32768, 2048]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    k_seq = np.minimum(int(os.environ["C3K"]), (np.array(lens) + 127) // 128).astype(np.int32)
+else:
+    cu, k_seq = bench.workload(0)
 T = int(cu[-1]); H, D, B = 32, 128, 128
 lay = ops.VarlenLayout.build(cu, B)
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -23,7 +28,7 @@ base = min(t[0, 0, 0], t[1, 0, 0])
 names = ["QK issued", "PV issued", "S seen", "P arrive", "epi start", "epi end"]
 for s in range(2):
     print(f"stream {s}")
-    for gg in range(0, 40):
+    for gg in range(0, int(os.environ.get("ROWS", "40"))):
         print(f"  g={gg:3d} " + " ".join(f"{n}={int(t[s, gg, i] - base) if t[s, gg, i] else -1:8d}" for i, n in enumerate(names)))
     r = slice(2, 150)
     d = np.diff(t[s, :150, 2]); d = d[d > 0]
