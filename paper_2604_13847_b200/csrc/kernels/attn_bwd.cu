@@ -34,33 +34,41 @@ constexpr float kLog2e = 1.4426950408889634f;
 __host__ __device__ constexpr uint32_t pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
 // ------------------------------------------------------------------------------------ prep
-// With ores (the forward's bf16 rounding residual of O), D = rowsum(dO * (O + O_res)): O to ~2^-16
-// instead of bf16, which keeps dS accurate on rows that attend few keys (there dP - D cancels).
+// lse2 = LSE * log2(e) and D = rowsum(dO * O) per (token, q head). With ores (the forward's bf16
+// rounding residual of O), D = rowsum(dO * (O + O_res)): O to ~2^-16 instead of bf16, which keeps
+// dS accurate on rows that attend few keys (there dP - D cancels).
+// HBM-bound: O, dO (and O_res) are streamed once in memory order -- the d/8 threads of a
+// (token, head) row take one 16-byte chunk each, consecutive rows are consecutive heads of a
+// token, so a warp reads 512 contiguous bytes and the grid walks the tensors front to back (the
+// earlier head-major walk touched every 8 KB token row once per head). Two rows per thread per
+// step keep 4-6 loads in flight; the row's threads finish with xor-shuffles.
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ d_o,
                                                        const uint16_t* __restrict__ ores,
                                                        const float* __restrict__ lse, int total, int hq, int d, int tp,
                                                        float* __restrict__ lse2, float* __restrict__ dvec) {
-  // Head h = blockIdx.y; consecutive threads walk consecutive tokens of that head, so the
-  // lse / lse2 / dvec rows are read and written contiguously. Each thread reduces 8 bf16
-  // products (one 16-byte load of O and of dO); the d/8 threads of a row (16 for d=128, 8 for
-  // d=64) finish with xor-shuffles. Two rows per thread per step keep 4 loads in flight.
-  const int h = blockIdx.y;
   const int tpr_log = d == 128 ? 4 : 3;  // log2(threads per row)
   const int sub = threadIdx.x & ((1 << tpr_log) - 1);
-  const int rows_per_block = blockDim.x >> tpr_log;
-  const int stride = gridDim.x * rows_per_block;
-  for (int t0 = blockIdx.x * rows_per_block + (threadIdx.x >> tpr_log); t0 < total; t0 += 2 * stride) {
-    const int t1 = t0 + stride;
-    const bool has1 = t1 < total;
-    const size_t e0 = (static_cast<size_t>(t0) * hq + h) * (d >> 3) + sub;
-    const size_t e1 = (static_cast<size_t>(has1 ? t1 : t0) * hq + h) * (d >> 3) + sub;
+  const long long rows = static_cast<long long>(total) * hq;  // row = t * hq + h
+  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> tpr_log);
+  for (long long r0 = static_cast<long long>(blockIdx.x) * (blockDim.x >> tpr_log) + (threadIdx.x >> tpr_log);
+       r0 < rows; r0 += 2 * stride) {
+    const long long r1 = r0 + stride;
+    const bool has1 = r1 < rows;
+    const size_t e0 = static_cast<size_t>(r0) * (d >> 3) + sub;
+    const size_t e1 = static_cast<size_t>(has1 ? r1 : r0) * (d >> 3) + sub;
     const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(o) + e0);
     const uint4 b0 = __ldg(reinterpret_cast<const uint4*>(d_o) + e0);
     const uint4 a1 = __ldg(reinterpret_cast<const uint4*>(o) + e1);
     const uint4 b1 = __ldg(reinterpret_cast<const uint4*>(d_o) + e1);
+    uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
+    if (ores != nullptr) {
+      c0 = __ldg(reinterpret_cast<const uint4*>(ores) + e0);
+      c1 = __ldg(reinterpret_cast<const uint4*>(ores) + e1);
+    }
     float acc0 = 0.f, acc1 = 0.f;
     const uint32_t wa0[4] = {a0.x, a0.y, a0.z, a0.w}, wb0[4] = {b0.x, b0.y, b0.z, b0.w};
     const uint32_t wa1[4] = {a1.x, a1.y, a1.z, a1.w}, wb1[4] = {b1.x, b1.y, b1.z, b1.w};
+    const uint32_t wc0[4] = {c0.x, c0.y, c0.z, c0.w}, wc1[4] = {c1.x, c1.y, c1.z, c1.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       acc0 = fmaf(__uint_as_float(wa0[e] << 16), __uint_as_float(wb0[e] << 16), acc0);
@@ -68,34 +76,32 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const uint16_t* __restric
       acc1 = fmaf(__uint_as_float(wa1[e] << 16), __uint_as_float(wb1[e] << 16), acc1);
       acc1 = fmaf(__uint_as_float(wa1[e] & 0xffff0000u), __uint_as_float(wb1[e] & 0xffff0000u), acc1);
     }
-    if (ores != nullptr) {
-      const uint4 c0 = __ldg(reinterpret_cast<const uint4*>(ores) + e0);
-      const uint4 c1 = __ldg(reinterpret_cast<const uint4*>(ores) + e1);
-      const uint32_t wc0[4] = {c0.x, c0.y, c0.z, c0.w}, wc1[4] = {c1.x, c1.y, c1.z, c1.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        acc0 = fmaf(__uint_as_float(wc0[e] << 16), __uint_as_float(wb0[e] << 16), acc0);
-        acc0 = fmaf(__uint_as_float(wc0[e] & 0xffff0000u), __uint_as_float(wb0[e] & 0xffff0000u), acc0);
-        acc1 = fmaf(__uint_as_float(wc1[e] << 16), __uint_as_float(wb1[e] << 16), acc1);
-        acc1 = fmaf(__uint_as_float(wc1[e] & 0xffff0000u), __uint_as_float(wb1[e] & 0xffff0000u), acc1);
-      }
+    for (int e = 0; e < 4; ++e) {  // O_res terms (zero when ores == nullptr)
+      acc0 = fmaf(__uint_as_float(wc0[e] << 16), __uint_as_float(wb0[e] << 16), acc0);
+      acc0 = fmaf(__uint_as_float(wc0[e] & 0xffff0000u), __uint_as_float(wb0[e] & 0xffff0000u), acc0);
+      acc1 = fmaf(__uint_as_float(wc1[e] << 16), __uint_as_float(wb1[e] << 16), acc1);
+      acc1 = fmaf(__uint_as_float(wc1[e] & 0xffff0000u), __uint_as_float(wb1[e] & 0xffff0000u), acc1);
     }
     for (int off = (1 << tpr_log) >> 1; off; off >>= 1) {
       acc0 += __shfl_xor_sync(0xffffffffu, acc0, off);
       acc1 += __shfl_xor_sync(0xffffffffu, acc1, off);
     }
     if (sub == 0) {
-      dvec[static_cast<size_t>(h) * tp + t0] = acc0;
-      lse2[static_cast<size_t>(h) * tp + t0] = lse[static_cast<size_t>(h) * total + t0] * kLog2e;
+      const int t0 = static_cast<int>(r0 / hq), h0 = static_cast<int>(r0 - static_cast<long long>(t0) * hq);
+      dvec[static_cast<size_t>(h0) * tp + t0] = acc0;
+      lse2[static_cast<size_t>(h0) * tp + t0] = lse[static_cast<size_t>(h0) * total + t0] * kLog2e;
       if (has1) {
-        dvec[static_cast<size_t>(h) * tp + t1] = acc1;
-        lse2[static_cast<size_t>(h) * tp + t1] = lse[static_cast<size_t>(h) * total + t1] * kLog2e;
+        const int t1 = static_cast<int>(r1 / hq), h1 = static_cast<int>(r1 - static_cast<long long>(t1) * hq);
+        dvec[static_cast<size_t>(h1) * tp + t1] = acc1;
+        lse2[static_cast<size_t>(h1) * tp + t1] = lse[static_cast<size_t>(h1) * total + t1] * kLog2e;
       }
     }
   }
   // Padding columns [total, tp): never read for valid rows, but keep them finite.
   if (blockIdx.x == 0)
-    for (int t = total + threadIdx.x; t < tp; t += blockDim.x) {
+    for (int e = threadIdx.x; e < hq * (tp - total); e += blockDim.x) {
+      const int h = e / (tp - total), t = total + e % (tp - total);
       dvec[static_cast<size_t>(h) * tp + t] = 0.f;
       lse2[static_cast<size_t>(h) * tp + t] = 0.f;
     }
@@ -1784,7 +1790,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   const float scale_log2 = scale * kLog2e;
   const int sms = sched::num_sms();
 
-  bwd_prep_kernel<<<dim3(std::max(1, sms * 8 / hq), hq), 256, 0, st>>>(o, d_o, ores, lse, total, hq, D, w.tp, lse2,
+  bwd_prep_kernel<<<sms * 8, 256, 0, st>>>(o, d_o, ores, lse, total, hq, D, w.tp, lse2,
                                                                          dvec);
   launched("sb_sparse_attn_bwd/prep");
   const int kv_items = hkv * nb_total;

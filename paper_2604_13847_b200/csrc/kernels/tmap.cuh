@@ -28,19 +28,22 @@ inline EncodeTiledFn encode_tiled_fn() {
   return fn;
 }
 
-// 3-D view {D, H, T} of a [T][H][D] bf16 tensor; box {64, 1, rows}, 128-byte swizzle.
-// One box lands in shared memory as `rows` rows of 128 bytes (64 bf16), swizzled.
-inline CUtensorMap make_thd_map(const void* base, int total_tokens, int heads, int head_dim, int box_rows) {
+// 3-D view {D, H, T} of a [T][H][D] bf16 tensor; box {box_cols, 1, rows}: 64 columns land in shared
+// memory as `rows` rows of 128 bytes with the 128-byte swizzle, 32 columns as 64-byte rows with
+// the 64-byte swizzle.
+inline CUtensorMap make_thd_map(const void* base, int total_tokens, int heads, int head_dim, int box_rows,
+                                int box_cols = 64) {
   CUtensorMap map;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(head_dim), static_cast<cuuint64_t>(heads),
                               static_cast<cuuint64_t>(total_tokens)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(head_dim) * 2,
                                  static_cast<cuuint64_t>(heads) * head_dim * 2};
-  const cuuint32_t box[3] = {64, 1, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_cols), 1, static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_tiled_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
                                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                       box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return map;

@@ -10,5 +10,5 @@ run() {  # tag strategy extra
     --layers 36 --dense-grid $EXTRA $3 --out $OUT/$1_N$N/$2 > $OUT/$1_N$N.$2.log 2>&1
   echo "== $1 $2 rc=$?"; cat $OUT/$1_N$N/$2/iterations.csv
 }
-for s in baseline sab_dst; do run c3 $s "--gbs-per-rank 5 --mbs 5 --table profiles/b200_cost_table_h32_d128_b128.csv"; done
-for s in baseline sab_dst; do run c4 $s "--gbs-per-rank 10 --mbs 10 --heads 32 --kv-heads 8 --table profiles/b200_cost_table_h32kv8_d128_b128.csv"; done
+for s in baseline sab_dst; do run c3 $s "--gbs-per-rank 5 --mbs 5 --table profiles/b200_cost_table_mix4060_h32_d128_b128.csv"; done
+for s in baseline sab_dst; do run c4 $s "--gbs-per-rank 10 --mbs 10 --heads 32 --kv-heads 8 --table profiles/b200_cost_table_mix4060_h32kv8_d128_b128.csv"; done
