@@ -115,6 +115,8 @@ class ClockSampler:
         self.path = f"/tmp/sb_clocks_{os.getpid()}.csv"
 
     def __enter__(self):
+        if os.environ.get("SB_NO_CLOCK_SAMPLER"):  # debug: measure without nvidia-smi polling
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"

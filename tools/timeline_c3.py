@@ -24,8 +24,9 @@ mine = [int(lengths_all[i]) for i in ids]
 cu = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
 lay = ops.VarlenLayout.build(cu, 128)
 q, k, v, do = synth.planted_qkv(mine, [routing_all[i][0] for i in ids], 32, 32, 128, 128, seed=42, device="cuda")
-runner = dp.DPStep(dp.RankBatch(np.asarray(mine), ids, lay), q, k, v, do, synth.layer_scales(layers, 42), table,
-                   dp.DstSettings())
+cfg = dp.DstSettings()
+cfg.budget_grid = list(range(1, 257))
+runner = dp.DPStep(dp.RankBatch(np.asarray(mine), ids, lay), q, k, v, do, synth.layer_scales(layers, 42), table, cfg)
 for _ in range(3):
     runner.run()
 torch.cuda.synchronize()
@@ -39,7 +40,9 @@ gaps = []
 for a, b in zip(ev, ev[1:]):
     gaps.append(b.time_range.start - a.time_range.end)
 for e in ev:
-    n = e.name.split("(")[0].split("<")[0][-48:]
+    import re as _re
+    m_ = _re.search(r"([A-Za-z_0-9]+)(<[^>]*>)?\(", e.name)
+    n = (m_.group(1) + (m_.group(2) or "")) if m_ else e.name[:48]
     agg[n] += e.time_range.end - e.time_range.start
     cnt[n] += 1
 span = ev[-1].time_range.end - ev[0].time_range.start
