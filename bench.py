@@ -561,7 +561,9 @@ def main():
         time.sleep(0.3)  # let nvidia-smi start sampling
         t0.record(stream)
         for s_ in range(args.steps):
-            step_outs.append(step(markers[s_]))
+            # keep only each step's selections (for its FLOP count): retaining the last layer's
+            # O / gradients of every step would grow the caching allocator inside the timed region
+            step_outs.append([(i_, c_) for i_, c_, *_ in step(markers[s_])])
             if runner is not None:
                 busy_pairs.append(list(runner.last["busy"]))
         t1.record(stream)

@@ -132,7 +132,7 @@ int sb_sparse_attn_fwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* 
 size_t sb_sparse_attn_bwd_workspace_size(int total_tokens, int nb_total, int hq, int hkv,
                                          int head_dim, int hsel, int k_max);
 size_t sb_sparse_attn_bwd_workspace_size_ex(int nseq, int total_tokens, int nb_total, int hq, int hkv,
-                                            int head_dim, int hsel, int k_max, int block_size);
+                                            int head_dim, int hsel, int k_max, int block_size, int flags);
 int sb_sparse_attn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                        const uint16_t* o, const uint16_t* d_o, const float* lse,
                        const int32_t* cu_seqlens, const int32_t* blk_off, int nseq,

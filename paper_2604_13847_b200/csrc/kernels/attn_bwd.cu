@@ -1746,7 +1746,7 @@ struct BwdWorkspace {
 
 inline size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
-BwdWorkspace bwd_layout(int total, int nb_total, int hq, int hkv, int hsel, int k_max) {
+BwdWorkspace bwd_layout(int total, int nb_total, int hq, int hkv, int hsel, int k_max, bool fused = true) {
   BwdWorkspace w;
   w.tp = ((total + 3) / 4) * 4 + 128;
   size_t off = 0;
@@ -1769,7 +1769,7 @@ BwdWorkspace bwd_layout(int total, int nb_total, int hq, int hkv, int hsel, int 
   w.rec_q = off;
   off = align256(off + sched::rec_workspace_bytes(hq * nb_total));
   w.dqacc = off;  // fused path (D = 128): fp32 dQ accumulator [T][Hq][128]
-  off = align256(off + static_cast<size_t>(total) * hq * 128 * 4);
+  if (fused) off = align256(off + static_cast<size_t>(total) * hq * 128 * 4);
   w.total = off;
   return w;
 }
@@ -1779,9 +1779,9 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
                 const uint16_t* ores, const float* lse, const int32_t* cu, const int32_t* blk_off, int nseq, int total, int nb_total, int hq,
                 int hkv, const int32_t* idx, const int32_t* cnt, int hsel, int k_max, float scale, uint16_t* dq,
                 uint16_t* dk, uint16_t* dv, uint8_t* ws, cudaStream_t st, bool fused_requested) {
-  const BwdWorkspace w = bwd_layout(total, nb_total, hq, hkv, hsel, k_max);
   constexpr bool kFusable = D == 128 && B == 128;
   const bool fused = kFusable && fused_requested;
+  const BwdWorkspace w = bwd_layout(total, nb_total, hq, hkv, hsel, k_max, fused);
   float* lse2 = reinterpret_cast<float*>(ws + w.lse2);
   float* dvec = reinterpret_cast<float*>(ws + w.dvec);
   int32_t* tr_cnt = reinterpret_cast<int32_t*>(ws + w.tr_cnt);
@@ -1902,10 +1902,12 @@ SB_API size_t sb_sparse_attn_bwd_workspace_size(int total_tokens, int nb_total, 
 }
 
 SB_API size_t sb_sparse_attn_bwd_workspace_size_ex(int nseq, int total_tokens, int nb_total, int hq, int hkv,
-                                                   int head_dim, int hsel, int k_max, int block_size) {
-  if (block_size != 256) return sb_sparse_attn_bwd_workspace_size(total_tokens, nb_total, hq, hkv, head_dim, hsel, k_max);
+                                                   int head_dim, int hsel, int k_max, int block_size, int flags) {
+  (void)head_dim;
+  const bool fused = (flags & SB_BWD_FUSED) != 0;  // only the fused pass needs the fp32 dQ accumulator
+  if (block_size != 256) return sbk::bwd_layout(total_tokens, nb_total, hq, hkv, hsel, k_max, fused).total;
   return sbk::expand256_workspace_bytes(nseq, nb_total, hsel, k_max) +
-         sbk::bwd_layout(total_tokens, 2 * nb_total, hq, hkv, hsel, 2 * k_max).total;
+         sbk::bwd_layout(total_tokens, 2 * nb_total, hq, hkv, hsel, 2 * k_max, fused).total;
 }
 
 SB_API int sb_sparse_attn_bwd_ex(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o,

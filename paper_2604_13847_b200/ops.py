@@ -39,7 +39,7 @@ def _lib():
             "sb_coverage_at_grid": (i, [_vp, _vp, i, i, _vp, i, _vp, _vp]),
             "sb_sparse_attn_fwd_workspace_size": (sz, [i, i, i]),
             "sb_sparse_attn_fwd_workspace_size_ex": (sz, [i, i, i, i, i, i]),
-            "sb_sparse_attn_bwd_workspace_size_ex": (sz, [i, i, i, i, i, i, i, i, i]),
+            "sb_sparse_attn_bwd_workspace_size_ex": (sz, [i, i, i, i, i, i, i, i, i, i]),
             "sb_sparse_attn_fwd": (i, [_vp, _vp, _vp, _vp, _vp, i, i, i, i, i, i, i, _vp, _vp, i, i, f, _vp, _vp,
                                        _vp, _vp]),
             "sb_sparse_attn_fwd_ex": (i, [_vp, _vp, _vp, _vp, _vp, i, i, i, i, i, i, i, _vp, _vp, i, i, f, _vp, _vp,
@@ -311,14 +311,15 @@ def sparse_attn_bwd(q, k, v, o, do, lse, lay: VarlenLayout, idx, cnt, scale: flo
     Hkv = k.shape[1]
     hsel, _, k_max = idx.shape
     scale = 1.0 / math.sqrt(D) if scale is None else scale
+    flags = SB_BWD_FUSED if fused else SB_BWD_DETERMINISTIC
     ws_bytes = int(_lib().sb_sparse_attn_bwd_workspace_size_ex(lay.nseq, T, lay.nb_total, Hq, Hkv, D, hsel, k_max,
-                                                               lay.block_size))
+                                                               lay.block_size, flags))
     ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=q.device)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     _call("sb_sparse_attn_bwd_ex", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(o_res), _ptr(do), _ptr(lse),
           _ptr(lay.cu_seqlens), _ptr(lay.blk_off), lay.nseq, T, lay.nb_total, Hq, Hkv, D, lay.block_size, _ptr(idx),
           _ptr(cnt), hsel, k_max, C.c_float(scale), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), _stream(),
-          SB_BWD_FUSED if fused else SB_BWD_DETERMINISTIC)
+          flags)
     return dq, dk, dv
 
 
