@@ -26,6 +26,7 @@ keep 0.25, forward latency beside the CPU oracle on the same input).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -557,6 +558,10 @@ def main():
     torch.cuda.synchronize()
     launches0 = ops.launch_count()
     step_outs, busy_pairs = [], []
+    # Python's cyclic GC can pause the host for tens of ms while it enqueues a layer; the GPU
+    # then drains its queue and idles inside the timed window (seen as erratic fwd phases).
+    gc.collect()
+    gc.disable()
     with ClockSampler(local_rank) as clk:
         time.sleep(0.3)  # let nvidia-smi start sampling
         t0.record(stream)
@@ -568,6 +573,7 @@ def main():
                 busy_pairs.append(list(runner.last["busy"]))
         t1.record(stream)
         torch.cuda.synchronize()
+        gc.enable()
         launches = ops.launch_count() - launches0
         # Keep the GPU under the same load (untimed) so the sampler sees >= ~1 s of it.
         t_load = time.perf_counter()
@@ -661,10 +667,13 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()
     e0.record(stream)
     pipelined(e2e_steps)
     e1.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     nbytes_in = sum(t.numel() * 2 for t in (q, k, v, do))
     nbytes_out = sum(t.numel() * 2 for t in (q, q, k, v))  # O, dQ, dK, dV

@@ -27,3 +27,17 @@ for i in range(int(os.environ.get("N", "20"))):
     out.append((a.elapsed_time(b), (h1 - h0) * 1e3, sum(x.elapsed_time(y) for x, y in runner.last["busy"])))
 for r in out:
     print("step ms %.2f  host-enqueue ms %.2f  busy ms %.2f" % r)
+
+# Back to back (no sync between steps), per-step phase marks as bench.py records them.
+marks = []
+for i in range(int(os.environ.get("N", "20"))):
+    m = bench.Marker(torch, torch.cuda.current_stream())
+    m("start")
+    runner.run(mark=m)
+    marks.append(m)
+torch.cuda.synchronize()
+for m in marks:
+    d = m.durations()
+    fwd_ev = [b.elapsed_time(a) for (ta, a), (tb, b) in zip(m.marks, m.marks[1:]) if ta == "bwd" and tb == "fwd"]
+    print("b2b step: decided %.2f fwd %.2f bwd %.2f  max fwd-layer %.2f" % (d.get("decided", 0), d.get("fwd", 0),
+                                                                            d.get("bwd", 0), -min(fwd_ev or [0])))
