@@ -595,6 +595,10 @@ def main():
         for k_, v_ in m.durations().items():
             phase[k_] = phase.get(k_, 0.0) + v_ / args.steps
     sel_ms, fwd_ms, bwd_ms = phase.get("decided", 0.0), phase.get("fwd", 0.0), phase.get("bwd", 0.0)
+    if os.environ.get("SB_PHASE_DUMP"):  # debug: every step's per-layer phase times
+        for si, m in enumerate(markers):
+            seg = [(tb, a.elapsed_time(b)) for (ta, a), (tb, b) in zip(m.marks, m.marks[1:])]
+            print(f"step {si}: " + " ".join(f"{t[0]}{d:.2f}" for t, d in seg), file=sys.stderr)
     if world > 1:
         dist.barrier()
 
