@@ -286,11 +286,13 @@ class Marker:
     def __init__(self, torch, stream):
         self.torch, self.stream = torch, stream
         self.marks = []
+        self.host = []
 
     def __call__(self, tag):
         e = self.torch.cuda.Event(enable_timing=True)
         e.record(self.stream)
         self.marks.append((tag, e))
+        self.host.append(time.perf_counter())
 
     def durations(self):
         """ms per tag: time from the previous mark to this one, summed per tag."""
@@ -597,8 +599,9 @@ def main():
     sel_ms, fwd_ms, bwd_ms = phase.get("decided", 0.0), phase.get("fwd", 0.0), phase.get("bwd", 0.0)
     if os.environ.get("SB_PHASE_DUMP"):  # debug: every step's per-layer phase times
         for si, m in enumerate(markers):
-            seg = [(tb, a.elapsed_time(b)) for (ta, a), (tb, b) in zip(m.marks, m.marks[1:])]
-            print(f"step {si}: " + " ".join(f"{t[0]}{d:.2f}" for t, d in seg), file=sys.stderr)
+            seg = [(tb, a.elapsed_time(b), 1e3 * (hb - ha))
+                   for ((ta, a), ha), ((tb, b), hb) in zip(zip(m.marks, m.host), zip(m.marks[1:], m.host[1:]))]
+            print(f"step {si}: " + " ".join(f"{t[0]}{d:.2f}/{hh:.2f}" for t, d, hh in seg), file=sys.stderr)
     if world > 1:
         dist.barrier()
 
