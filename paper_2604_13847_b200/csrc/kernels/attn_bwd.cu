@@ -1831,9 +1831,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
       const CUtensorMap tk = make_thd_map(k, total, hkv, D, kM);
       const CUtensorMap tv = make_thd_map(v, total, hkv, D, kM);
       const CUtensorMap tacc = make_thd_map_f32(dqacc, total, hq, D, kM, kRedCols);
-      cuda_check(cudaFuncSetAttribute(attn_bwd_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      FusedCfg::kSmemBytes),
-                 "sb_sparse_attn_bwd: smem attribute (fused)");
+      set_smem_once(attn_bwd_fused_kernel, FusedCfg::kSmemBytes, "sb_sparse_attn_bwd: smem attribute (fused)");
       attn_bwd_fused_kernel<<<std::min(kv_items, sms), kFusedThreads, FusedCfg::kSmemBytes, st>>>(
           tq, tk, tv, tdo, tacc, cu, blk_off, nseq, hq, hkv, hsel, tr_off, tr_ent, lse2, dvec, w.tp, scale, scale_log2,
           dk, dv, order_kv, kv_items);
@@ -1863,8 +1861,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
     const CUtensorMap tdk = make_thd_map(dk, total, hkv, D, kM);
     const CUtensorMap tdv = make_thd_map(dv, total, hkv, D, kM);
     auto kern = attn_bwd_dkv_kernel<D, B>;
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes),
-               "sb_sparse_attn_bwd: smem attribute (dkv)");
+    set_smem_once(kern, C::kSmemBytes, "sb_sparse_attn_bwd: smem attribute (dkv)");
     kern<<<std::min(kv_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, tdk, tdv, cu, blk_off, nseq, hq, hkv, hsel,
                                                                    tr_off, tr_ent, lse2, dvec, w.tp, scale,
                                                                    scale_log2, dk, dv, order_kv, kv_items, g_trace_bwd);
@@ -1878,8 +1875,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
     const CUtensorMap tv = make_thd_map(v, total, hkv, D, B);
     const CUtensorMap tdq = make_thd_map(dq, total, hq, D, B);
     auto kern = attn_bwd_dq_kernel<D, B>;
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes),
-               "sb_sparse_attn_bwd: smem attribute (dq)");
+    set_smem_once(kern, C::kSmemBytes, "sb_sparse_attn_bwd: smem attribute (dq)");
     kern<<<std::min(q_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, tdq, cu, blk_off, nseq, hq, hkv, idx,
                                                                   cnt, hsel, k_max, lse2, dvec, w.tp, scale,
                                                                   scale_log2, dq, rec_q, q_items, g_trace_dq);

@@ -456,8 +456,7 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
   const int grid = std::min(n_items, sched::num_sms());
   using C2 = Fwd2Cfg<D, B>;
   auto k2 = attn_fwd2_kernel<D, B>;
-  cuda_check(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::kSmemBytes),
-             "sb_sparse_attn_fwd: smem attribute");
+  set_smem_once(k2, C2::kSmemBytes, "sb_sparse_attn_fwd: smem attribute");
   k2<<<grid, kThreads2, C2::kSmemBytes, st>>>(tq, tk, tv, to, tores, blk_off, nseq, total, hq, hkv, idx, k_max,
                                               scale * 1.4426950408889634f, o, ores, lse, recs, n_items, g_trace);
   launched("sb_sparse_attn_fwd");

@@ -1,5 +1,8 @@
 // C ABI plumbing shared by every kernel entry point: last-error string, launch counter and
 // the host-side block layout helper.
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "sb_kernels.h"
 
@@ -11,6 +14,22 @@ std::atomic<uint64_t> g_launches{0};
 }  // namespace
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+std::mutex g_attr_mu;
+std::unordered_map<const void*, int> g_attr;  // kernel -> dynamic shared memory opted into
+}  // namespace
+
+bool smem_attr_needed(const void* kernel, int bytes) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  const auto it = g_attr.find(kernel);
+  return it == g_attr.end() || it->second < bytes;
+}
+
+void smem_attr_done(const void* kernel, int bytes) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  g_attr[kernel] = bytes;
+}
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 }  // namespace sbk

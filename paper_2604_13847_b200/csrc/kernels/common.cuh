@@ -43,6 +43,18 @@ inline void cuda_check(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// Opt a kernel into `bytes` of dynamic shared memory once per process (the attribute is sticky;
+// calling cudaFuncSetAttribute on every launch puts a driver call on the per-layer host path).
+bool smem_attr_needed(const void* kernel, int bytes);  // common.cu: per-kernel record of the set value
+void smem_attr_done(const void* kernel, int bytes);
+template <typename K>
+inline void set_smem_once(K kernel, int bytes, const char* where) {
+  const void* key = reinterpret_cast<const void*>(kernel);
+  if (!smem_attr_needed(key, bytes)) return;
+  cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), where);
+  smem_attr_done(key, bytes);
+}
+
 // Check the launch that was just issued and count it.
 inline void launched(const char* name) {
   cuda_check(cudaGetLastError(), name);

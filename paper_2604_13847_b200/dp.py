@@ -249,7 +249,10 @@ class DPStep:
     def local_estimate(self, profs: torch.Tensor) -> RankEstimate:
         """One D2H of all layers' profiles, then the local merge + coverage tables."""
         lay = self.batch.layout
-        host = profs.cpu().numpy()
+        if getattr(self, "_prof_host", None) is None or self._prof_host.shape != profs.shape:
+            self._prof_host = torch.empty(profs.shape, dtype=profs.dtype).pin_memory()
+        self._prof_host.copy_(profs)  # synchronous D2H into persistent pinned memory
+        host = self._prof_host.numpy()
         nb = lay.nb_per_seq
         layer_profiles = [[host[l, s, :nb[s]].copy() for s in range(lay.nseq)] for l in range(host.shape[0])]
         self.last_profiles = layer_profiles
@@ -288,7 +291,11 @@ class DPStep:
         # All layers' per-sequence keep counts in one pinned, asynchronous H2D copy (a pageable
         # copy would block the host behind the GPU once per layer).
         k_all = np.minimum(k_final[self.rank][:, None], nb[None, :]).astype(np.int32)
-        self._k_host = torch.from_numpy(k_all).pin_memory()
+        # persistent pinned staging (a fresh pin_memory() per step can cudaHostAlloc on the host path);
+        # the previous step's copy out of it completed before this step's profile D2H returned
+        if getattr(self, "_k_host", None) is None or self._k_host.shape != k_all.shape:
+            self._k_host = torch.empty(k_all.shape, dtype=torch.int32).pin_memory()
+        self._k_host.numpy()[...] = k_all
         k_dev = self._k_host.to(self.q.device, non_blocking=True)
         ev[2].record()
         outs, works = [], []
