@@ -462,6 +462,26 @@ def main():
 
     from paper_2604_13847_b200 import dp, ops, synth
 
+    if os.environ.get("SB_OPS_TIMING"):  # debug: host time of every ops call, slow ones to stderr
+        import functools
+
+        def _timed(name, fn):
+            @functools.wraps(fn)
+            def w(*a, **kw):
+                h0 = time.perf_counter()
+                r = fn(*a, **kw)
+                dt = (time.perf_counter() - h0) * 1e3
+                if dt > 3.0:
+                    print(f"slow host call {name}: {dt:.1f} ms", file=sys.stderr)
+                return r
+            return w
+
+        for _n in ("topk_select", "sparse_attn_fwd", "sparse_attn_bwd", "block_scores", "coverage_profile",
+                   "block_pool", "_call"):
+            setattr(ops, _n, _timed(_n, getattr(ops, _n)))
+        torch.empty = _timed("torch.empty", torch.empty)
+        torch.empty_like = _timed("torch.empty_like", torch.empty_like)
+
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
