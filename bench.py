@@ -618,6 +618,11 @@ def main():
             phase[k_] = phase.get(k_, 0.0) + v_ / args.steps
     sel_ms, fwd_ms, bwd_ms = phase.get("decided", 0.0), phase.get("fwd", 0.0), phase.get("bwd", 0.0)
     if os.environ.get("SB_PHASE_DUMP"):  # debug: every step's per-layer phase times
+        free_b, total_b = torch.cuda.mem_get_info()
+        print(f"memory: allocated {torch.cuda.memory_allocated() / 2**30:.1f} GiB reserved "
+              f"{torch.cuda.memory_reserved() / 2**30:.1f} GiB free {free_b / 2**30:.1f} / {total_b / 2**30:.1f} GiB; "
+              f"allocator stats: {dict((k, v) for k, v in torch.cuda.memory_stats().items() if 'num_alloc_retries' in k or 'num_device_alloc' in k or 'num_device_free' in k or 'num_sync_all_streams' in k)}",
+              file=sys.stderr)
         for si, m in enumerate(markers):
             seg = [(tb, a.elapsed_time(b), 1e3 * (hb - ha))
                    for ((ta, a), ha), ((tb, b), hb) in zip(zip(m.marks, m.host), zip(m.marks[1:], m.host[1:]))]
