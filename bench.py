@@ -456,6 +456,9 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
     os.environ.setdefault("NCCL_DEBUG", "WARN")
+    # The host only enqueues kernels here: keep OpenMP worker threads from spinning on the cores
+    # the launching thread needs (host stalls mid-enqueue idle the GPU inside the timed window).
+    os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 
     import torch
     import torch.distributed as dist
@@ -483,6 +486,7 @@ def main():
         torch.empty_like = _timed("torch.empty_like", torch.empty_like)
 
     torch.cuda.set_device(local_rank)
+    torch.set_num_threads(1)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)

@@ -1,6 +1,6 @@
 #!/bin/bash
 OUT=gpurun_out/r2r; mkdir -p $OUT
-for i in 1 2; do
+for i in 1 2 3; do
 for mode in sampler nosampler; do
   if [ $mode = nosampler ]; then export SB_NO_CLOCK_SAMPLER=1; else unset SB_NO_CLOCK_SAMPLER; fi
   SB_OPS_TIMING=1 SB_PHASE_DUMP=1 timeout 600 python bench.py --steps 5 --warmup 3 --no-sub --no-cpu-baseline > $OUT/bench_$mode$i.log 2>$OUT/phases_$mode$i.log
