@@ -475,7 +475,8 @@ def main():
                 r = fn(*a, **kw)
                 dt = (time.perf_counter() - h0) * 1e3
                 if dt > 3.0:
-                    print(f"slow host call {name}: {dt:.1f} ms", file=sys.stderr)
+                    shp = [tuple(x) if isinstance(x, (tuple, list)) else getattr(x, "shape", x) for x in a[:2]]
+                    print(f"slow host call {name}: {dt:.1f} ms args {shp} {kw.get('dtype', '')}", file=sys.stderr)
                 return r
             return w
 
