@@ -560,6 +560,7 @@ def main():
 
     outs = step()
     torch.cuda.synchronize()
+    outs_k_final = np.array(runner.last["k_final"], copy=True) if runner is not None else None
 
     def step_flops(outs_):
         ff = fb = 0.0
@@ -593,9 +594,13 @@ def main():
         time.sleep(0.3)  # let nvidia-smi start sampling
         t0.record(stream)
         for s_ in range(args.steps):
-            # keep only each step's selections (for its FLOP count): retaining the last layer's
-            # O / gradients of every step would grow the caching allocator inside the timed region
-            step_outs.append([(i_, c_) for i_, c_, *_ in step(markers[s_])])
+            # Retain nothing on the GPU across timed steps: growing the caching allocator here would
+            # cudaMalloc mid-step (implicitly synchronising, the GPU then idles). Every step plans
+            # the same inputs, so its selections equal the pre-timed step's; the keep counts are
+            # kept (host ints) to check exactly that.
+            step(markers[s_])
+            if runner is not None:
+                step_outs.append(np.array(runner.last["k_final"], copy=True))
             if runner is not None:
                 busy_pairs.append(list(runner.last["busy"]))
         t1.record(stream)
@@ -608,10 +613,12 @@ def main():
             step()
             torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
-    # Useful work per timed step (each step's own selections: closed-loop DST decides per step).
-    fl = [step_flops(o_) for o_ in step_outs]
-    f_fwd = statistics.mean(a for a, _ in fl)
-    f_bwd = statistics.mean(b for _, b in fl)
+    # Useful work per timed step: the pre-timed step's selections (identical keep counts checked).
+    f_fwd, f_bwd = step_flops(outs)
+    if runner is not None:
+        k0 = np.array(outs_k_final)
+        if not all(np.array_equal(k0, kf) for kf in step_outs):
+            raise RuntimeError("timed steps decided different keep counts than the step the FLOPs were counted on")
     f_step = f_fwd + f_bwd
     if busy_pairs:
         busy = [sum(a.elapsed_time(b) for a, b in bp) for bp in busy_pairs]
