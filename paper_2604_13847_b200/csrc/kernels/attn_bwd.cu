@@ -293,6 +293,7 @@ struct DkvBars {
   uint64_t pds_part[2];        // math -> UMMA: P^T and dS^T (bf16) of 32-column chunk c2 packed over dP^T
   uint64_t acc_done;           // UMMA -> epilogue: the item's dV / dK are final
   uint64_t epi_free[kStages];  // epilogue -> producer: the item's dV / dK store read ring stage st
+  uint64_t epi_staged[kStages];  // math -> store warp: the item's dV / dK are staged in ring stage st
   uint32_t tmem_base;
 };
 
@@ -381,7 +382,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     mbar_init(&bars->pds_part[0], 256);
     mbar_init(&bars->pds_part[1], 256);
     mbar_init(&bars->acc_done, 1);
-    for (int st = 0; st < kStages; ++st) mbar_init(&bars->epi_free[st], 1);
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&bars->epi_free[st], 1);
+      mbar_init(&bars->epi_staged[st], 256);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kCols>(&bars->tmem_base);
@@ -725,18 +729,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
             }
           }
         }
+        // Warp 10 issues the TMA stores and waits for them to read the stage, so the math
+        // warps go straight on to the next item's S^T.
         fence_proxy_async_smem();
-        named_bar_sync(1, 256);
-        if (threadIdx.x == 64) {
-#pragma unroll
-          for (int ch = 0; ch < 2; ++ch) {
-            tma_store_3d(&tm_dv, q_smem + sl * C::kQBytes + ch * (kM * 128), ch * 64, w.hk, kv0);
-            tma_store_3d(&tm_dk, do_smem + sl * C::kQBytes + ch * (kM * 128), ch * 64, w.hk, kv0);
-          }
-          bulk_commit();
-          bulk_wait_read();
-          mbar_arrive(&bars->epi_free[sl]);
-        }
+        mbar_arrive(&bars->epi_staged[sl]);
       } else {
         if (kStagedEpi && items > 0 && threadIdx.x == 64) mbar_arrive(&bars->epi_free[(g - 1) % kStages]);
 #pragma unroll
@@ -768,7 +764,37 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
       if (threadIdx.x == 64 && items > 0) tri(4, t - 1);
       tc_fence_before();  // epilogue TMEM reads precede the next item's dV / dK (ordered via pt/dst_full)
     }
-    if (threadIdx.x == 64) bulk_wait_all();  // outstanding dV / dK stores reach global before exit
+  } else if (kStagedEpi) {
+    // ------------------------------------------------------------ dV / dK store warp (warp 10)
+    // Mirrors the math warps' item walk: for every full key tile it waits for the staged dV / dK
+    // (epi_staged), stores them by TMA, and hands the ring stage back to the producer once the
+    // stores have read it (epi_free).
+    int g = 0;
+    uint32_t phase = 0;  // bit st: parity of the next epi_staged[st] phase
+    for (int k = 0;; ++k) {
+      const int it = sched::snake_item(order, n_items, grid, cta, k);
+      if (it < 0) break;
+      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
+      const int items = w.ne * sg;
+      g += items;
+      if (items == 0 || min(B, w.seq_len - w.jl * B) != kM) continue;
+      const int sl = (g - 1) % kStages;
+      const int kv0 = w.seq0 + w.jl * B;
+      mbar_wait(&bars->epi_staged[sl], (phase >> sl) & 1u);
+      phase ^= 1u << sl;
+      if (lane == 0) {
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          tma_store_3d(&tm_dv, q_smem + sl * C::kQBytes + ch * (kM * 128), ch * 64, w.hk, kv0);
+          tma_store_3d(&tm_dk, do_smem + sl * C::kQBytes + ch * (kM * 128), ch * 64, w.hk, kv0);
+        }
+        bulk_commit();
+        bulk_wait_read();
+        mbar_arrive(&bars->epi_free[sl]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) bulk_wait_all();  // outstanding dV / dK stores reach global before exit
   }
   tc_fence_before();
   __syncthreads();
@@ -803,7 +829,7 @@ struct DqCfg {
 
 struct DqBars {
   uint64_t stage_full, stage_empty;  // Q / dO staging buffer (TMA -> tcgen05.cp)
-  uint64_t stage_free;               // the epilogue's dQ store has read the staging buffer
+  uint64_t dq_staged[2];             // math -> producer: item q's dQ is staged (full tile) / stored (partial), [q & 1]
   uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
   uint64_t s_full, s_free, dp_full, dq_done, dq_free;
   uint64_t ds_part[2];  // math -> UMMA: dS of 32-column chunk c2 (of both halves) packed in TMEM
@@ -846,7 +872,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
   if (threadIdx.x == 0) {
     mbar_init(&bars->stage_full, 1);
     mbar_init(&bars->stage_empty, 1);
-    mbar_init(&bars->stage_free, 1);
+    mbar_init(&bars->dq_staged[0], 256);
+    mbar_init(&bars->dq_staged[1], 256);
     for (int st = 0; st < 4; ++st) {
       mbar_init(&bars->k_full[st], 1);
       mbar_init(&bars->k_empty[st], 1);
@@ -897,6 +924,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         tma_prefetch(&tm_v);
       }
       int g = 0, q = 0;
+      // The producer also stores dQ: full tiles are staged by the math warps in the Q half of the
+      // staging buffer, and item q + 2's Q / dO may overwrite it only once the store has read it.
+      // Pending items q - 2 (p2) and q - 1 (p1): head, first row, full tile.
+      int p1h = 0, p1r = 0, p2h = 0, p2r = 0;
+      bool p1f = false, p2f = false;
+      auto store_dq = [&](int qq, int h, int row0, bool full) {
+        mbar_wait(&bars->dq_staged[qq & 1], (qq >> 1) & 1);
+        if (full) {
+          fence_proxy_async_smem();
+#pragma unroll
+          for (int c = 0; c < C::kChunks; ++c) tma_store_3d(&tm_dq, q_stage + c * (B * 128), c * 64, h, row0);
+          bulk_commit();
+          bulk_wait_read();
+        }
+      };
       for (sched::RecCursor cur(recs, n_items, grid, cta);;) {
         const sched::ItemRec rec = cur.next();
         if (rec.it < 0) break;
@@ -905,7 +947,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
         const int hk = w.h / (hq / hkv);
         if (role == 0) {
           const int row0 = w.seq0 + w.i * B;
-          if (q >= 2) mbar_wait(&bars->stage_free, q & 1);  // item q-2's dQ store read the buffer
+          if (q >= 2) store_dq(q - 2, p2h, p2r, p2f);  // item q-2's dQ store has read the buffer
+          p2h = p1h, p2r = p1r, p2f = p1f;
+          p1h = w.h, p1r = row0, p1f = min(B, w.seq_len - w.i * B) == B;
           mbar_wait(&bars->stage_empty, (q & 1) ^ 1);
           mbar_expect_tx(&bars->stage_full, 2 * C::kQBytes);
           for (int c = 0; c < C::kChunks; ++c) {
@@ -934,6 +978,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
           }
         }
         ++q;
+      }
+      if (role == 0) {
+        if (q >= 2) store_dq(q - 2, p2h, p2r, p2f);
+        if (q >= 1) store_dq(q - 1, p1h, p1r, p1f);
+        bulk_wait_all();  // outstanding dQ stores reach global before exit
       }
     }
   } else if (warp == 1) {
@@ -1136,8 +1185,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
       if (nrows == B) {
         // Full tile: dQ goes out by TMA through the Q half of the staging buffer, once the next
         // item's tcgen05.cp has read its Q / dO from it (no next item: the buffer is idle).
-        // The producer loads item q + 2's Q / dO only after this store has read the buffer
-        // (stage_free). Row-per-thread stores cost ~4.6 % of the pass (skip-store bound).
+        // The producer issues the store (dq_staged) and loads item q + 2's Q / dO once it has
+        // read the buffer. Row-per-thread stores cost ~4.6 % of the pass (skip-store bound).
         bool more = false;
         for (sched::RecCursor peek = cur;;) {
           const sched::ItemRec nr = peek.next();
@@ -1161,14 +1210,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
           }
         }
         fence_proxy_async_smem();
-        named_bar_sync(1, 256);
-        if (threadIdx.x == 64) {
-#pragma unroll
-          for (int c = 0; c < D / 64; ++c) tma_store_3d(&tm_dq, q_stage + c * (B * 128), c * 64, w.h, row0);
-          bulk_commit();
-          bulk_wait_read();
-          mbar_arrive(&bars->stage_free);
-        }
       } else {
         if (valid) {  // the last (partial) tile of a sequence: a box would cross into the next
           SB_DCHECK(row0 + r < cu[nseq]);
@@ -1181,12 +1222,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
             store_64B(dq_row + cc * 32, w16);
           }
         }
-        if (threadIdx.x == 64) mbar_arrive(&bars->stage_free);
       }
+      mbar_arrive(&bars->dq_staged[q & 1]);
       if (trace != nullptr && blockIdx.x == 0 && q < 64 && threadIdx.x == 64) trace[4096 + q * 4 + 1] = clock64();
       ++q;
     }
-    if (threadIdx.x == 64) bulk_wait_all();  // outstanding dQ stores reach global before exit
   }
   tc_fence_before();
   __syncthreads();

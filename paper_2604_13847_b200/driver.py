@@ -278,6 +278,9 @@ def main():
     ap.add_argument("--heads", type=int, default=32, help="query heads")
     ap.add_argument("--kv-heads", type=int, default=32, help="kv heads; < --heads = GQA with group-shared selection "
                                                              "(BASELINE C4: 32q / 8kv)")
+    ap.add_argument("--anchor", default="mean", choices=["min", "mean", "max"],
+                    help="DST anchor over the base-budget latencies (dst.cpp select_anchor)")
+    ap.add_argument("--threshold-p", type=float, default=0.1, help="DST coverage-drop bound p")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     if args.heads % args.kv_heads:
@@ -297,8 +300,8 @@ def main():
     drv = Driver(args.strategy, gbs=args.gbs_per_rank * world, mbs=args.mbs, layers=args.layers, dist_spec=dist_spec,
                  table=table, varlen_block_size=128 if args.varlen else 0, project_pp=args.project_pp, rank=rank,
                  world=world, heads=args.heads, kv_heads=args.kv_heads,
-                 dst_grid=list(range(1, 257)) if args.dense_grid else None,
-                 device=torch.device("cuda", local))
+                 dst_grid=list(range(1, 257)) if args.dense_grid else None, anchor=args.anchor,
+                 threshold_p=args.threshold_p, device=torch.device("cuda", local))
     recs = drv.run(args.iters, args.out)
     if rank == 0:
         for it, r in enumerate(recs):
