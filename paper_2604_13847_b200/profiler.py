@@ -136,15 +136,18 @@ def main():
     ap.add_argument("--block", type=int, default=128)
     ap.add_argument("--max-x", type=int, default=262144)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--grid", default=None, help="comma-separated budget grid (default: the reference's 16 points)")
+    ap.add_argument("--bins", default=None, help="comma-separated length bins (default: the reference's 15, <= --max-x)")
     ap.add_argument("--mix", default=None, help="'40/60': cells are packed micro-batches of the 40%% 32K / 60%% 2K "
                                                 "mix (C3 / C4) instead of single sequences")
     args = ap.parse_args()
     if args.heads % args.kv_heads:
         ap.error("--heads must be a multiple of --kv-heads")
     prefix = args.out[:-4] if args.out.endswith(".csv") else args.out
-    bins = [x for x in DEFAULT_LENGTH_BINS if x <= args.max_x]
+    bins = [int(x) for x in args.bins.split(",")] if args.bins else [x for x in DEFAULT_LENGTH_BINS if x <= args.max_x]
+    grid = [int(k) for k in args.grid.split(",")] if args.grid else None
     mix = (32768, 2048, 0.4) if args.mix == "40/60" else None
-    fwd, bwd, tot = profile_tables(bins, None, args.heads, args.kv_heads, args.head_dim, args.block, args.reps, mix=mix)
+    fwd, bwd, tot = profile_tables(bins, grid, args.heads, args.kv_heads, args.head_dim, args.block, args.reps, mix=mix)
     rep = write_tables(prefix, fwd, bwd, tot)
     ratio = bwd.latency_ms / np.maximum(fwd.latency_ms, 1e-9)
     for p, r in rep.items():

@@ -6,7 +6,7 @@ Useful FLOPs follow bench.useful_flops: 4*d*sum(e_ij) f
 10*d*sum(e_ij) bwd per q head; with GQA group selection (--kv-heads < --heads, one index set per
 kv group, reference routing shared by the group) every q head of the group does the same work, so
 the per-selection-head sum is multiplied by the group size. The fraction is against the measured
-sustained bf16 peak in MEASURED_PEAKS.json (bench.peaks()).
+burst bf16 peak in MEASURED_PEAKS.json (bench.peaks()).
 
     python tools/sweep_c5.py --out gpurun_out/c5_sweep.json
 """
@@ -56,7 +56,7 @@ def main():
 
     T, Hq, Hkv, D, B = a.tokens, a.heads, a.kv_heads, a.head_dim, a.block
     group = Hq // Hkv
-    peak_tf, _, peak_kind = bench.peaks()
+    peak_tf, _, _, _, peak_kind = bench.peaks()  # burst bf16 peak
     cu = np.array([0, T], np.int64)
     lay = ops.VarlenLayout.build(cu, B)
     nb = int(lay.nb_max)
