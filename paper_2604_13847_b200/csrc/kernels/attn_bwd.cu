@@ -312,6 +312,25 @@ struct KvItem {
   int hk, gj, jl, seq0, seq_len, e0, ne;
 };
 
+// Split of long dK/dV items (dkv_split_kernel): an order entry is item | chunk << 22 | nchunks << 27.
+// A key block listed by (almost) every later q block -- column-concentrated routing, e.g. a
+// sink block, times the GQA group -- is one item up to ~4x a CTA's fair share of pairs; the
+// LPT snake cannot balance that (C4 planted: makespan 1.52x the mean). Such items are cut into
+// nchunks pair ranges whose fp32 dK / dV partials a second kernel sums in chunk order.
+constexpr int kSplitItemBits = 22;  // item | chunk << 22 | nchunks << 26 (4 bits each: entries stay >= 0)
+constexpr int kSplitMaxChunks = 15;
+#ifndef SB_DKV_SPLIT_PER_CTA
+#define SB_DKV_SPLIT_PER_CTA 4
+#endif
+constexpr int kSplitPerCta = SB_DKV_SPLIT_PER_CTA;  // cap = total pairs / (kSplitPerCta * grid)
+constexpr int kSplitMinPairs = 16;
+__host__ __device__ constexpr int split_slots(int grid) { return 2 * kSplitPerCta * grid; }
+
+struct KvChunk {
+  KvItem w;
+  int it, c, nc, m0, items;  // item, chunk c of nc, its pair range [m0, m0 + items)
+};
+
 // dkv decodes items in place (order -> blk_off -> cu / tr_off): measured 5% faster than the
 // prefetched ItemRec path the fwd / dq kernels use (2.01 vs 1.91 ms on C2).
 __device__ __forceinline__ KvItem decode_kv(int it, const int32_t* cu, const int32_t* blk_off, int nseq, int nbt,
@@ -336,8 +355,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off, int nseq, int hq, int hkv, int hsel,
     const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent, const float* __restrict__ lse2,
     const float* __restrict__ dvec, int tp, float scale, float scale_log2, uint16_t* __restrict__ dk,
-    uint16_t* __restrict__ dv, const int32_t* __restrict__ order, int n_items, unsigned long long* trace) {
+    uint16_t* __restrict__ dv, const int32_t* __restrict__ order, const int32_t* __restrict__ n_items_dev,
+    const int32_t* __restrict__ slot_base, float* __restrict__ partials, unsigned long long* trace) {
   using C = DkvCfg<D, B>;
+  const int n_items = __ldg(n_items_dev);  // entries of the split order (dkv_split_kernel)
   // D = B = 128: an item's dV / dK (32 KB each) are stored by TMA through the Q / dO slots of
   // the ring stage its last pair used, free once acc_done fires (see the epilogue).
   constexpr bool kStagedEpi = D == 128 && B == 128;
@@ -404,6 +425,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
+  // Chunk of schedule round k of this CTA (false past the end).
+  auto next_chunk = [&](int k, KvChunk& ch) {
+    const int e = sched::snake_item(order, n_items, grid, cta, k);
+    if (e < 0) return false;
+    ch.it = e & ((1 << kSplitItemBits) - 1);
+    ch.c = (e >> kSplitItemBits) & 15;
+    ch.nc = e >> (kSplitItemBits + 4);
+    ch.w = decode_kv(ch.it, cu, blk_off, nseq, nbt, tr_off);
+    const int P = ch.w.ne * sg;
+    ch.m0 = ch.c * P / ch.nc;
+    ch.items = (ch.c + 1) * P / ch.nc - ch.m0;
+    return true;
+  };
+
   // (q head, q block) of the m-th pair of an item. Pairs are q-head major (GQA: the sg q heads of
   // the selected entries are walked one head at a time): 0.3-1 % faster than entry-major at C5
   // GQA, DRAM reads unchanged (profiles/r2/gqa_ab.md).
@@ -427,19 +462,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     uint32_t epi_need = 0;            // bit st: an item epilogue is staging through ring stage st
     int epi_uses0 = 0, epi_uses1 = 0;  // epilogues assigned to stage 0 / 1 so far
     for (int k = 0;; ++k) {
-      const int it = sched::snake_item(order, n_items, grid, cta, k);
-      if (it < 0) break;
-      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
-      const int items = w.ne * sg;
+      KvChunk ch;
+      if (!next_chunk(k, ch)) break;
+      const KvItem& w = ch.w;
+      const int items = ch.items;
       if (items == 0) continue;
       const int kv0 = w.seq0 + w.jl * B;
       if (lane == 0) {
         // L2 prefetch of the next non-empty item's K / V: short items (small keep counts) would
         // otherwise expose a DRAM round trip at every item boundary (single K / V buffer).
         for (int k2 = k + 1; k2 < k + 4; ++k2) {
-          const int it2 = sched::snake_item(order, n_items, grid, cta, k2);
-          if (it2 < 0) break;
-          const KvItem w2 = decode_kv(it2, cu, blk_off, nseq, nbt, tr_off);
+          KvChunk ch2;
+          if (!next_chunk(k2, ch2)) break;
+          const KvItem& w2 = ch2.w;
           if (w2.ne == 0) continue;
           const int kv2 = w2.seq0 + w2.jl * B;
           for (int c = 0; c < C::kChunks; ++c) {
@@ -460,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         const int st = g % kStages;
         const uint32_t ph = (g / kStages) & 1;
         int h, gi;
-        pair_of(w, m, h, gi);
+        pair_of(w, ch.m0 + m, h, gi);
         const int q0 = w.seq0 + (gi - (w.gj - w.jl)) * B;  // gj - jl: the sequence's first block
         const int nq = min(B, w.seq_len - (gi - (w.gj - w.jl)) * B);
         // lse2 / D of the pair's query rows: all loads in flight before the ring-slot wait.
@@ -570,10 +605,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
       };
       int g = 0, t = 0;
       for (int k = 0;; ++k) {
-        const int it = sched::snake_item(order, n_items, grid, cta, k);
-        if (it < 0) break;
-        const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
-        const int items = w.ne * sg;
+        KvChunk ch;
+        if (!next_chunk(k, ch)) break;
+        const int items = ch.items;
         if (items == 0) continue;
         tri(1, t);
         mbar_wait(&bars->kv_full, t & 1);
@@ -627,20 +661,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     const uint32_t st_col = C::kSt + hf * HB, dpt_col = C::kDPt + hf * HB;
     int g = 0, t = 0;
     for (int k = 0;; ++k) {
-      const int it = sched::snake_item(order, n_items, grid, cta, k);
-      if (it < 0) break;
-      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
-      const int items = w.ne * sg;
+      KvChunk ch;
+      if (!next_chunk(k, ch)) break;
+      const KvItem& w = ch.w;
+      const int items = ch.items;
       const int kv0 = w.seq0 + w.jl * B;
       const int nkv = min(B, w.seq_len - w.jl * B);
       // Pair entries are loaded one pair ahead so their global-load latency is not exposed
       // after the st_full wait when S^T is already there.
-      int ent_nx = __ldg(tr_ent + w.e0);
+      int ent_nx = __ldg(tr_ent + w.e0 + (w.ne > 0 ? ch.m0 % w.ne : 0));
       const int blk0 = w.gj - w.jl;
       for (int m = 0; m < items; ++m, ++g) {
         const int st = g % kStages;
         const int ent = ent_nx;
-        if (m + 1 < items) ent_nx = __ldg(tr_ent + w.e0 + (m + 1) % w.ne);
+        if (m + 1 < items) ent_nx = __ldg(tr_ent + w.e0 + (ch.m0 + m + 1) % w.ne);
         const int gi = ent - (ent / nbt) * nbt;
         const int il = gi - blk0;
         const int nq = min(B, w.seq_len - il * B);
@@ -704,7 +738,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
       // Epilogue: dV and dK * scale for the valid key rows (zeros if nobody selected the block);
       // warpgroup hf writes output columns [hf * D/2, (hf + 1) * D/2).
       const bool store = c < nkv;
-      if (kStagedEpi && items > 0 && nkv == kM) {
+      if (ch.nc > 1) {
+        // Split item: this chunk's fp32 dV / dK partials -> slot; dkv_split_reduce_kernel sums
+        // the chunks in order (scale applied there) and writes the valid rows.
+        if (kStagedEpi && threadIdx.x == 64) mbar_arrive(&bars->epi_free[(g - 1) % kStages]);
+        const int slot = __ldg(slot_base + ch.it) + ch.c;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          const uint32_t col = (part == 0 ? C::kDV : C::kDK) + hf * (D / 2);
+          float4* prow = reinterpret_cast<float4*>(partials + ((static_cast<size_t>(slot) * 2 + part) * kM + c) * D +
+                                                   hf * (D / 2));
+#pragma unroll
+          for (int cc = 0; cc < D / 64; ++cc) {
+            uint32_t v[32];
+            tmem_ld32(tmem + lf + col + cc * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              prow[cc * 8 + e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
+                                             __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
+          }
+        }
+      } else if (kStagedEpi && items > 0 && nkv == kM) {
         // Full key tile: dV -> the Q slot, dK -> the dO slot of the ring stage the item's last
         // pair used (all its UMMAs are complete), SW128 [chunk hf][key row], then TMA stores.
         // Row-per-thread stores held the math warps ~3000 cycles per item (skip-store bound
@@ -775,12 +830,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     int g = 0;
     uint32_t phase = 0;  // bit st: parity of the next epi_staged[st] phase
     for (int k = 0;; ++k) {
-      const int it = sched::snake_item(order, n_items, grid, cta, k);
-      if (it < 0) break;
-      const KvItem w = decode_kv(it, cu, blk_off, nseq, nbt, tr_off);
-      const int items = w.ne * sg;
+      KvChunk ch;
+      if (!next_chunk(k, ch)) break;
+      const KvItem& w = ch.w;
+      const int items = ch.items;
       g += items;
-      if (items == 0 || min(B, w.seq_len - w.jl * B) != kM) continue;
+      if (items == 0 || ch.nc > 1 || min(B, w.seq_len - w.jl * B) != kM) continue;
       const int sl = (g - 1) % kStages;
       const int kv0 = w.seq0 + w.jl * B;
       mbar_wait(&bars->epi_staged[sl], (phase >> sl) & 1u);
@@ -1766,6 +1821,119 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
   }
 }
 
+// Split order for the dK/dV pass (one CTA of 1024 threads). cap = max(kSplitMinPairs,
+// ceil(total pairs / (kSplitPerCta * grid))); an item of P > cap pairs becomes nc = ceil(P / cap)
+// consecutive entries (chunks) at its place in the longest-first order, and gets slot_base[it]
+// (its first fp32 partial slot) and a split_list entry {it, nc, slot0}. counts = {entries,
+// split items}. Thread t owns positions [t * per, (t + 1) * per): count, block scan, write.
+__global__ void __launch_bounds__(1024) dkv_split_kernel(const int32_t* __restrict__ order, int n,
+                                                         const int32_t* __restrict__ tr_off, int kv_items, int sg,
+                                                         int grid, int32_t* __restrict__ out,
+                                                         int32_t* __restrict__ counts, int32_t* __restrict__ slot_base,
+                                                         int4* __restrict__ split_list) {
+  __shared__ int wsum[3][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int total = __ldg(tr_off + kv_items) * sg;
+  const int cap = max(kSplitMinPairs, (total + kSplitPerCta * grid - 1) / (kSplitPerCta * grid));
+  const int per = (n + 1023) / 1024;
+  const int i0 = min(n, threadIdx.x * per), i1 = min(n, i0 + per);
+  auto nchunks = [&](int it) {
+    const int P = (__ldg(tr_off + it + 1) - __ldg(tr_off + it)) * sg;
+    return P > cap ? min(kSplitMaxChunks, (P + cap - 1) / cap) : 1;
+  };
+  int v[3] = {0, 0, 0};  // entries, split items, partial slots
+  for (int i = i0; i < i1; ++i) {
+    const int nc = nchunks(__ldg(order + i));
+    v[0] += nc;
+    if (nc > 1) {
+      v[1] += 1;
+      v[2] += nc;
+    }
+  }
+  int x[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {  // block-wide exclusive scan
+    int incl = v[j];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[j][warp] = incl;
+    x[j] = incl - v[j];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int w0 = wsum[j][lane];
+      int incl = w0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      wsum[j][lane] = incl - w0;
+    }
+  }
+  __syncthreads();
+  int oa = x[0] + wsum[0][warp], ob = x[1] + wsum[1][warp], oc = x[2] + wsum[2][warp];
+  for (int i = i0; i < i1; ++i) {
+    const int it = __ldg(order + i);
+    const int nc = nchunks(it);
+    for (int q = 0; q < nc; ++q) out[oa + q] = it | (q << kSplitItemBits) | (nc << (kSplitItemBits + 4));
+    oa += nc;
+    if (nc > 1) {
+      SB_DCHECK(oc + nc <= split_slots(grid));
+      slot_base[it] = oc;
+      split_list[ob] = make_int4(it, nc, oc, 0);
+      ++ob;
+      oc += nc;
+    }
+  }
+  if (threadIdx.x == 1023) {
+    counts[0] = oa;
+    counts[1] = ob;
+  }
+}
+
+// dK / dV of the split items: sum of the chunks' fp32 partials in chunk order (deterministic),
+// dK * scale, bf16, valid key rows only. One CTA per split item (grid-stride).
+template <int D, int B>
+__global__ void __launch_bounds__(256) dkv_split_reduce_kernel(const int4* __restrict__ split_list,
+                                                               const int32_t* __restrict__ counts,
+                                                               const float* __restrict__ partials,
+                                                               const int32_t* __restrict__ cu,
+                                                               const int32_t* __restrict__ blk_off, int nseq, int nbt,
+                                                               int hkv, float scale, uint16_t* __restrict__ dk,
+                                                               uint16_t* __restrict__ dv) {
+  const int n_split = __ldg(counts + 1);
+  constexpr int kG = kM * D / 4;  // float4 granules per part
+  for (int si = blockIdx.x; si < n_split; si += gridDim.x) {
+    const int4 e = __ldg(split_list + si);
+    const int it = e.x, nc = e.y, slot0 = e.z;
+    const int hk = it / nbt, gj = it - hk * nbt;
+    const int s = seq_of_block(blk_off, nseq, gj);
+    const int kv0 = cu[s] + (gj - blk_off[s]) * B;
+    const int nkv = min(B, cu[s + 1] - kv0);
+    for (int u = threadIdx.x; u < 2 * kG; u += blockDim.x) {
+      const int part = u / kG, rem = u - part * kG, row = rem / (D / 4), c4 = rem - row * (D / 4);
+      if (row >= nkv) continue;
+      const float4* p = reinterpret_cast<const float4*>(partials) + (static_cast<size_t>(slot0) * 2 + part) * kG + rem;
+      float4 a = __ldg(p);
+      for (int q = 1; q < nc; ++q) {
+        const float4 b = __ldg(p + static_cast<size_t>(q) * 2 * kG);
+        a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+      }
+      const float mul = part ? scale : 1.0f;
+      uint2 o;
+      o.x = pack_bf16x2(a.x * mul, a.y * mul);
+      o.y = pack_bf16x2(a.z * mul, a.w * mul);
+      *reinterpret_cast<uint2*>((part ? dk : dv) + (static_cast<size_t>(kv0 + row) * hkv + hk) * D + c4 * 4) = o;
+    }
+  }
+}
+
 // dQ = bf16(acc * scale): 8 fp32 -> 8 bf16 (one 16-byte store) per thread and step.
 __global__ void __launch_bounds__(256) dq_convert_kernel(const float4* __restrict__ acc, size_t n8, float scale,
                                                          uint4* __restrict__ dq) {
@@ -1783,7 +1951,8 @@ unsigned long long* g_trace_bwd = nullptr;  // debug timeline buffer (sb_debug_s
 unsigned long long* g_trace_dq = nullptr;   // debug timeline buffer (sb_debug_set_trace_dq)
 
 struct BwdWorkspace {
-  size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, order_kv_matched, rec_q, dqacc, total;
+  size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, order_kv_matched, rec_q, dqacc;
+  size_t order_split, split_counts, slot_base, split_list, partials, total;
   int tp;
 };
 
@@ -1811,6 +1980,20 @@ BwdWorkspace bwd_layout(int total, int nb_total, int hq, int hkv, int hsel, int 
   off = align256(off + static_cast<size_t>(hkv) * nb_total * 4);
   w.rec_q = off;
   off = align256(off + sched::rec_workspace_bytes(hq * nb_total));
+  // dK/dV item split (dkv_split_kernel): entries, {entries, split items}, per-item first slot,
+  // split list, fp32 partials [slot][dV, dK][128 key rows][D <= 128].
+  const int sms = sched::num_sms();
+  const size_t kv_items = static_cast<size_t>(hkv) * nb_total;
+  w.order_split = off;
+  off = align256(off + (kv_items + split_slots(sms)) * 4);
+  w.split_counts = off;
+  off = align256(off + 16);
+  w.slot_base = off;
+  off = align256(off + kv_items * 4);
+  w.split_list = off;
+  off = align256(off + static_cast<size_t>(split_slots(sms)) * 16);
+  w.partials = off;
+  off = align256(off + static_cast<size_t>(split_slots(sms)) * 2 * kM * 128 * 4);
   w.dqacc = off;  // fused path (D = 128): fp32 dQ accumulator [T][Hq][128]
   if (fused) off = align256(off + static_cast<size_t>(total) * hq * 128 * 4);
   w.total = off;
@@ -1886,6 +2069,16 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
       return;
     }
   }
+  // Long items -> chunks (see kSplitItemBits); the dK/dV pass walks the split order.
+  require(kv_items < (1 << kSplitItemBits), "sb_sparse_attn_bwd: too many (kv head, key block) items");
+  int32_t* order_split = reinterpret_cast<int32_t*>(ws + w.order_split);
+  int32_t* split_counts = reinterpret_cast<int32_t*>(ws + w.split_counts);
+  int32_t* slot_base = reinterpret_cast<int32_t*>(ws + w.slot_base);
+  int4* split_list = reinterpret_cast<int4*>(ws + w.split_list);
+  float* partials = reinterpret_cast<float*>(ws + w.partials);
+  dkv_split_kernel<<<1, 1024, 0, st>>>(order_kv, kv_items, tr_off, kv_items, hq / hsel, grid_kv, order_split,
+                                       split_counts, slot_base, split_list);
+  launched("sb_sparse_attn_bwd/split");
   const int q_items = hq * nb_total;
   const int32_t* order_q = sched::build_order(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, q_items,
                                               ws + w.order_q, st, "sb_sparse_attn_bwd/order_q");
@@ -1907,8 +2100,12 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
     set_smem_once(kern, C::kSmemBytes, "sb_sparse_attn_bwd: smem attribute (dkv)");
     kern<<<std::min(kv_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, tdk, tdv, cu, blk_off, nseq, hq, hkv, hsel,
                                                                    tr_off, tr_ent, lse2, dvec, w.tp, scale,
-                                                                   scale_log2, dk, dv, order_kv, kv_items, g_trace_bwd);
+                                                                   scale_log2, dk, dv, order_split, split_counts,
+                                                                   slot_base, partials, g_trace_bwd);
     launched("sb_sparse_attn_bwd/dkv");
+    dkv_split_reduce_kernel<D, B><<<2 * sms, 256, 0, st>>>(split_list, split_counts, partials, cu, blk_off, nseq,
+                                                            nb_total, hkv, scale, dk, dv);
+    launched("sb_sparse_attn_bwd/split_reduce");
   }
   {
     using C = DqCfg<D, B>;

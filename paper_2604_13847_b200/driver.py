@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import argparse
 import copy
+import json
 import math
 import os
 import time
@@ -224,6 +225,13 @@ class Driver:
         else:
             all_rows = [rows]
         mb_ms = [[r[0] for r in rr] for rr in all_rows]
+        if plan_json is not None and self.rank == 0:  # per-(rank, mb) measured detail beside the plan
+            L = self.layers
+            detail = [[dict(total_ms=r[0], fwd_ms=sum(r[1:1 + L]), bwd_ms=sum(r[1 + L:1 + 2 * L]),
+                            budgets=[int(x) for x in sp["budgets"][ri][mi]])
+                       for mi, r in enumerate(rr)] for ri, rr in enumerate(all_rows)]
+            with open(plan_json[:-len(".json")] + "_measured.json", "w") as f:
+                json.dump(dict(ranks=detail), f)
         rec = summarize(mb_ms)
         rec.update(dst_overhead_ms=host_ms, avg_budget=sp["avg_budget"], mean_cov_drop=sp["mean_cov_drop"],
                    mb_ms=mb_ms, budgets=sp["budgets"], decisions=sp["decisions"])

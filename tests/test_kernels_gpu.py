@@ -250,6 +250,42 @@ def test_bwd_deterministic():
         assert torch.equal(x, y)
 
 
+@pytest.mark.parametrize("hq,hkv,d,B", [(8, 2, 128, 128), (4, 4, 64, 64)])
+def test_bwd_split_items_sink_column(hq, hkv, d, B):
+    """Column-concentrated selection: every q block selects key block 0 (a sink), with GQA group
+    selection, so key block 0's dK/dV item holds every q block x the group's q heads -- far over
+    the split cap (attn_bwd.cu dkv_split_kernel). Its chunks' fp32 partials are summed in chunk
+    order by dkv_split_reduce_kernel: oracle parity, and bit-identical run to run."""
+    from paper_2604_13847_b200 import ops
+
+    cu = [0, 8192, 8300, 12000]
+    T = cu[-1]
+    q, k, v, do = _rand_bf16((T, hq, d), 41), _rand_bf16((T, hkv, d), 42), _rand_bf16((T, hkv, d), 43), \
+        _rand_bf16((T, hq, d), 44)
+    lay = _layout(cu, B)
+    hsel = hkv
+    S = _rand_scores(lay, hsel, 7)
+    for s in range(lay.nseq):  # sink: column 0 of every causal row
+        for i in range(int(lay.nb_per_seq[s])):
+            S[:, lay.tri_off_host[s] + i * (i + 1) // 2] += 50.0
+    nb = lay.nb_per_seq
+    k_seq = np.minimum(3, nb).astype(np.int32)
+    idx, cnt = ops.topk_select(torch.from_numpy(S).cuda(), lay, torch.from_numpy(k_seq).cuda(), 3)
+    ic, cc = idx.cpu().numpy(), cnt.cpu().numpy()
+    assert (ic[:, : int(nb[0]), 0] == 0).all()  # ascending lists: the sink is every row's first entry
+    scale = 1.0 / math.sqrt(d)
+    o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt, scale)
+    a = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+    b = ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt, scale)
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    ro, rlse = orc.sparse_attn_fwd(_bits(q), _bits(k), _bits(v), cu, B, ic, cc, scale)
+    rdq, rdk, rdv = orc.sparse_attn_bwd(_bits(q), _bits(k), _bits(v), ro, _bits(do), rlse, cu, B, ic, cc, scale)
+    for got, ref, name in zip(a, (rdq, rdk, rdv), ("dq", "dk", "dv")):
+        check_bf16(got, ref, name)
+
+
 def test_fused_bwd_vs_two_pass():
     """d = B = 128: the opt-in fused single pass against the default deterministic two-pass on the
     same inputs: dK / dV accumulate in TMEM in a fixed order (bit-identical run to run); dQ is
