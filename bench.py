@@ -46,8 +46,9 @@ C3_DIST = dict(short_weight=0.6, short_log_mean=float(np.log(2048)), short_log_s
                long_log_mean=float(np.log(32768)), long_log_sigma=0.0)
 FWD_TILE_M = {64: 128, 128: 128}  # query rows per forward UMMA tile at block size B (attn_fwd.cu)
 # The C3 / C4 workload's own GPU-measured cost table: cells are packed micro-batches of the 40 %
-# 32K / 60 % 2K mix (profiler.py --mix 40/60), fwd + bwd per layer.
-COST_TABLE = os.path.join(ROOT, "profiles", "b200_cost_table_mix4060_h32_d128_b128.csv")
+# 32K / 60 % 2K mix (profiler.py --mix 40/60), fwd + bwd per layer, every budget 1..16 (align()
+# returns table-grid budgets, so the grid step is DST's balance granularity; tables_dense.sh).
+COST_TABLE = os.path.join(ROOT, "profiles", "b200_cost_table_mix4060dense_h32_d128_b128.csv")
 
 
 def peaks():

@@ -19,6 +19,7 @@ cost the tuner balances. load_table() applies the reference's isotonic repair in
     python -m paper_2604_13847_b200.profiler --out profiles/b200_cost_table_h32_d128_b128
     python -m paper_2604_13847_b200.profiler --kv-heads 8 --out profiles/b200_cost_table_h32kv8_d128_b128
     python -m paper_2604_13847_b200.profiler --mix 40/60 --out profiles/b200_cost_table_mix4060_h32_d128_b128
+    # dense budget grid + extra bins (the tables bench.py / the balance runs use): tools/gpu/tables_dense.sh
 """
 from __future__ import annotations
 
