@@ -89,12 +89,16 @@ def mix_lengths(x: int, long_len: int = 32768, short_len: int = 2048, long_frac:
 
 
 def profile_tables(length_bins=None, budget_grid=None, heads=32, kv_heads=32, head_dim=128, block=128, reps=3,
-                   seed=0, device="cuda", mix=None):
+                   seed=0, device="cuda", mix=None, passes=1):
     """-> (fwd, bwd, fwd + bwd) ProfileTables over the (length_bins x budget_grid) cells. With
     mix = (long_len, short_len, long_frac) every cell is a packed micro-batch of that mix
     (mix_lengths) with the cell's keep count clamped per member, as the kernels run it; the
     reference's predict(x = summed length, k) then prices packed micro-batches of that mix
-    directly. Without it, a cell is one sequence of x tokens (the reference's model)."""
+    directly. Without it, a cell is one sequence of x tokens (the reference's model).
+
+    passes > 1 sweeps the whole grid that many times and keeps each cell's median over the
+    sweeps: a cell measured once varies by ~5 % between sweeps minutes apart (clock / power
+    state under sw_power_cap), more than one budget step of the dense grid at large k."""
     length_bins = list(DEFAULT_LENGTH_BINS if length_bins is None else length_bins)
     budget_grid = list(DEFAULT_BUDGET_GRID if budget_grid is None else budget_grid)
     g = torch.Generator(device=device).manual_seed(seed)
@@ -105,13 +109,15 @@ def profile_tables(length_bins=None, budget_grid=None, heads=32, kv_heads=32, he
     do = torch.randn((T, heads, head_dim), generator=g, device=device).to(torch.bfloat16)
     scale = 1.0 / math.sqrt(head_dim)
     group = heads // kv_heads
-    lf = np.zeros((len(length_bins), len(budget_grid)))
+    lf = np.zeros((passes, len(length_bins), len(budget_grid)))
     lb = np.zeros_like(lf)
-    for xi, x in enumerate(length_bins):
-        lens = mix_lengths(x, *mix) if mix else [x]
-        lay = ops.VarlenLayout.build(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32), block, device=device)
-        for ki, kk in enumerate(budget_grid):
-            lf[xi, ki], lb[xi, ki] = measure_cell(q[:x], k[:x], v[:x], do[:x], lay, kk, reps, scale, group)
+    for p in range(passes):
+        for xi, x in enumerate(length_bins):
+            lens = mix_lengths(x, *mix) if mix else [x]
+            lay = ops.VarlenLayout.build(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32), block, device=device)
+            for ki, kk in enumerate(budget_grid):
+                lf[p, xi, ki], lb[p, xi, ki] = measure_cell(q[:x], k[:x], v[:x], do[:x], lay, kk, reps, scale, group)
+    lf, lb = np.median(lf, axis=0), np.median(lb, axis=0)
     bins = np.asarray(length_bins, np.int64)
     grid = np.asarray(budget_grid, np.int32)
     return ProfileTable(bins, grid, lf), ProfileTable(bins, grid, lb), ProfileTable(bins, grid, lf + lb)
@@ -137,6 +143,7 @@ def main():
     ap.add_argument("--block", type=int, default=128)
     ap.add_argument("--max-x", type=int, default=262144)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--passes", type=int, default=1, help="sweeps of the whole grid; each cell keeps its median")
     ap.add_argument("--grid", default=None, help="comma-separated budget grid (default: the reference's 16 points)")
     ap.add_argument("--bins", default=None, help="comma-separated length bins (default: the reference's 15, <= --max-x)")
     ap.add_argument("--mix", default=None, help="'40/60': cells are packed micro-batches of the 40%% 32K / 60%% 2K "
@@ -148,7 +155,8 @@ def main():
     bins = [int(x) for x in args.bins.split(",")] if args.bins else [x for x in DEFAULT_LENGTH_BINS if x <= args.max_x]
     grid = [int(k) for k in args.grid.split(",")] if args.grid else None
     mix = (32768, 2048, 0.4) if args.mix == "40/60" else None
-    fwd, bwd, tot = profile_tables(bins, grid, args.heads, args.kv_heads, args.head_dim, args.block, args.reps, mix=mix)
+    fwd, bwd, tot = profile_tables(bins, grid, args.heads, args.kv_heads, args.head_dim, args.block, args.reps, mix=mix,
+                                   passes=args.passes)
     rep = write_tables(prefix, fwd, bwd, tot)
     ratio = bwd.latency_ms / np.maximum(fwd.latency_ms, 1e-9)
     for p, r in rep.items():
