@@ -130,10 +130,12 @@ class Driver:
         q, k, v, do = inputs
         nb = lay.nb_per_seq
         k_all = torch.from_numpy(np.minimum(budgets[:, None], nb[None, :]).astype(np.int32)).to(self.device)
-        # One untimed layer per micro-batch: a new micro-batch shape can grow the caching allocator
-        # (a cudaMalloc stalls the host and the GPU idles inside the timed window); one layer
-        # allocates what every layer does.
-        self._layers(q, k, v, do, lay, nb, k_all, budgets, 1)
+        # One untimed pass of every layer first: a new micro-batch shape, and every per-layer keep
+        # count (the selection tensors are [Hsel, NB, k_max]), can grow the caching allocator; a
+        # cudaMalloc inside the timed window stalls the host and idles the GPU (measured: +20-70 ms
+        # on single micro-batches, i.e. false imbalance). A one-layer warm-up did not cover the
+        # per-layer k_max shapes.
+        self._layers(q, k, v, do, lay, nb, k_all, budgets, self.layers)
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * self.layers + 1)]
         ev[0].record()
@@ -170,6 +172,8 @@ class Driver:
             cu = np.concatenate([[0], np.cumsum([int(lengths[i]) for i in ids])]).astype(np.int64)
             lay = ops.VarlenLayout.build(cu, self.B, device=self.device)
             inputs = self._inputs(ids, lengths, routing)
+            self._profile_pass(inputs[0], inputs[1], lay)  # untimed: allocator warm-up (see _run_micro_batch)
+            torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             profs = self._profile_pass(inputs[0], inputs[1], lay)
