@@ -1898,7 +1898,9 @@ __global__ void __launch_bounds__(1024) dkv_split_kernel(const int32_t* __restri
 }
 
 // dK / dV of the split items: sum of the chunks' fp32 partials in chunk order (deterministic),
-// dK * scale, bf16, valid key rows only. One CTA per split item (grid-stride).
+// dK * scale, bf16, valid key rows only. One thread per 4-column granule; a task is 256
+// granules (256 / (D / 4) key rows) of one part of one split item, grid-strided. All of a
+// granule's nc (<= 15) partial loads are issued before the adds.
 template <int D, int B>
 __global__ void __launch_bounds__(256) dkv_split_reduce_kernel(const int4* __restrict__ split_list,
                                                                const int32_t* __restrict__ counts,
@@ -1907,30 +1909,36 @@ __global__ void __launch_bounds__(256) dkv_split_reduce_kernel(const int4* __res
                                                                const int32_t* __restrict__ blk_off, int nseq, int nbt,
                                                                int hkv, float scale, uint16_t* __restrict__ dk,
                                                                uint16_t* __restrict__ dv) {
-  const int n_split = __ldg(counts + 1);
-  constexpr int kG = kM * D / 4;  // float4 granules per part
-  for (int si = blockIdx.x; si < n_split; si += gridDim.x) {
+  constexpr int kG = kM * D / 4;         // float4 granules per part (128 key rows)
+  constexpr int kTasksPerPart = kG / 256;
+  const int n_tasks = __ldg(counts + 1) * 2 * kTasksPerPart;
+  for (int task = blockIdx.x; task < n_tasks; task += gridDim.x) {
+    const int si = task / (2 * kTasksPerPart);
+    const int rem_t = task - si * 2 * kTasksPerPart;
+    const int part = rem_t / kTasksPerPart;
+    const int gidx = (rem_t - part * kTasksPerPart) * 256 + threadIdx.x;  // granule in the part
+    const int row = gidx / (D / 4), c4 = gidx - row * (D / 4);
     const int4 e = __ldg(split_list + si);
     const int it = e.x, nc = e.y, slot0 = e.z;
     const int hk = it / nbt, gj = it - hk * nbt;
     const int s = seq_of_block(blk_off, nseq, gj);
     const int kv0 = cu[s] + (gj - blk_off[s]) * B;
     const int nkv = min(B, cu[s + 1] - kv0);
-    for (int u = threadIdx.x; u < 2 * kG; u += blockDim.x) {
-      const int part = u / kG, rem = u - part * kG, row = rem / (D / 4), c4 = rem - row * (D / 4);
-      if (row >= nkv) continue;
-      const float4* p = reinterpret_cast<const float4*>(partials) + (static_cast<size_t>(slot0) * 2 + part) * kG + rem;
-      float4 a = __ldg(p);
-      for (int q = 1; q < nc; ++q) {
-        const float4 b = __ldg(p + static_cast<size_t>(q) * 2 * kG);
-        a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
-      }
-      const float mul = part ? scale : 1.0f;
-      uint2 o;
-      o.x = pack_bf16x2(a.x * mul, a.y * mul);
-      o.y = pack_bf16x2(a.z * mul, a.w * mul);
-      *reinterpret_cast<uint2*>((part ? dk : dv) + (static_cast<size_t>(kv0 + row) * hkv + hk) * D + c4 * 4) = o;
-    }
+    if (row >= nkv) continue;
+    const float4* p = reinterpret_cast<const float4*>(partials) + (static_cast<size_t>(slot0) * 2 + part) * kG + gidx;
+    float4 v[kSplitMaxChunks];
+#pragma unroll
+    for (int q = 0; q < kSplitMaxChunks; ++q)
+      if (q < nc) v[q] = __ldg(p + static_cast<size_t>(q) * 2 * kG);
+    float4 a = v[0];
+#pragma unroll
+    for (int q = 1; q < kSplitMaxChunks; ++q)
+      if (q < nc) a.x += v[q].x, a.y += v[q].y, a.z += v[q].z, a.w += v[q].w;
+    const float mul = part ? scale : 1.0f;
+    uint2 o;
+    o.x = pack_bf16x2(a.x * mul, a.y * mul);
+    o.y = pack_bf16x2(a.z * mul, a.w * mul);
+    *reinterpret_cast<uint2*>((part ? dk : dv) + (static_cast<size_t>(kv0 + row) * hkv + hk) * D + c4 * 4) = o;
   }
 }
 
@@ -2103,7 +2111,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
                                                                    scale_log2, dk, dv, order_split, split_counts,
                                                                    slot_base, partials, g_trace_bwd);
     launched("sb_sparse_attn_bwd/dkv");
-    dkv_split_reduce_kernel<D, B><<<2 * sms, 256, 0, st>>>(split_list, split_counts, partials, cu, blk_off, nseq,
+    dkv_split_reduce_kernel<D, B><<<8 * sms, 256, 0, st>>>(split_list, split_counts, partials, cu, blk_off, nseq,
                                                             nb_total, hkv, scale, dk, dv);
     launched("sb_sparse_attn_bwd/split_reduce");
   }
