@@ -18,7 +18,7 @@ for r in rows[hi + 1:]:
     d = launch.setdefault(int(r[ii]), {"name": name})
     d[r[mi]] = float(r[vi].replace(",", ""))
 bwd_names = ("bwd_prep_kernel", "transpose_sel_kernel", "scan_kernel", "attn_bwd_dkv_kernel", "attn_bwd_dq_kernel",
-             "q_records_kernel", "match_rounds_kernel")
+             "q_records_kernel", "match_rounds_kernel", "dkv_split_kernel", "dkv_split_reduce_kernel")
 first_bwd = {}
 for lid, d in launch.items():  # layer 0: the first launch of every backward kernel
     if d["name"] in bwd_names and d["name"] not in first_bwd:
