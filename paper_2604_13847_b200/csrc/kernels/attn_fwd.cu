@@ -441,13 +441,10 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
                 int nseq, int total, int nb_total, int hq, int hkv, const int32_t* idx, const int32_t* cnt, int hsel,
                 int k_max, float scale, uint16_t* o, uint16_t* ores, float* lse, void* ws, cudaStream_t st) {
   const int n_items = hq * nb_total;
-  const int32_t* order = sched::build_order(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, n_items, ws, st,
-                                            "sb_sparse_attn_fwd/order");
   auto* recs = reinterpret_cast<sched::ItemRec*>(
       (reinterpret_cast<uintptr_t>(ws) + sched::order_workspace_bytes(n_items, hq * (k_max + 1)) + 255) & ~uintptr_t(255));
-  sched::q_records_kernel<<<(n_items + 255) / 256, 256, 0, st>>>(order, n_items, cu, blk_off, nseq, nb_total, hq, hsel,
-                                                                 idx, cnt, k_max, recs);
-  launched("sb_sparse_attn_fwd/records");
+  sched::build_q_schedule(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, n_items, ws, recs, cu, blk_off, nseq,
+                          idx, k_max, st, "sb_sparse_attn_fwd/order");
   const CUtensorMap tq = make_thd_map(q, total, hq, D, kM);
   const CUtensorMap tk = make_thd_map(k, total, hkv, D, B);
   const CUtensorMap tv = make_thd_map(v, total, hkv, D, B);

@@ -114,10 +114,8 @@ __global__ void scatter_kernel(Key key, int n_items, const int32_t* __restrict__
 constexpr int kSortOneCtaMaxBins = 8192;
 constexpr int kSortOneCtaMaxItems = 1 << 17;
 template <typename Key>
-__global__ void __launch_bounds__(1024) sort_one_cta_kernel(Key key, int n_items, int bins,
-                                                            int32_t* __restrict__ order) {
-  extern __shared__ int32_t sh[];
-  __shared__ int warp_sum[32];
+__device__ __forceinline__ void sort_one_cta_body(Key key, int n_items, int bins, int32_t* __restrict__ order,
+                                                  int32_t* sh, int* warp_sum) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int b = threadIdx.x; b < bins; b += 1024) sh[b] = 0;
   __syncthreads();
@@ -160,6 +158,14 @@ __global__ void __launch_bounds__(1024) sort_one_cta_kernel(Key key, int n_items
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n_items; i += 1024) order[atomicAdd(&sh[key(i)], 1)] = i;
+}
+
+template <typename Key>
+__global__ void __launch_bounds__(1024) sort_one_cta_kernel(Key key, int n_items, int bins,
+                                                            int32_t* __restrict__ order) {
+  extern __shared__ int32_t sh[];
+  __shared__ int warp_sum[32];
+  sort_one_cta_body(key, n_items, bins, order, sh, warp_sum);
 }
 
 inline size_t order_workspace_bytes(int n_items, int bins) {
@@ -289,14 +295,11 @@ static_assert(sizeof(ItemRec) == 32, "ItemRec is two 16-byte loads");
 
 inline size_t rec_workspace_bytes(int n_items) { return static_cast<size_t>(n_items) * sizeof(ItemRec) + 256; }
 
-__global__ void q_records_kernel(const int32_t* __restrict__ order, int n_items, const int32_t* __restrict__ cu,
-                                 const int32_t* __restrict__ blk_off, int nseq, int nbt, int hq, int hsel,
-                                 const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt, int k_max,
-                                 ItemRec* __restrict__ rec) {
-  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pos >= n_items) return;
+__device__ __forceinline__ ItemRec q_record(int it, const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off,
+                                            int nseq, int nbt, int hq, int hsel, const int32_t* __restrict__ idx,
+                                            const int32_t* __restrict__ cnt, int k_max) {
   ItemRec r;
-  r.it = order[pos];
+  r.it = it;
   const int h = r.it / nbt, gi = r.it - h * nbt;
   r.s = seq_of_block(blk_off, nseq, gi);
   r.loc = gi - blk_off[r.s];
@@ -305,7 +308,29 @@ __global__ void q_records_kernel(const int32_t* __restrict__ order, int n_items,
   r.base = (h / (hq / hsel)) * nbt + gi;
   r.n = cnt[r.base];
   r.first = r.n > 0 ? idx[static_cast<size_t>(r.base) * k_max] : 0;
-  rec[pos] = r;
+  return r;
+}
+
+__global__ void q_records_kernel(const int32_t* __restrict__ order, int n_items, const int32_t* __restrict__ cu,
+                                 const int32_t* __restrict__ blk_off, int nseq, int nbt, int hq, int hsel,
+                                 const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt, int k_max,
+                                 ItemRec* __restrict__ rec) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n_items) return;
+  rec[pos] = q_record(order[pos], cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
+}
+
+// Longest-first q-item order + its records (fwd and dQ passes). Returns the order pointer.
+inline int32_t* build_q_schedule(const CostFromCnt& key, int n_items, void* order_ws, ItemRec* rec,
+                                 const int32_t* cu, const int32_t* blk_off, int nseq, const int32_t* idx, int k_max,
+                                 cudaStream_t st, const char* who) {
+  // (Fusing the records into the one-CTA sort measured 50 us against 13 + 4: each record is a
+  // chain of dependent loads, which one CTA cannot overlap the way 40 CTAs do.)
+  int32_t* order = build_order(key, n_items, order_ws, st, who);
+  q_records_kernel<<<(n_items + 255) / 256, 256, 0, st>>>(order, n_items, cu, blk_off, nseq, key.nb_total, key.hq,
+                                                          key.hsel, idx, key.cnt, k_max, rec);
+  launched(who);
+  return order;
 }
 
 __global__ void kv_records_kernel(const int32_t* __restrict__ order, int n_items, const int32_t* __restrict__ cu,
