@@ -46,6 +46,8 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const uint16_t* __restric
                                                        const uint16_t* __restrict__ ores,
                                                        const float* __restrict__ lse, int total, int hq, int d, int tp,
                                                        float* __restrict__ lse2, float* __restrict__ dvec) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int tpr_log = d == 128 ? 4 : 3;  // log2(threads per row)
   const int sub = threadIdx.x & ((1 << tpr_log) - 1);
   const long long rows = static_cast<long long>(total) * hq;  // row = t * hq + h
@@ -115,6 +117,8 @@ __global__ void transpose_sel_kernel(const int32_t* __restrict__ idx, const int3
                                      const int32_t* __restrict__ blk_off, int nseq, int hkv, int rows_per_kv,
                                      int k_max, int pass, int32_t* __restrict__ tr_cnt,
                                      const int32_t* __restrict__ tr_off, int32_t* __restrict__ tr_ent) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int nbt = blk_off[nseq];
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -157,6 +161,8 @@ __global__ void transpose_sel_kernel(const int32_t* __restrict__ idx, const int3
 // block-wide scan of the 1024 sums follows, then it writes its segment's prefixes. One pass
 // instead of n / 1024 dependent tile rounds (10 rounds at C3: 11 -> ~4 us).
 __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ in, int n, int32_t* __restrict__ out) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   __shared__ int warp_sum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int per = (n + 1023) / 1024;
@@ -358,6 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     const float* __restrict__ dvec, int tp, float scale, float scale_log2, uint16_t* __restrict__ dk,
     uint16_t* __restrict__ dv, const int32_t* __restrict__ order, const int32_t* __restrict__ n_items_dev,
     const int32_t* __restrict__ slot_base, float* __restrict__ partials, unsigned long long* trace) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   using C = DkvCfg<D, B>;
   const int n_items = __ldg(n_items_dev);  // entries of the split order (dkv_split_kernel)
   // D = B = 128: an item's dV / dK (32 KB each) are stored by TMA through the Q / dO slots of
@@ -910,6 +918,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
     int nseq, int hq, int hkv, const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt, int hsel, int k_max,
     const float* __restrict__ lse2, const float* __restrict__ dvec, int tp, float scale, float scale_log2,
     uint16_t* __restrict__ dq, const sched::ItemRec* __restrict__ recs, int n_items, unsigned long long* trace) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   using C = DqCfg<D, B>;
   constexpr int kKS = C::kKStages, kVS = C::kVStages;
   auto tr = [&](int slot, int g) {
@@ -1361,6 +1371,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) attn_bwd_fused_kernel(
     int nseq, int hq, int hkv, int hsel, const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent,
     const float* __restrict__ lse2, const float* __restrict__ dvec, int tp, float scale, float scale_log2,
     uint16_t* __restrict__ dk, uint16_t* __restrict__ dv, const int32_t* __restrict__ order, int n_items) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   constexpr int D = 128, B = 128;
   using C = FusedCfg;
   extern __shared__ uint8_t smem_raw[];
@@ -1832,6 +1844,8 @@ __global__ void __launch_bounds__(1024) dkv_split_kernel(const int32_t* __restri
                                                          int grid, int32_t* __restrict__ out,
                                                          int32_t* __restrict__ counts, int32_t* __restrict__ slot_base,
                                                          int4* __restrict__ split_list) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   __shared__ int wsum[3][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int total = __ldg(tr_off + kv_items) * sg;
@@ -1910,6 +1924,8 @@ __global__ void __launch_bounds__(256) dkv_split_reduce_kernel(const int4* __res
                                                                const int32_t* __restrict__ blk_off, int nseq, int nbt,
                                                                int hkv, float scale, uint16_t* __restrict__ dk,
                                                                uint16_t* __restrict__ dv) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   constexpr int kG = kM * D / 4;         // float4 granules per part (128 key rows)
   constexpr int kTasksPerPart = kG / 256;
   const int n_tasks = __ldg(counts + 1) * 2 * kTasksPerPart;
@@ -1946,6 +1962,8 @@ __global__ void __launch_bounds__(256) dkv_split_reduce_kernel(const int4* __res
 // dQ = bf16(acc * scale): 8 fp32 -> 8 bf16 (one 16-byte store) per thread and step.
 __global__ void __launch_bounds__(256) dq_convert_kernel(const float4* __restrict__ acc, size_t n8, float scale,
                                                          uint4* __restrict__ dq) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const float4 a = __ldg(acc + 2 * i), b = __ldg(acc + 2 * i + 1);
@@ -2025,17 +2043,17 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   const float scale_log2 = scale * kLog2e;
   const int sms = sched::num_sms();
 
-  bwd_prep_kernel<<<sms * 8, 256, 0, st>>>(o, d_o, ores, lse, total, hq, D, w.tp, lse2,
+  launch(bwd_prep_kernel, sms * 8, 256, 0, st, o, d_o, ores, lse, total, hq, D, w.tp, lse2,
                                                                          dvec);
   launched("sb_sparse_attn_bwd/prep");
   const int kv_items = hkv * nb_total;
   const int rows_per_kv = hsel / hkv;
-  transpose_sel_kernel<<<(kv_items + 3) / 4, 128, 0, st>>>(idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 0,
+  launch(transpose_sel_kernel, (kv_items + 3) / 4, 128, 0, st, idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 0,
                                                             tr_cnt, nullptr, nullptr);
   launched("sb_sparse_attn_bwd/transpose_count");
-  scan_kernel<<<1, 1024, 0, st>>>(tr_cnt, kv_items, tr_off);
+  launch(scan_kernel, 1, 1024, 0, st, tr_cnt, kv_items, tr_off);
   launched("sb_sparse_attn_bwd/scan");
-  transpose_sel_kernel<<<(kv_items + 3) / 4, 128, 0, st>>>(idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 1,
+  launch(transpose_sel_kernel, (kv_items + 3) / 4, 128, 0, st, idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 1,
                                                             tr_cnt, tr_off, tr_ent);
   launched("sb_sparse_attn_bwd/transpose_fill");
   const int32_t* order_kv_lpt = sched::build_order(sched::CostFromLists{tr_off, hq / hsel, kMaxKvCost, nb_total, hkv},
@@ -2052,7 +2070,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   // match_rounds_kernel keeps per-CTA state in 256-entry shared arrays: grid_kv <= 256 (B200: 148).
   if (grid_kv <= sched::kMatchMaxGrid && match_us < 0.06 * dkv_est_us) {
     int32_t* matched = reinterpret_cast<int32_t*>(ws + w.order_kv_matched);
-    sched::match_rounds_kernel<<<1, sched::kMatchThreads, 0, st>>>(sched::ListCost{tr_off, hq / hsel}, order_kv_lpt,
+    launch(sched::match_rounds_kernel<sched::ListCost>, 1, sched::kMatchThreads, 0, st, sched::ListCost{tr_off, hq / hsel}, order_kv_lpt,
                                                                    kv_items, grid_kv, matched);
     launched("sb_sparse_attn_bwd/order_kv_match");
     order_kv = matched;
@@ -2067,12 +2085,12 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
       const CUtensorMap tv = make_thd_map(v, total, hkv, D, kM);
       const CUtensorMap tacc = make_thd_map_f32(dqacc, total, hq, D, kM, kRedCols);
       set_smem_once(attn_bwd_fused_kernel, FusedCfg::kSmemBytes, "sb_sparse_attn_bwd: smem attribute (fused)");
-      attn_bwd_fused_kernel<<<std::min(kv_items, sms), kFusedThreads, FusedCfg::kSmemBytes, st>>>(
+      launch(attn_bwd_fused_kernel, std::min(kv_items, sms), kFusedThreads, FusedCfg::kSmemBytes, st, 
           tq, tk, tv, tdo, tacc, cu, blk_off, nseq, hq, hkv, hsel, tr_off, tr_ent, lse2, dvec, w.tp, scale, scale_log2,
           dk, dv, order_kv, kv_items);
       launched("sb_sparse_attn_bwd/fused");
       const size_t n8 = static_cast<size_t>(total) * hq * D / 8;
-      dq_convert_kernel<<<std::max(1, std::min<int>(sms * 8, static_cast<int>((n8 + 255) / 256))), 256, 0, st>>>(
+      launch(dq_convert_kernel, std::max(1, std::min<int>(sms * 8, static_cast<int>((n8 + 255) / 256))), 256, 0, st, 
           reinterpret_cast<const float4*>(dqacc), n8, scale, reinterpret_cast<uint4*>(dq));
       launched("sb_sparse_attn_bwd/dq_convert");
       return;
@@ -2085,7 +2103,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   int32_t* slot_base = reinterpret_cast<int32_t*>(ws + w.slot_base);
   int4* split_list = reinterpret_cast<int4*>(ws + w.split_list);
   float* partials = reinterpret_cast<float*>(ws + w.partials);
-  dkv_split_kernel<<<1, 1024, 0, st>>>(order_kv, kv_items, tr_off, kv_items, hq / hsel, grid_kv, order_split,
+  launch(dkv_split_kernel, 1, 1024, 0, st, order_kv, kv_items, tr_off, kv_items, hq / hsel, grid_kv, order_split,
                                        split_counts, slot_base, split_list);
   launched("sb_sparse_attn_bwd/split");
   const int q_items = hq * nb_total;
@@ -2104,12 +2122,12 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
     const CUtensorMap tdv = make_thd_map(dv, total, hkv, D, kM);
     auto kern = attn_bwd_dkv_kernel<D, B>;
     set_smem_once(kern, C::kSmemBytes, "sb_sparse_attn_bwd: smem attribute (dkv)");
-    kern<<<std::min(kv_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, tdk, tdv, cu, blk_off, nseq, hq, hkv, hsel,
+    launch(kern, std::min(kv_items, sms), kThreads, C::kSmemBytes, st, tq, tk, tv, tdo, tdk, tdv, cu, blk_off, nseq, hq, hkv, hsel,
                                                                    tr_off, tr_ent, lse2, dvec, w.tp, scale,
                                                                    scale_log2, dk, dv, order_split, split_counts,
                                                                    slot_base, partials, g_trace_bwd);
     launched("sb_sparse_attn_bwd/dkv");
-    dkv_split_reduce_kernel<D, B><<<8 * sms, 256, 0, st>>>(split_list, split_counts, partials, cu, blk_off, nseq,
+    launch(dkv_split_reduce_kernel<D, B>, 8 * sms, 256, 0, st, split_list, split_counts, partials, cu, blk_off, nseq,
                                                             nb_total, hkv, scale, dk, dv);
     launched("sb_sparse_attn_bwd/split_reduce");
   }
@@ -2122,7 +2140,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
     const CUtensorMap tdq = make_thd_map(dq, total, hq, D, B);
     auto kern = attn_bwd_dq_kernel<D, B>;
     set_smem_once(kern, C::kSmemBytes, "sb_sparse_attn_bwd: smem attribute (dq)");
-    kern<<<std::min(q_items, sms), kThreads, C::kSmemBytes, st>>>(tq, tk, tv, tdo, tdq, cu, blk_off, nseq, hq, hkv, idx,
+    launch(kern, std::min(q_items, sms), kThreads, C::kSmemBytes, st, tq, tk, tv, tdo, tdq, cu, blk_off, nseq, hq, hkv, idx,
                                                                   cnt, hsel, k_max, lse2, dvec, w.tp, scale,
                                                                   scale_log2, dq, rec_q, q_items, g_trace_dq);
     launched("sb_sparse_attn_bwd/dq");

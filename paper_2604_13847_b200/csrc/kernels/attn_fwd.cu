@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
     int hq, int hkv, const int32_t* __restrict__ idx, int k_max, float scale_log2, uint16_t* __restrict__ out,
     uint16_t* __restrict__ ores, float* __restrict__ lse, const sched::ItemRec* __restrict__ recs, int n_items,
     unsigned long long* __restrict__ trace) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   using C = Fwd2Cfg<D, B>;
   // Debug timeline: CTA 0, per stream s and block g < 256: [s][g][slot] (slots: 0 QK issued,
   // 1 PV issued, 2 S seen by softmax warp 0, 3 P arrived, 4 epilogue start, 5 end, 6 k_full seen).
@@ -454,7 +456,7 @@ void launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const i
   using C2 = Fwd2Cfg<D, B>;
   auto k2 = attn_fwd2_kernel<D, B>;
   set_smem_once(k2, C2::kSmemBytes, "sb_sparse_attn_fwd: smem attribute");
-  k2<<<grid, kThreads2, C2::kSmemBytes, st>>>(tq, tk, tv, to, tores, blk_off, nseq, total, hq, hkv, idx, k_max,
+  launch(k2, grid, kThreads2, C2::kSmemBytes, st, tq, tk, tv, to, tores, blk_off, nseq, total, hq, hkv, idx, k_max,
                                               scale * 1.4426950408889634f, o, ores, lse, recs, n_items, g_trace);
   launched("sb_sparse_attn_fwd");
 }

@@ -43,6 +43,32 @@ inline void cuda_check(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// Programmatic dependent launch. Every kernel is launched with programmatic stream
+// serialization (launch() below): its grid may be scheduled while the previous kernel in the
+// stream is still running, so launch latency and prologues (barrier init, TMEM allocation,
+// descriptor prefetch) overlap the predecessor's tail. Each kernel therefore calls pdl_wait()
+// before its first global-memory access that may depend on an earlier kernel (the wait returns
+// once the predecessor grid has completed and its writes are visible), then pdl_trigger() so its
+// own dependent may be scheduled. A successor can only occupy resources that are free, so a
+// persistent kernel's successor starts on SMs as its CTAs exit.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
+}
+
 // Opt a kernel into `bytes` of dynamic shared memory once per process (the attribute is sticky;
 // calling cudaFuncSetAttribute on every launch puts a driver call on the per-layer host path).
 bool smem_attr_needed(const void* kernel, int bytes);  // common.cu: per-kernel record of the set value

@@ -37,6 +37,8 @@ __global__ void __launch_bounds__(kDstThreads) dst_decide_kernel(
     int nb_max, const int32_t* __restrict__ mb_off, const int32_t* __restrict__ k_base,
     const int32_t* __restrict__ k_anchor, const int32_t* __restrict__ bottleneck, const int32_t* __restrict__ grid,
     int ngrid, double p, int32_t* __restrict__ k_final, double* __restrict__ cov_drop, int32_t* __restrict__ k_seq) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   __shared__ double acc[kDstMaxWidth];
   __shared__ double sh_norm;
   __shared__ int sh_kf;
@@ -122,7 +124,7 @@ SB_API int sb_dst_decide(const double* profile, const int32_t* blk_off, const in
     sbk::require(profile && blk_off && cu_seqlens && mb_off && k_base && k_anchor && bottleneck && grid && k_final &&
                      coverage_drop && k_seq,
                  "null pointer");
-    sbk::dst_decide_kernel<<<n_mb, sbk::kDstThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+    sbk::launch(sbk::dst_decide_kernel, n_mb, sbk::kDstThreads, 0, static_cast<cudaStream_t>(stream), 
         profile, blk_off, cu_seqlens, nb_max, mb_off, k_base, k_anchor, bottleneck, grid, ngrid, threshold_p, k_final,
         coverage_drop, k_seq);
     sbk::launched("sb_dst_decide");

@@ -19,6 +19,8 @@ namespace sbk {
 namespace {
 
 __global__ void blk_off_2x_kernel(const int32_t* __restrict__ blk_off256, int nseq, int32_t* __restrict__ blk_off128) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s <= nseq; s += gridDim.x * blockDim.x)
     blk_off128[s] = 2 * blk_off256[s];
 }
@@ -27,6 +29,8 @@ __global__ void blk_off_2x_kernel(const int32_t* __restrict__ blk_off256, int ns
 __global__ void expand_kernel(const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off256, int nseq,
                               int nb256, int hsel, const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt,
                               int k_max, int32_t* __restrict__ idx128, int32_t* __restrict__ cnt128) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int nb128 = 2 * nb256;
   const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (t >= static_cast<long long>(hsel) * nb128) return;
@@ -80,10 +84,10 @@ Expanded256 expand_selection_256(const int32_t* cu, const int32_t* blk_off256, i
   e.used = a + b + c;
   e.nb_total = 2 * nb256;
   e.k_max = 2 * k_max;
-  blk_off_2x_kernel<<<std::max(1, std::min(64, (nseq + 256) / 256)), 256, 0, st>>>(blk_off256, nseq, e.blk_off);
+  launch(blk_off_2x_kernel, std::max(1, std::min(64, (nseq + 256) / 256)), 256, 0, st, blk_off256, nseq, e.blk_off);
   launched("expand256/blk_off");
   const long long n = static_cast<long long>(hsel) * 2 * nb256;
-  expand_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(cu, blk_off256, nseq, nb256, hsel, idx, cnt,
+  launch(expand_kernel, static_cast<unsigned>((n + 255) / 256), 256, 0, st, cu, blk_off256, nseq, nb256, hsel, idx, cnt,
                                                                           k_max, e.idx, e.cnt);
   launched("expand256/selection");
   return e;

@@ -43,6 +43,8 @@ struct CostFromLists {  // dkv: item = hk * NB + gj, cost = (#selection rows lis
 
 template <typename Key>
 __global__ void key_hist_kernel(Key key, int n_items, int32_t* __restrict__ hist) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += gridDim.x * blockDim.x)
     atomicAdd(hist + key(i), 1);
 }
@@ -54,6 +56,8 @@ __global__ void key_hist_kernel(Key key, int n_items, int32_t* __restrict__ hist
 // bin count reaches ~3 * 10^4 for the key-block order).
 __global__ void __launch_bounds__(1024) key_start_kernel(int32_t* __restrict__ hist, int bins,
                                                          int32_t* __restrict__ start) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   __shared__ int warp_sum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int per = (bins + 1023) / 1024;  // 32-bin steps per warp
@@ -100,6 +104,8 @@ __global__ void __launch_bounds__(1024) key_start_kernel(int32_t* __restrict__ h
 template <typename Key>
 __global__ void scatter_kernel(Key key, int n_items, const int32_t* __restrict__ start,
                                int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += gridDim.x * blockDim.x) {
     const int b = key(i);
     order[start[b] + atomicAdd(cursor + b, 1)] = i;
@@ -163,6 +169,8 @@ __device__ __forceinline__ void sort_one_cta_body(Key key, int n_items, int bins
 template <typename Key>
 __global__ void __launch_bounds__(1024) sort_one_cta_kernel(Key key, int n_items, int bins,
                                                             int32_t* __restrict__ order) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   extern __shared__ int32_t sh[];
   __shared__ int warp_sum[32];
   sort_one_cta_body(key, n_items, bins, order, sh, warp_sum);
@@ -180,7 +188,7 @@ int32_t* build_order(Key key, int n_items, void* ws, cudaStream_t st, const char
   if (bins <= kSortOneCtaMaxBins && n_items <= kSortOneCtaMaxItems) {
     const int smem = bins * static_cast<int>(sizeof(int32_t));
     set_smem_once(sort_one_cta_kernel<Key>, smem, who);
-    sort_one_cta_kernel<Key><<<1, 1024, smem, st>>>(key, n_items, bins, order);
+    launch(sort_one_cta_kernel<Key>, 1, 1024, smem, st, key, n_items, bins, order);
     launched(who);
     return order;
   }
@@ -188,11 +196,11 @@ int32_t* build_order(Key key, int n_items, void* ws, cudaStream_t st, const char
   int32_t* start = hist + bins;
   cuda_check(cudaMemsetAsync(hist, 0, sizeof(int32_t) * bins, st), who);
   const int blocks = min(1184, (n_items + 255) / 256);
-  key_hist_kernel<<<blocks, 256, 0, st>>>(key, n_items, hist);
+  launch(key_hist_kernel<Key>, blocks, 256, 0, st, key, n_items, hist);
   launched(who);
-  key_start_kernel<<<1, 1024, 0, st>>>(hist, bins, start);
+  launch(key_start_kernel, 1, 1024, 0, st, hist, bins, start);
   launched(who);
-  scatter_kernel<<<blocks, 256, 0, st>>>(key, n_items, start, hist, order);
+  launch(scatter_kernel<Key>, blocks, 256, 0, st, key, n_items, start, hist, order);
   launched(who);
   return order;
 }
@@ -213,6 +221,8 @@ constexpr int kMatchMaxGrid = 256;  // shared arrays below are sized per CTA of 
 template <typename Cost>
 __global__ void __launch_bounds__(kMatchThreads) match_rounds_kernel(Cost cost, const int32_t* __restrict__ order,
                                                                      int n_items, int grid, int32_t* __restrict__ out) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   __shared__ int load[kMatchMaxGrid], item_cost[kMatchMaxGrid], item_id[kMatchMaxGrid], cta_at[kMatchMaxGrid],
       rank_cta[kMatchMaxGrid], rank_item[kMatchMaxGrid];
   if (grid > kMatchMaxGrid) __trap();  // host gates on grid <= kMatchMaxGrid (B200 has 148 SMs)
@@ -315,6 +325,8 @@ __global__ void q_records_kernel(const int32_t* __restrict__ order, int n_items,
                                  const int32_t* __restrict__ blk_off, int nseq, int nbt, int hq, int hsel,
                                  const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt, int k_max,
                                  ItemRec* __restrict__ rec) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int pos = blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= n_items) return;
   rec[pos] = q_record(order[pos], cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
@@ -327,7 +339,7 @@ inline int32_t* build_q_schedule(const CostFromCnt& key, int n_items, void* orde
   // (Fusing the records into the one-CTA sort measured 50 us against 13 + 4: each record is a
   // chain of dependent loads, which one CTA cannot overlap the way 40 CTAs do.)
   int32_t* order = build_order(key, n_items, order_ws, st, who);
-  q_records_kernel<<<(n_items + 255) / 256, 256, 0, st>>>(order, n_items, cu, blk_off, nseq, key.nb_total, key.hq,
+  launch(q_records_kernel, (n_items + 255) / 256, 256, 0, st, order, n_items, cu, blk_off, nseq, key.nb_total, key.hq,
                                                           key.hsel, idx, key.cnt, k_max, rec);
   launched(who);
   return order;
@@ -337,6 +349,8 @@ __global__ void kv_records_kernel(const int32_t* __restrict__ order, int n_items
                                   const int32_t* __restrict__ blk_off, int nseq, int nbt,
                                   const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent,
                                   ItemRec* __restrict__ rec) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int pos = blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= n_items) return;
   ItemRec r;

@@ -21,6 +21,8 @@ constexpr int kPoolRows = 8;  // rows in flight per thread
 __global__ void __launch_bounds__(kPoolThreads) block_pool_kernel(
     const uint16_t* __restrict__ x, const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off,
     int nseq, int row_elems, int block_size, float* __restrict__ xbar) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int gi = blockIdx.x;
   const int ch = blockIdx.y * kPoolThreads + threadIdx.x;
   const int chunks = row_elems >> 3;
@@ -68,6 +70,8 @@ template <int D>
 __global__ void __launch_bounds__(256) block_scores_kernel(
     const float* __restrict__ qbar, const float* __restrict__ kbar, const int32_t* __restrict__ blk_off,
     const int64_t* __restrict__ tri_off, int nseq, int hq, int hkv, float scale, float* __restrict__ scores) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   constexpr int kV = D / 4;  // float4 per row
   const int s = blockIdx.y, h = blockIdx.z;
   const int nb = blk_off[s + 1] - blk_off[s];
@@ -126,7 +130,7 @@ SB_API int sb_block_pool(const uint16_t* x, const int32_t* cu_seqlens, const int
     if (nb_total == 0 || nseq == 0) return;
     sbk::require(x && cu_seqlens && blk_off && xbar, "null pointer");
     const dim3 grid(nb_total, (heads * head_dim / 8 + sbk::kPoolThreads - 1) / sbk::kPoolThreads);
-    sbk::block_pool_kernel<<<grid, sbk::kPoolThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+    sbk::launch(sbk::block_pool_kernel, grid, sbk::kPoolThreads, 0, static_cast<cudaStream_t>(stream), 
         x, cu_seqlens, blk_off, nseq, heads * head_dim, block_size, xbar);
     sbk::launched("sb_block_pool");
   });
@@ -144,9 +148,9 @@ SB_API int sb_block_scores(const float* qbar, const float* kbar, const int32_t* 
     dim3 grid((nb_max + sbk::kRowsPerCta - 1) / sbk::kRowsPerCta, nseq, hq);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (head_dim == 128) {
-      sbk::block_scores_kernel<128><<<grid, 256, 0, st>>>(qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, scores);
+      sbk::launch(sbk::block_scores_kernel<128>, grid, 256, 0, st, qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, scores);
     } else {
-      sbk::block_scores_kernel<64><<<grid, 256, 0, st>>>(qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, scores);
+      sbk::launch(sbk::block_scores_kernel<64>, grid, 256, 0, st, qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, scores);
     }
     sbk::launched("sb_block_scores");
   });

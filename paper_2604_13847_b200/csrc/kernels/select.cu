@@ -52,6 +52,8 @@ __global__ void __launch_bounds__(256) topk_select_warp_kernel(
     const float* __restrict__ scores, const int32_t* __restrict__ blk_off, const int64_t* __restrict__ tri_off,
     int nseq, int nbt, int group, const int32_t* __restrict__ k_seq, int k_max, int force_diag,
     int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int gi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int g = blockIdx.y;
@@ -137,6 +139,8 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(
     const float* __restrict__ scores, const int32_t* __restrict__ blk_off, const int64_t* __restrict__ tri_off,
     int nseq, int group, const int32_t* __restrict__ k_seq, int k_max, int force_diag,
     int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int gi = blockIdx.x;
   const int g = blockIdx.y;
   const int nbt = blk_off[nseq];
@@ -264,6 +268,8 @@ __global__ void __launch_bounds__(256) row_sorted_mass_warp_kernel(const float* 
                                                                    const int32_t* __restrict__ blk_off,
                                                                    const int64_t* __restrict__ tri_off, int nseq,
                                                                    int nb_total, float* __restrict__ sorted) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int gi = blockIdx.x * 8 + (threadIdx.x >> 5), h = blockIdx.y, lane = threadIdx.x & 31;
   if (gi >= nb_total) return;
   const int64_t tri = tri_off[nseq];
@@ -337,6 +343,8 @@ __global__ void __launch_bounds__(256) row_sorted_mass_warp_kernel(const float* 
 __global__ void row_sorted_mass_kernel(const float* __restrict__ scores, const int32_t* __restrict__ blk_off,
                                        const int64_t* __restrict__ tri_off, int nseq, int pow2, int min_n,
                                        float* __restrict__ sorted) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   extern __shared__ float buf[];
   __shared__ float red[32];
   const int gi = blockIdx.x, h = blockIdx.y;
@@ -397,6 +405,8 @@ __global__ void row_sorted_mass_kernel(const float* __restrict__ scores, const i
 __global__ void profile_partial_kernel(const float* __restrict__ sorted, const int32_t* __restrict__ blk_off,
                                        const int64_t* __restrict__ tri_off, int nseq, int nb_max,
                                        double* __restrict__ partial) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int s = blockIdx.y, h = blockIdx.z;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nb_max) return;
@@ -410,6 +420,8 @@ __global__ void profile_partial_kernel(const float* __restrict__ sorted, const i
 
 __global__ void profile_reduce_kernel(const double* __restrict__ partial, const int32_t* __restrict__ blk_off,
                                       int nseq, int nb_max, int hs, double* __restrict__ profile) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int s = blockIdx.y;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nb_max) return;
@@ -425,6 +437,8 @@ __global__ void profile_reduce_kernel(const double* __restrict__ partial, const 
 __global__ void coverage_at_grid_kernel(const double* __restrict__ profile, const int32_t* __restrict__ blk_off,
                                         int nseq, int nb_max, const int32_t* __restrict__ grid, int ngrid,
                                         double* __restrict__ cov) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nseq * ngrid) return;
   const int s = t / ngrid, g = t % ngrid;
@@ -455,12 +469,12 @@ SB_API int sb_topk_select(const float* scores, const int32_t* blk_off, const int
     sbk::require(scores && blk_off && tri_off && k_seq && idx && cnt, "null pointer");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     dim3 wgrid((nb_total + 7) / 8, hs / group);
-    sbk::topk_select_warp_kernel<<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, group, k_seq, k_max,
+    sbk::launch(sbk::topk_select_warp_kernel, wgrid, 256, 0, st, scores, blk_off, tri_off, nseq, nb_total, group, k_seq, k_max,
                                                          force_diag ? 1 : 0, idx, cnt);
     sbk::launched("sb_topk_select");
     if (nb_max > sbk::kWarpRow) {  // rows longer than 256 candidates
       dim3 grid(nb_total, hs / group);
-      sbk::topk_select_kernel<<<grid, sbk::kSelThreads, 0, st>>>(scores, blk_off, tri_off, nseq, group, k_seq, k_max,
+      sbk::launch(sbk::topk_select_kernel, grid, sbk::kSelThreads, 0, st, scores, blk_off, tri_off, nseq, group, k_seq, k_max,
                                                                  force_diag ? 1 : 0, idx, cnt);
       sbk::launched("sb_topk_select");
     }
@@ -489,18 +503,18 @@ SB_API int sb_coverage_profile(const float* scores, const int32_t* blk_off, cons
       // Rows of <= 256 blocks: one warp each; longer rows: one CTA each (shared-memory sort).
       const dim3 wgrid((nb_total + 7) / 8, hs);
       if (p2 <= 32) {
-        sbk::row_sorted_mass_warp_kernel<1><<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, sorted);
+        sbk::launch(sbk::row_sorted_mass_warp_kernel<1>, wgrid, 256, 0, st, scores, blk_off, tri_off, nseq, nb_total, sorted);
       } else if (p2 <= 64) {
-        sbk::row_sorted_mass_warp_kernel<2><<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, sorted);
+        sbk::launch(sbk::row_sorted_mass_warp_kernel<2>, wgrid, 256, 0, st, scores, blk_off, tri_off, nseq, nb_total, sorted);
       } else if (p2 <= 128) {
-        sbk::row_sorted_mass_warp_kernel<4><<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, sorted);
+        sbk::launch(sbk::row_sorted_mass_warp_kernel<4>, wgrid, 256, 0, st, scores, blk_off, tri_off, nseq, nb_total, sorted);
       } else {
-        sbk::row_sorted_mass_warp_kernel<8><<<wgrid, 256, 0, st>>>(scores, blk_off, tri_off, nseq, nb_total, sorted);
+        sbk::launch(sbk::row_sorted_mass_warp_kernel<8>, wgrid, 256, 0, st, scores, blk_off, tri_off, nseq, nb_total, sorted);
       }
       sbk::launched("sb_coverage_profile/sort");
       if (nb_max > 256) {
         dim3 grid(nb_total, hs);
-        sbk::row_sorted_mass_kernel<<<grid, 256, p2 * sizeof(float), st>>>(scores, blk_off, tri_off, nseq, p2, 256,
+        sbk::launch(sbk::row_sorted_mass_kernel, grid, 256, p2 * sizeof(float), st, scores, blk_off, tri_off, nseq, p2, 256,
                                                                           sorted);
         sbk::launched("sb_coverage_profile/sort_long");
       }
@@ -508,10 +522,10 @@ SB_API int sb_coverage_profile(const float* scores, const int32_t* blk_off, cons
     const size_t sorted_bytes = (static_cast<size_t>(tri_total_host) * hs * sizeof(float) + 255) & ~size_t(255);
     double* partial = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + sorted_bytes);
     dim3 g1((nb_max + 127) / 128, nseq, hs);
-    sbk::profile_partial_kernel<<<g1, 128, 0, st>>>(sorted, blk_off, tri_off, nseq, nb_max, partial);
+    sbk::launch(sbk::profile_partial_kernel, g1, 128, 0, st, sorted, blk_off, tri_off, nseq, nb_max, partial);
     sbk::launched("sb_coverage_profile/partial");
     dim3 g2((nb_max + 127) / 128, nseq);
-    sbk::profile_reduce_kernel<<<g2, 128, 0, st>>>(partial, blk_off, nseq, nb_max, hs, profile);
+    sbk::launch(sbk::profile_reduce_kernel, g2, 128, 0, st, partial, blk_off, nseq, nb_max, hs, profile);
     sbk::launched("sb_coverage_profile/reduce");
   });
 }
@@ -523,7 +537,7 @@ SB_API int sb_coverage_at_grid(const double* profile, const int32_t* blk_off, in
     if (nseq == 0) return;
     sbk::require(profile && blk_off && grid && coverage, "null pointer");
     const int n = nseq * ngrid;
-    sbk::coverage_at_grid_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+    sbk::launch(sbk::coverage_at_grid_kernel, (n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream), 
         profile, blk_off, nseq, nb_max, grid, ngrid, coverage);
     sbk::launched("sb_coverage_at_grid");
   });
