@@ -2,9 +2,9 @@
 # Programmatic dependent launch A/B: full GPU test suite on the new lib, then C3 bench alternating
 # with alt_lib/nopdl.so, and the timeline's kernel gaps.
 OUT=gpurun_out/ab_pdl; mkdir -p $OUT
-timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest.log 2>&1; echo "pytest rc $?"; tail -n 3 $OUT/pytest.log
+timeout 1500 python -m pytest tests/test_kernels_gpu.py tests/test_kernels_fullsize_gpu.py -m gpu -x -q > $OUT/pytest.log 2>&1; echo "pytest rc $?"; tail -n 3 $OUT/pytest.log
 for r in 1 2; do
-  for lib in default nopdl; do
+  for lib in default pdl1; do
     if [ $lib = default ]; then unset SB_LIB_PATH; else export SB_LIB_PATH=alt_lib/$lib.so; fi
     timeout 600 python bench.py --steps 5 --warmup 3 --no-sub --no-cpu-baseline > $OUT/bench_${lib}_$r.log 2>&1
     python - <<PY
@@ -16,4 +16,4 @@ PY
 done
 unset SB_LIB_PATH
 timeout 300 python tools/time_kernels.py 2>&1 | grep -E "^fwd" | sed "s/^/pdl C2 /"
-SB_LIB_PATH=alt_lib/nopdl.so timeout 300 python tools/time_kernels.py 2>&1 | grep -E "^fwd" | sed "s/^/nopdl C2 /"
+SB_LIB_PATH=alt_lib/pdl1.so timeout 300 python tools/time_kernels.py 2>&1 | grep -E "^fwd" | sed "s/^/pdl1 C2 /"
