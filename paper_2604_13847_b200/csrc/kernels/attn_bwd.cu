@@ -42,64 +42,76 @@ __host__ __device__ constexpr uint32_t pow2_cols(int c) { return c <= 32 ? 32 : 
 // token, so a warp reads 512 contiguous bytes and the grid walks the tensors front to back (the
 // earlier head-major walk touched every 8 KB token row once per head). Two rows per thread per
 // step keep 4-6 loads in flight; the row's threads finish with xor-shuffles.
-__global__ void __launch_bounds__(256) bwd_prep_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ d_o,
-                                                       const uint16_t* __restrict__ ores,
-                                                       const float* __restrict__ lse, int total, int hq, int d, int tp,
-                                                       float* __restrict__ lse2, float* __restrict__ dvec) {
-  pdl_wait();  // see launch() (common.cuh)
-  pdl_trigger();
+// One grid-stride pass over the rows: R rows per thread group and step, all 3R 16-byte loads
+// issued before any arithmetic (kRes: the O residual is read and added).
+template <bool kRes>
+__device__ __forceinline__ void prep_rows(const uint16_t* __restrict__ o, const uint16_t* __restrict__ d_o,
+                                          const uint16_t* __restrict__ ores, const float* __restrict__ lse,
+                                          int total, int hq, int d, int tp, float* __restrict__ lse2,
+                                          float* __restrict__ dvec) {
+  constexpr int R = 4;
   const int tpr_log = d == 128 ? 4 : 3;  // log2(threads per row)
   const int sub = threadIdx.x & ((1 << tpr_log) - 1);
   const long long rows = static_cast<long long>(total) * hq;  // row = t * hq + h
   const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> tpr_log);
   for (long long r0 = static_cast<long long>(blockIdx.x) * (blockDim.x >> tpr_log) + (threadIdx.x >> tpr_log);
-       r0 < rows; r0 += 2 * stride) {
-    const long long r1 = r0 + stride;
-    const bool has1 = r1 < rows;
-    const size_t e0 = static_cast<size_t>(r0) * (d >> 3) + sub;
-    const size_t e1 = static_cast<size_t>(has1 ? r1 : r0) * (d >> 3) + sub;
-    const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(o) + e0);
-    const uint4 b0 = __ldg(reinterpret_cast<const uint4*>(d_o) + e0);
-    const uint4 a1 = __ldg(reinterpret_cast<const uint4*>(o) + e1);
-    const uint4 b1 = __ldg(reinterpret_cast<const uint4*>(d_o) + e1);
-    uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
-    if (ores != nullptr) {
-      c0 = __ldg(reinterpret_cast<const uint4*>(ores) + e0);
-      c1 = __ldg(reinterpret_cast<const uint4*>(ores) + e1);
-    }
-    float acc0 = 0.f, acc1 = 0.f;
-    const uint32_t wa0[4] = {a0.x, a0.y, a0.z, a0.w}, wb0[4] = {b0.x, b0.y, b0.z, b0.w};
-    const uint32_t wa1[4] = {a1.x, a1.y, a1.z, a1.w}, wb1[4] = {b1.x, b1.y, b1.z, b1.w};
-    const uint32_t wc0[4] = {c0.x, c0.y, c0.z, c0.w}, wc1[4] = {c1.x, c1.y, c1.z, c1.w};
+       r0 < rows; r0 += R * stride) {
+    uint4 a[R], b[R], c[R];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      acc0 = fmaf(__uint_as_float(wa0[e] << 16), __uint_as_float(wb0[e] << 16), acc0);
-      acc0 = fmaf(__uint_as_float(wa0[e] & 0xffff0000u), __uint_as_float(wb0[e] & 0xffff0000u), acc0);
-      acc1 = fmaf(__uint_as_float(wa1[e] << 16), __uint_as_float(wb1[e] << 16), acc1);
-      acc1 = fmaf(__uint_as_float(wa1[e] & 0xffff0000u), __uint_as_float(wb1[e] & 0xffff0000u), acc1);
+    for (int u = 0; u < R; ++u) {
+      const long long r = r0 + u * stride;
+      const size_t e = static_cast<size_t>(r < rows ? r : r0) * (d >> 3) + sub;
+      a[u] = __ldg(reinterpret_cast<const uint4*>(o) + e);
+      b[u] = __ldg(reinterpret_cast<const uint4*>(d_o) + e);
+      if (kRes) c[u] = __ldg(reinterpret_cast<const uint4*>(ores) + e);
+    }
+    asm volatile("" ::: "memory");  // keeps every load above the arithmetic (ptxas interleaves otherwise)
+    float acc[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const uint32_t wa[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, wb[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+      float x = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        x = fmaf(__uint_as_float(wa[e] << 16), __uint_as_float(wb[e] << 16), x);
+        x = fmaf(__uint_as_float(wa[e] & 0xffff0000u), __uint_as_float(wb[e] & 0xffff0000u), x);
+      }
+      if (kRes) {
+        const uint32_t wc[4] = {c[u].x, c[u].y, c[u].z, c[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          x = fmaf(__uint_as_float(wc[e] << 16), __uint_as_float(wb[e] << 16), x);
+          x = fmaf(__uint_as_float(wc[e] & 0xffff0000u), __uint_as_float(wb[e] & 0xffff0000u), x);
+        }
+      }
+      acc[u] = x;
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {  // O_res terms (zero when ores == nullptr)
-      acc0 = fmaf(__uint_as_float(wc0[e] << 16), __uint_as_float(wb0[e] << 16), acc0);
-      acc0 = fmaf(__uint_as_float(wc0[e] & 0xffff0000u), __uint_as_float(wb0[e] & 0xffff0000u), acc0);
-      acc1 = fmaf(__uint_as_float(wc1[e] << 16), __uint_as_float(wb1[e] << 16), acc1);
-      acc1 = fmaf(__uint_as_float(wc1[e] & 0xffff0000u), __uint_as_float(wb1[e] & 0xffff0000u), acc1);
-    }
-    for (int off = (1 << tpr_log) >> 1; off; off >>= 1) {
-      acc0 += __shfl_xor_sync(0xffffffffu, acc0, off);
-      acc1 += __shfl_xor_sync(0xffffffffu, acc1, off);
-    }
+    for (int u = 0; u < R; ++u)
+      for (int off = (1 << tpr_log) >> 1; off; off >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], off);
     if (sub == 0) {
-      const int t0 = static_cast<int>(r0 / hq), h0 = static_cast<int>(r0 - static_cast<long long>(t0) * hq);
-      dvec[static_cast<size_t>(h0) * tp + t0] = acc0;
-      lse2[static_cast<size_t>(h0) * tp + t0] = lse[static_cast<size_t>(h0) * total + t0] * kLog2e;
-      if (has1) {
-        const int t1 = static_cast<int>(r1 / hq), h1 = static_cast<int>(r1 - static_cast<long long>(t1) * hq);
-        dvec[static_cast<size_t>(h1) * tp + t1] = acc1;
-        lse2[static_cast<size_t>(h1) * tp + t1] = lse[static_cast<size_t>(h1) * total + t1] * kLog2e;
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const long long r = r0 + u * stride;
+        if (r >= rows) break;
+        const int t = static_cast<int>(r / hq), h = static_cast<int>(r - static_cast<long long>(t) * hq);
+        dvec[static_cast<size_t>(h) * tp + t] = acc[u];
+        lse2[static_cast<size_t>(h) * tp + t] = lse[static_cast<size_t>(h) * total + t] * kLog2e;
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256, 4) bwd_prep_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ d_o,
+                                                       const uint16_t* __restrict__ ores,
+                                                       const float* __restrict__ lse, int total, int hq, int d, int tp,
+                                                       float* __restrict__ lse2, float* __restrict__ dvec) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
+  if (ores != nullptr)
+    prep_rows<true>(o, d_o, ores, lse, total, hq, d, tp, lse2, dvec);
+  else
+    prep_rows<false>(o, d_o, ores, lse, total, hq, d, tp, lse2, dvec);
   // Padding columns [total, tp): never read for valid rows, but keep them finite.
   if (blockIdx.x == 0)
     for (int e = threadIdx.x; e < hq * (tp - total); e += blockDim.x) {
