@@ -2,8 +2,8 @@
 //
 // K1 streams X [T][H][D] once with 128-bit coalesced loads (CTAs split each block's
 // contiguous B x H x D slab by columns) and writes the fp32 block means: HBM-bound.
-// K2 forms the per-sequence lower-triangular score matrix S = scale * Qbar Kbar^T (one warp
-// per score row, Kbar staged through shared memory in 32-key chunks).
+// K2 forms the per-sequence lower-triangular score matrix S = scale * Qbar Kbar^T (64 rows per
+// CTA, 8 per thread, Kbar staged through shared memory in 32-key chunks).
 #include "common.cuh"
 #include "sb_kernels.h"
 
@@ -58,14 +58,15 @@ __global__ void __launch_bounds__(kPoolThreads) block_pool_kernel(
   out[2 * ch + 1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
 }
 
-constexpr int kRowsPerCta = 8;  // one warp per score row
+constexpr int kRowsPerCta = 64;  // score rows per CTA
+constexpr int kRowsPerThread = 8;
 
-// Scores of 8 consecutive rows i of sequence s, q head h (one warp per row): the rows' Qbar
-// and 32-key chunks of Kbar (transposed, conflict-free) are staged in shared memory and lane
-// l computes S[i][j0 + l] for j0 + l <= i. Every score is acc = fma over d = 0..D-1 in order
-// from 0, times scale -- the same operation sequence as the 64x64-tile kernel this replaced
-// (bit-identical output), which launched mostly-empty CTAs and ran four latency-bound rounds
-// each (36 us on C2).
+// Scores of 64 consecutive rows i of sequence s, q head h. The rows' Qbar are staged once,
+// transposed ([d][row]); Kbar goes through shared memory in 32-key chunks ([d][key]).
+// Thread (warp w, lane l) computes rows i0 + 8w .. i0 + 8w + 7 against key j0 + l: per d one
+// 4-byte load of Kbar and two broadcast float4 loads of Qbar feed 8 FMAs. The one-warp-per-row
+// kernel this replaced (one 4-byte load per FMA) was shared-memory bound: 66 us per C3 layer.
+// Every score is still acc = fma over d = 0..D-1 in order from 0, times scale: bit-identical.
 template <int D>
 __global__ void __launch_bounds__(256) block_scores_kernel(
     const float* __restrict__ qbar, const float* __restrict__ kbar, const int32_t* __restrict__ blk_off,
@@ -80,20 +81,24 @@ __global__ void __launch_bounds__(256) block_scores_kernel(
   const int b0 = blk_off[s];
   const int hk = h / (hq / hkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = i0 + warp;
+  const int r0 = warp * kRowsPerThread;
   const int i_last = min(i0 + kRowsPerCta - 1, nb - 1);
-  __shared__ float4 qs[kRowsPerCta][kV];
-  __shared__ float kt[D][33];
+  __shared__ __align__(16) float qt[D][kRowsPerCta];
+  __shared__ float kt[D][32];
   for (int e = threadIdx.x; e < kRowsPerCta * kV; e += blockDim.x) {
-    const int r = e / kV, c = e % kV;
-    qs[r][c] = i0 + r < nb ? reinterpret_cast<const float4*>(qbar + (static_cast<size_t>(b0 + i0 + r) * hq + h) * D)[c]
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int r = e % kRowsPerCta, c = e / kRowsPerCta;  // consecutive threads: consecutive rows (no bank conflict)
+    const float4 x = i0 + r < nb ? reinterpret_cast<const float4*>(qbar + (static_cast<size_t>(b0 + i0 + r) * hq + h) * D)[c]
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    qt[4 * c][r] = x.x;
+    qt[4 * c + 1][r] = x.y;
+    qt[4 * c + 2][r] = x.z;
+    qt[4 * c + 3][r] = x.w;
   }
-  float* srow = scores + static_cast<size_t>(h) * tri_off[nseq] + tri_off[s] + static_cast<int64_t>(i) * (i + 1) / 2;
+  float* sbase = scores + static_cast<size_t>(h) * tri_off[nseq] + tri_off[s];
   for (int j0 = 0; j0 <= i_last; j0 += 32) {
-    __syncthreads();  // the previous chunk is consumed (first pass: qs is written)
+    __syncthreads();  // the previous chunk is consumed (first pass: qt is written)
     for (int e = threadIdx.x; e < 32 * kV; e += blockDim.x) {
-      const int jr = e / kV, c = e % kV;
+      const int jr = e % 32, c = e / 32;  // consecutive threads: consecutive keys (no bank conflict)
       const int j = j0 + jr;
       const float4 x = j <= i_last ? reinterpret_cast<const float4*>(kbar + (static_cast<size_t>(b0 + j) * hkv + hk) * D)[c]
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -103,18 +108,29 @@ __global__ void __launch_bounds__(256) block_scores_kernel(
       kt[4 * c + 3][jr] = x.w;
     }
     __syncthreads();
-    const int j = j0 + lane;
-    if (i <= i_last && j <= i) {
-      float acc = 0.f;
+    if (i0 + r0 + kRowsPerThread - 1 < j0 || i0 + r0 > i_last) continue;  // this warp's rows: all above the chunk
+    float acc[kRowsPerThread];
 #pragma unroll
-      for (int c = 0; c < kV; ++c) {
-        const float4 qv = qs[warp][c];
-        acc = fmaf(qv.x, kt[4 * c][lane], acc);
-        acc = fmaf(qv.y, kt[4 * c + 1][lane], acc);
-        acc = fmaf(qv.z, kt[4 * c + 2][lane], acc);
-        acc = fmaf(qv.w, kt[4 * c + 3][lane], acc);
-      }
-      srow[j] = acc * scale;
+    for (int u = 0; u < kRowsPerThread; ++u) acc[u] = 0.f;
+#pragma unroll 8
+    for (int d = 0; d < D; ++d) {
+      const float kv = kt[d][lane];
+      const float4 qa = *reinterpret_cast<const float4*>(&qt[d][r0]);
+      const float4 qb = *reinterpret_cast<const float4*>(&qt[d][r0 + 4]);
+      acc[0] = fmaf(qa.x, kv, acc[0]);
+      acc[1] = fmaf(qa.y, kv, acc[1]);
+      acc[2] = fmaf(qa.z, kv, acc[2]);
+      acc[3] = fmaf(qa.w, kv, acc[3]);
+      acc[4] = fmaf(qb.x, kv, acc[4]);
+      acc[5] = fmaf(qb.y, kv, acc[5]);
+      acc[6] = fmaf(qb.z, kv, acc[6]);
+      acc[7] = fmaf(qb.w, kv, acc[7]);
+    }
+    const int j = j0 + lane;
+#pragma unroll
+    for (int u = 0; u < kRowsPerThread; ++u) {
+      const int i = i0 + r0 + u;
+      if (i <= i_last && j <= i) sbase[static_cast<int64_t>(i) * (i + 1) / 2 + j] = acc[u] * scale;
     }
   }
 }
