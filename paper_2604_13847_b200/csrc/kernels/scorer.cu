@@ -59,9 +59,12 @@ __global__ void __launch_bounds__(kPoolThreads) block_pool_kernel(
 }
 
 constexpr int kRowsPerCta = 64;  // score rows per CTA
+constexpr int kColsPerCta = 64;  // keys per CTA (two 32-key chunks)
 constexpr int kRowsPerThread = 8;
 
-// Scores of 64 consecutive rows i of sequence s, q head h. The rows' Qbar are staged once,
+// Scores of 64 consecutive rows i x 64 consecutive keys j of sequence s, q head h (CTA x = one
+// lower-triangular (row tile, column tile) pair, so a long sequence's rows are not one CTA's
+// serial chain of key chunks). The rows' Qbar are staged once,
 // transposed ([d][row]); Kbar goes through shared memory in 32-key chunks ([d][key]).
 // Thread (warp w, lane l) computes rows i0 + 8w .. i0 + 8w + 7 against key j0 + l: per d one
 // 4-byte load of Kbar and two broadcast float4 loads of Qbar feed 8 FMAs. The one-warp-per-row
@@ -70,13 +73,20 @@ constexpr int kRowsPerThread = 8;
 template <int D>
 __global__ void __launch_bounds__(256) block_scores_kernel(
     const float* __restrict__ qbar, const float* __restrict__ kbar, const int32_t* __restrict__ blk_off,
-    const int64_t* __restrict__ tri_off, int nseq, int hq, int hkv, float scale, float* __restrict__ scores) {
+    const int64_t* __restrict__ tri_off, int nseq, int hq, int hkv, float scale, int tiles,
+    float* __restrict__ scores) {
   pdl_wait();  // see launch() (common.cuh)
   pdl_trigger();
   constexpr int kV = D / 4;  // float4 per row
   const int s = blockIdx.y, h = blockIdx.z;
   const int nb = blk_off[s + 1] - blk_off[s];
-  const int i0 = blockIdx.x * kRowsPerCta;
+  // blockIdx.x enumerates the lower-triangular (row tile, column tile) pairs: x = rt (rt + 1) / 2 + ct.
+  int rt = static_cast<int>((sqrtf(8.0f * blockIdx.x + 1.0f) - 1.0f) * 0.5f);
+  while ((rt + 1) * (rt + 2) / 2 <= static_cast<int>(blockIdx.x)) ++rt;
+  while (rt * (rt + 1) / 2 > static_cast<int>(blockIdx.x)) --rt;
+  const int ct = blockIdx.x - rt * (rt + 1) / 2;
+  (void)tiles;
+  const int i0 = rt * kRowsPerCta, jt0 = ct * kColsPerCta;
   if (i0 >= nb) return;
   const int b0 = blk_off[s];
   const int hk = h / (hq / hkv);
@@ -85,27 +95,45 @@ __global__ void __launch_bounds__(256) block_scores_kernel(
   const int i_last = min(i0 + kRowsPerCta - 1, nb - 1);
   __shared__ __align__(16) float qt[D][kRowsPerCta];
   __shared__ float kt[D][32];
-  for (int e = threadIdx.x; e < kRowsPerCta * kV; e += blockDim.x) {
-    const int r = e % kRowsPerCta, c = e / kRowsPerCta;  // consecutive threads: consecutive rows (no bank conflict)
-    const float4 x = i0 + r < nb ? reinterpret_cast<const float4*>(qbar + (static_cast<size_t>(b0 + i0 + r) * hq + h) * D)[c]
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-    qt[4 * c][r] = x.x;
-    qt[4 * c + 1][r] = x.y;
-    qt[4 * c + 2][r] = x.z;
-    qt[4 * c + 3][r] = x.w;
+  {  // all loads in flight before the transposed stores (consecutive threads: consecutive rows)
+    constexpr int kQ = kRowsPerCta * kV / 256;
+    float4 x[kQ];
+#pragma unroll
+    for (int u = 0; u < kQ; ++u) {
+      const int e = threadIdx.x + u * 256, r = e % kRowsPerCta, c = e / kRowsPerCta;
+      x[u] = i0 + r < nb ? __ldg(reinterpret_cast<const float4*>(qbar + (static_cast<size_t>(b0 + i0 + r) * hq + h) * D) + c)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kQ; ++u) {
+      const int e = threadIdx.x + u * 256, r = e % kRowsPerCta, c = e / kRowsPerCta;
+      qt[4 * c][r] = x[u].x;
+      qt[4 * c + 1][r] = x[u].y;
+      qt[4 * c + 2][r] = x[u].z;
+      qt[4 * c + 3][r] = x[u].w;
+    }
   }
   float* sbase = scores + static_cast<size_t>(h) * tri_off[nseq] + tri_off[s];
-  for (int j0 = 0; j0 <= i_last; j0 += 32) {
+  for (int j0 = jt0; j0 <= i_last && j0 < jt0 + kColsPerCta; j0 += 32) {
     __syncthreads();  // the previous chunk is consumed (first pass: qt is written)
-    for (int e = threadIdx.x; e < 32 * kV; e += blockDim.x) {
-      const int jr = e % 32, c = e / 32;  // consecutive threads: consecutive keys (no bank conflict)
-      const int j = j0 + jr;
-      const float4 x = j <= i_last ? reinterpret_cast<const float4*>(kbar + (static_cast<size_t>(b0 + j) * hkv + hk) * D)[c]
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-      kt[4 * c][jr] = x.x;
-      kt[4 * c + 1][jr] = x.y;
-      kt[4 * c + 2][jr] = x.z;
-      kt[4 * c + 3][jr] = x.w;
+    {
+      constexpr int kK = 32 * kV / 256;
+      float4 x[kK];
+#pragma unroll
+      for (int u = 0; u < kK; ++u) {
+        const int e = threadIdx.x + u * 256, jr = e % 32, c = e / 32;  // consecutive threads: consecutive keys
+        const int j = j0 + jr;
+        x[u] = j <= i_last ? __ldg(reinterpret_cast<const float4*>(kbar + (static_cast<size_t>(b0 + j) * hkv + hk) * D) + c)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kK; ++u) {
+        const int e = threadIdx.x + u * 256, jr = e % 32, c = e / 32;
+        kt[4 * c][jr] = x[u].x;
+        kt[4 * c + 1][jr] = x[u].y;
+        kt[4 * c + 2][jr] = x[u].z;
+        kt[4 * c + 3][jr] = x[u].w;
+      }
     }
     __syncthreads();
     if (i0 + r0 + kRowsPerThread - 1 < j0 || i0 + r0 > i_last) continue;  // this warp's rows: all above the chunk
@@ -161,12 +189,14 @@ SB_API int sb_block_scores(const float* qbar, const float* kbar, const int32_t* 
     if (nseq == 0 || nb_max == 0) return;
     sbk::require(qbar && kbar && blk_off && tri_off && scores, "null pointer");
     sbk::require(nseq <= 65535 && hq <= 65535, "nseq and hq must be <= 65535");
-    dim3 grid((nb_max + sbk::kRowsPerCta - 1) / sbk::kRowsPerCta, nseq, hq);
+    const int tiles = (nb_max + sbk::kRowsPerCta - 1) / sbk::kRowsPerCta;
+    sbk::require(static_cast<long long>(tiles) * (tiles + 1) / 2 < (1ll << 31), "nb_max too large");
+    dim3 grid(tiles * (tiles + 1) / 2, nseq, hq);  // lower-triangular tile pairs
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (head_dim == 128) {
-      sbk::launch(sbk::block_scores_kernel<128>, grid, 256, 0, st, qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, scores);
+      sbk::launch(sbk::block_scores_kernel<128>, grid, 256, 0, st, qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, tiles, scores);
     } else {
-      sbk::launch(sbk::block_scores_kernel<64>, grid, 256, 0, st, qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, scores);
+      sbk::launch(sbk::block_scores_kernel<64>, grid, 256, 0, st, qbar, kbar, blk_off, tri_off, nseq, hq, hkv, scale, tiles, scores);
     }
     sbk::launched("sb_block_scores");
   });
