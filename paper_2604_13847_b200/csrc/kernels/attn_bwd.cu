@@ -482,28 +482,80 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     int g = 0, t = 0;  // global pair counter, item counter
     uint32_t epi_need = 0;            // bit st: an item epilogue is staging through ring stage st
     int epi_uses0 = 0, epi_uses1 = 0;  // epilogues assigned to stage 0 / 1 so far
-    for (int k = 0;; ++k) {
-      KvChunk ch;
-      if (!next_chunk(k, ch)) break;
+    // Q / dO (+ augmented slices) of pair m of chunk ch into ring stage g % kStages.
+    auto load_pair = [&](const KvChunk& ch, int m, int g) {
       const KvItem& w = ch.w;
-      const int items = ch.items;
-      if (items == 0) continue;
-      const int kv0 = w.seq0 + w.jl * B;
+      const int st = g % kStages;
+      const uint32_t ph = (g / kStages) & 1;
+      int h, gi;
+      pair_of(w, ch.m0 + m, h, gi);
+      const int q0 = w.seq0 + (gi - (w.gj - w.jl)) * B;  // gj - jl: the sequence's first block
+      const int nq = min(B, w.seq_len - (gi - (w.gj - w.jl)) * B);
+      // lse2 / D of the pair's query rows: all loads in flight before the ring-slot wait.
+      float nl[B / 32], nd[B / 32];
+#pragma unroll
+      for (int e = 0; e < B / 32; ++e) {
+        const int r = e * 32 + lane;
+        const bool ok = r < nq;
+        nl[e] = ok ? __ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+        nd[e] = ok ? __ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+      }
+      // Q and dO are separate rings: the UMMA releases Q_i after dK_i and dO_i after dV_i.
+      if (lane == 0) tr(11, g);
+      if (kStagedEpi && ((epi_need >> st) & 1u)) {  // an item's dV / dK store reads this stage
+        mbar_wait(&bars->epi_free[st], ((st ? epi_uses1 : epi_uses0) - 1) & 1);
+        epi_need &= ~(1u << st);
+      }
+      mbar_wait(&bars->q_empty[st], ph ^ 1);
+      if (lane == 0) tr(12, g);
       if (lane == 0) {
-        // L2 prefetch of the next non-empty item's K / V: short items (small keep counts) would
-        // otherwise expose a DRAM round trip at every item boundary (single K / V buffer).
-        for (int k2 = k + 1; k2 < k + 4; ++k2) {
-          KvChunk ch2;
-          if (!next_chunk(k2, ch2)) break;
-          const KvItem& w2 = ch2.w;
-          if (w2.ne == 0) continue;
-          const int kv2 = w2.seq0 + w2.jl * B;
-          for (int c = 0; c < C::kChunks; ++c) {
-            tma_prefetch_l2_3d(&tm_k, c * 64, w2.hk, kv2);
-            tma_prefetch_l2_3d(&tm_v, c * 64, w2.hk, kv2);
-          }
-          break;
-        }
+        mbar_expect_tx(&bars->q_full[st], C::kQBytes);
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d(q_smem + st * C::kQBytes + c * B * 128, &tm_q, &bars->q_full[st], c * 64, h, q0);
+      }
+      uint8_t* qa = qaug_smem + st * C::kAugBytes;
+#pragma unroll
+      for (int e = 0; e < B / 32; ++e)
+        *reinterpret_cast<uint2*>(qa + aug_off(e * 32 + lane)) = split3_bf16(-nl[e] * inv_scale_log2);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> UMMA operand reads
+      __syncwarp();
+      if (lane == 0) tr(13, g);
+      if (lane == 0) mbar_arrive(&bars->q_full[st]);
+      mbar_wait(&bars->do_empty[st], ph ^ 1);
+      if (lane == 0) {
+        mbar_expect_tx(&bars->do_full[st], C::kQBytes);
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d(do_smem + st * C::kQBytes + c * B * 128, &tm_do, &bars->do_full[st], c * 64, h, q0);
+      }
+      uint8_t* da = daug_smem + st * C::kAugBytes;
+#pragma unroll
+      for (int e = 0; e < B / 32; ++e)
+        *reinterpret_cast<uint2*>(da + aug_off(e * 32 + lane)) = split3_bf16(-nd[e]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->do_full[st]);
+    };
+    // Non-empty chunks in schedule order from round k on (false past the end).
+    auto next_nonempty = [&](int& k, KvChunk& out) {
+      for (;; ++k)
+        if (!next_chunk(k, out)) return false;
+        else if (out.items > 0) return true;
+    };
+    // Per item: the first pair's Q / dO go first (they need a ring stage, not the K / V buffer),
+    // then K / V once the previous item's last S^T / dP^T are done (kv_empty), then the next
+    // item is decoded (its chain of dependent loads overlaps the tiles in flight) and its K / V
+    // prefetched to L2, then the remaining pairs. Each chunk is decoded once. Single-pair items
+    // (most of C3's under column-concentrated routing) were paced by this warp: decode, an
+    // extra look-ahead decode and K / V before Q put ~8-9k cycles on every item.
+    int kc = 0;
+    KvChunk cur;
+    bool have = next_nonempty(kc, cur);
+    while (have) {
+      const KvItem& w = cur.w;
+      const int items = cur.items;
+      const int kv0 = w.seq0 + w.jl * B;
+      load_pair(cur, 0, g);
+      if (lane == 0) {
         mbar_wait(&bars->kv_empty, (t & 1) ^ 1);
         mbar_expect_tx(&bars->kv_full, 2 * C::kTileBytes);
         for (int c = 0; c < C::kChunks; ++c) {
@@ -511,62 +563,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
           tma_load_3d(v_smem + c * kM * 128, &tm_v, &bars->kv_full, c * 64, w.hk, kv0);
         }
         tri(0, t);
+        if (trace != nullptr && blockIdx.x == 0 && t < 64) trace[4096 + t * 8 + 5] = static_cast<unsigned long long>(items);
       }
-      for (int m = 0; m < items; ++m, ++g) {
-        const int st = g % kStages;
-        const uint32_t ph = (g / kStages) & 1;
-        int h, gi;
-        pair_of(w, ch.m0 + m, h, gi);
-        const int q0 = w.seq0 + (gi - (w.gj - w.jl)) * B;  // gj - jl: the sequence's first block
-        const int nq = min(B, w.seq_len - (gi - (w.gj - w.jl)) * B);
-        // lse2 / D of the pair's query rows: all loads in flight before the ring-slot wait.
-        float nl[B / 32], nd[B / 32];
-#pragma unroll
-        for (int e = 0; e < B / 32; ++e) {
-          const int r = e * 32 + lane;
-          const bool ok = r < nq;
-          nl[e] = ok ? __ldg(lse2 + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
-          nd[e] = ok ? __ldg(dvec + static_cast<size_t>(h) * tp + q0 + r) : 0.f;
+      __syncwarp();
+      int kn = kc + 1;
+      KvChunk nxt;
+      const bool have_n = next_nonempty(kn, nxt);
+      if (lane == 0 && have_n) {
+        const int kv2 = nxt.w.seq0 + nxt.w.jl * B;
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_prefetch_l2_3d(&tm_k, c * 64, nxt.w.hk, kv2);
+          tma_prefetch_l2_3d(&tm_v, c * 64, nxt.w.hk, kv2);
         }
-        // Q and dO are separate rings: the UMMA releases Q_i after dK_i and dO_i after dV_i.
-        if (lane == 0) tr(11, g);
-        if (kStagedEpi && ((epi_need >> st) & 1u)) {  // an item's dV / dK store reads this stage
-          mbar_wait(&bars->epi_free[st], ((st ? epi_uses1 : epi_uses0) - 1) & 1);
-          epi_need &= ~(1u << st);
-        }
-        mbar_wait(&bars->q_empty[st], ph ^ 1);
-        if (lane == 0) tr(12, g);
-        if (lane == 0) {
-          mbar_expect_tx(&bars->q_full[st], C::kQBytes);
-          for (int c = 0; c < C::kChunks; ++c)
-            tma_load_3d(q_smem + st * C::kQBytes + c * B * 128, &tm_q, &bars->q_full[st], c * 64, h, q0);
-        }
-        uint8_t* qa = qaug_smem + st * C::kAugBytes;
-#pragma unroll
-        for (int e = 0; e < B / 32; ++e)
-          *reinterpret_cast<uint2*>(qa + aug_off(e * 32 + lane)) = split3_bf16(-nl[e] * inv_scale_log2);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> UMMA operand reads
-        __syncwarp();
-        if (lane == 0) tr(13, g);
-        if (lane == 0) mbar_arrive(&bars->q_full[st]);
-        if (trace != nullptr && blockIdx.x == 0) {  // debug timeline only: Q tile landing time
-          mbar_wait(&bars->q_full[st], ph);
-          if (lane == 0) tr(14, g);
-        }
-        mbar_wait(&bars->do_empty[st], ph ^ 1);
-        if (lane == 0) {
-          mbar_expect_tx(&bars->do_full[st], C::kQBytes);
-          for (int c = 0; c < C::kChunks; ++c)
-            tma_load_3d(do_smem + st * C::kQBytes + c * B * 128, &tm_do, &bars->do_full[st], c * 64, h, q0);
-        }
-        uint8_t* da = daug_smem + st * C::kAugBytes;
-#pragma unroll
-        for (int e = 0; e < B / 32; ++e)
-          *reinterpret_cast<uint2*>(da + aug_off(e * 32 + lane)) = split3_bf16(-nd[e]);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->do_full[st]);
       }
+      for (int m = 1; m < items; ++m) load_pair(cur, m, g + m);
+      g += items;
       if (kStagedEpi) {  // the item's epilogue stages through its last pair's ring stage
         const int sl = (g - 1) % kStages;
         if (sl) {
@@ -577,6 +588,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
         epi_need |= 1u << sl;
       }
       ++t;
+      cur = nxt;
+      kc = kn;
+      have = have_n;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ UMMA issuer

@@ -15,7 +15,15 @@ else:
 T = int(cu[-1]); H, D, B = 32, 128, 128
 lay = ops.VarlenLayout.build(cu, B)
 g = torch.Generator(device="cuda").manual_seed(0)
-q, k, v, do = (torch.randn((T, H, D), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+if os.environ.get("PLANTED"):  # planted column-concentrated routing (synth.py), as the bench's C3 step
+    from paper_2604_13847_b200 import synth
+    from paper_2604_13847_b200.host import api
+    lens_p = np.diff(cu).tolist()
+    _, routing = api().generate_samples(len(lens_p), 1, B, seed=7, sorted=False, dist=bench.C3_DIST)
+    rout = [np.resize(routing[s_][0], (L + B - 1) // B) for s_, L in enumerate(lens_p)]
+    q, k, v, do = synth.planted_qkv(lens_p, rout, H, H, D, B, seed=3, device="cuda")
+else:
+    q, k, v, do = (torch.randn((T, H, D), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
 S = ops.block_scores(q, k, lay)
 idx, cnt = ops.topk_select(S, lay, torch.from_numpy(k_seq).cuda(), int(k_seq.max()))
 o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)
@@ -52,5 +60,13 @@ print("t  KV issued | issuer kv wait start | kv_full seen | (wait) | prev acc_do
 for tt in range(1, min(nt, 14)):
     print(tt, int(ti[tt, 0] - ti[tt, 0]), int(ti[tt, 1] - ti[tt, 0]), int(ti[tt, 2] - ti[tt, 0]), int(ti[tt, 2] - ti[tt, 1]),
           int(ti[tt - 1, 3] - ti[tt, 0]), int(ti[tt - 1, 4] - ti[tt, 0]))
+print("item (pairs: period K/V issue -> next K/V issue), items 1..:", [f"{int(ti[tt, 5])}:{int(ti[tt + 1, 0] - ti[tt, 0])}" for tt in range(1, min(nt - 1, 40))])
 print("median K/V latency (issued -> seen):", float(np.median(ti[1:nt, 2] - ti[1:nt, 0])))
 print("median issuer wait on kv_full:", float(np.median(ti[1:nt, 2] - ti[1:nt, 1])))
+if os.environ.get("PAIRS"):  # per-pair event times (cycles) relative to the producer's pair start, pairs 1..12
+    names = {11: "prod start", 12: "q_empty ok", 13: "aug written", 14: "Q landed", 8: "iss st start", 9: "q_full seen",
+             4: "math st seen", 5: "P done", 6: "dpt seen", 7: "pds arrive", 1: "iss pds seen", 10: "dV issued"}
+    for gg in range(1, 13):
+        base = t[gg, 11]
+        print(gg, "  ".join(f"{names[s_]}={int(t[gg, s_] - base)}" for s_ in (12, 13, 14, 8, 9, 4, 5, 6, 7, 1, 10)))
+
