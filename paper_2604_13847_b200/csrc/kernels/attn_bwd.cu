@@ -345,6 +345,14 @@ constexpr int kSplitPerCta = SB_DKV_SPLIT_PER_CTA;  // cap = total pairs / (kSpl
 constexpr int kSplitMinPairs = 16;
 __host__ __device__ constexpr int split_slots(int grid) { return 2 * kSplitPerCta * grid; }
 
+// One 32-byte record per split-order entry (dkv_records_kernel): the dK/dV roles read a chunk
+// with two independent 16-byte loads instead of decoding it through a chain of dependent loads
+// (order -> blk_off binary search -> cu / tr_off), which put ~2.5k cycles on every item
+// boundary of every role.
+struct alignas(16) KvRec {
+  int e, hk, gj, jl, seq0, seq_len, e0, ne;
+};
+
 struct KvChunk {
   KvItem w;
   int it, c, nc, m0, items;  // item, chunk c of nc, its pair range [m0, m0 + items)
@@ -374,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off, int nseq, int hq, int hkv, int hsel,
     const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent, const float* __restrict__ lse2,
     const float* __restrict__ dvec, int tp, float scale, float scale_log2, uint16_t* __restrict__ dk,
-    uint16_t* __restrict__ dv, const int32_t* __restrict__ order, const int32_t* __restrict__ n_items_dev,
+    uint16_t* __restrict__ dv, const KvRec* __restrict__ recs, const int32_t* __restrict__ n_items_dev,
     const int32_t* __restrict__ slot_base, float* __restrict__ partials, unsigned long long* trace) {
   pdl_wait();  // see launch() (common.cuh)
   pdl_trigger();
@@ -448,12 +456,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
 
   // Chunk of schedule round k of this CTA (false past the end).
   auto next_chunk = [&](int k, KvChunk& ch) {
-    const int e = sched::snake_item(order, n_items, grid, cta, k);
-    if (e < 0) return false;
+    const int pos = k * grid + ((k & 1) ? (grid - 1 - cta) : cta);
+    if (pos >= n_items) return false;
+    const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + pos));
+    const int4 r1 = __ldg(reinterpret_cast<const int4*>(recs + pos) + 1);
+    const int e = r0.x;
     ch.it = e & ((1 << kSplitItemBits) - 1);
     ch.c = (e >> kSplitItemBits) & 15;
     ch.nc = e >> (kSplitItemBits + 4);
-    ch.w = decode_kv(ch.it, cu, blk_off, nseq, nbt, tr_off);
+    ch.w.hk = r0.y;
+    ch.w.gj = r0.z;
+    ch.w.jl = r0.w;
+    ch.w.seq0 = r1.x;
+    ch.w.seq_len = r1.y;
+    ch.w.e0 = r1.z;
+    ch.w.ne = r1.w;
     const int P = ch.w.ne * sg;
     ch.m0 = ch.c * P / ch.nc;
     ch.items = (ch.c + 1) * P / ch.nc - ch.m0;
@@ -1938,6 +1955,23 @@ __global__ void __launch_bounds__(1024) dkv_split_kernel(const int32_t* __restri
   }
 }
 
+// KvRec of every split-order entry (positions < counts[0]), grid-stride.
+__global__ void __launch_bounds__(256) dkv_records_kernel(const int32_t* __restrict__ order,
+                                                          const int32_t* __restrict__ counts,
+                                                          const int32_t* __restrict__ cu,
+                                                          const int32_t* __restrict__ blk_off, int nseq, int nbt,
+                                                          const int32_t* __restrict__ tr_off, KvRec* __restrict__ recs) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
+  const int n = __ldg(counts);
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const int e = order[p];
+    const KvItem w = decode_kv(e & ((1 << kSplitItemBits) - 1), cu, blk_off, nseq, nbt, tr_off);
+    reinterpret_cast<int4*>(recs + p)[0] = make_int4(e, w.hk, w.gj, w.jl);
+    reinterpret_cast<int4*>(recs + p)[1] = make_int4(w.seq0, w.seq_len, w.e0, w.ne);
+  }
+}
+
 // dK / dV of the split items: sum of the chunks' fp32 partials in chunk order (deterministic),
 // dK * scale, bf16, valid key rows only. One thread per 4-column granule; a task is 256
 // granules (256 / (D / 4) key rows) of one part of one split item, grid-strided. All of a
@@ -2005,7 +2039,7 @@ unsigned long long* g_trace_dq = nullptr;   // debug timeline buffer (sb_debug_s
 
 struct BwdWorkspace {
   size_t lse2, dvec, tr_cnt, tr_off, tr_ent, order_q, order_kv, order_kv_matched, rec_q, dqacc;
-  size_t order_split, split_counts, slot_base, split_list, partials, total;
+  size_t order_split, split_counts, slot_base, split_list, partials, recs_split, total;
   int tp;
 };
 
@@ -2047,6 +2081,8 @@ BwdWorkspace bwd_layout(int total, int nb_total, int hq, int hkv, int hsel, int 
   off = align256(off + static_cast<size_t>(split_slots(sms)) * 16);
   w.partials = off;
   off = align256(off + static_cast<size_t>(split_slots(sms)) * 2 * kM * 128 * 4);
+  w.recs_split = off;
+  off = align256(off + (kv_items + split_slots(sms)) * sizeof(KvRec));
   w.dqacc = off;  // fused path (D = 128): fp32 dQ accumulator [T][Hq][128]
   if (fused) off = align256(off + static_cast<size_t>(total) * hq * 128 * 4);
   w.total = off;
@@ -2132,6 +2168,13 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   launch(dkv_split_kernel, 1, 1024, 0, st, order_kv, kv_items, tr_off, kv_items, hq / hsel, grid_kv, order_split,
                                        split_counts, slot_base, split_list);
   launched("sb_sparse_attn_bwd/split");
+  KvRec* recs_split = reinterpret_cast<KvRec*>(ws + w.recs_split);
+  {
+    const int n_max = kv_items + split_slots(sms);
+    launch(dkv_records_kernel, std::max(1, std::min(4 * sms, (n_max + 255) / 256)), 256, 0, st, order_split,
+           split_counts, cu, blk_off, nseq, nb_total, tr_off, recs_split);
+    launched("sb_sparse_attn_bwd/records_kv");
+  }
   const int q_items = hq * nb_total;
   auto* rec_q = reinterpret_cast<sched::ItemRec*>(ws + w.rec_q);
   sched::build_q_schedule(sched::CostFromCnt{cnt, k_max, hq, hsel, nb_total}, q_items, ws + w.order_q, rec_q, cu,
@@ -2150,7 +2193,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
     set_smem_once(kern, C::kSmemBytes, "sb_sparse_attn_bwd: smem attribute (dkv)");
     launch(kern, std::min(kv_items, sms), kThreads, C::kSmemBytes, st, tq, tk, tv, tdo, tdk, tdv, cu, blk_off, nseq, hq, hkv, hsel,
                                                                    tr_off, tr_ent, lse2, dvec, w.tp, scale,
-                                                                   scale_log2, dk, dv, order_split, split_counts,
+                                                                   scale_log2, dk, dv, recs_split, split_counts,
                                                                    slot_base, partials, g_trace_bwd);
     launched("sb_sparse_attn_bwd/dkv");
     launch(dkv_split_reduce_kernel<D, B>, 8 * sms, 256, 0, st, split_list, split_counts, partials, cu, blk_off, nseq,
