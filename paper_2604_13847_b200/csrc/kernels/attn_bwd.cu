@@ -276,7 +276,7 @@ struct DkvCfg {
   static constexpr int kSmemTiles = 2 * kTileBytes + kStages * (2 * kQBytes) + kAugOnesBytes + kStages * 2 * kAugBytes;
   static constexpr int kSt = 0, kDPt = B, kDV = 2 * B, kDK = 2 * B + D;
   static constexpr uint32_t kCols = pow2_cols(2 * B + 2 * D);
-  static constexpr int kSmemBytes = kSmemTiles + 1024 + 256;
+  static constexpr int kSmemBytes = kSmemTiles + 1024 + 512;  // + alignment slack + DkvBars
 };
 
 __device__ __forceinline__ uint64_t desc_aug(uint32_t saddr) {  // SWIZZLE_NONE, LBO 128, SBO 256
@@ -303,6 +303,16 @@ __device__ __forceinline__ uint2 split3_bf16(float x) {
   return u;
 }
 
+// dK/dV work is claimed dynamically: round 0 of CTA c is entry c, every later round takes the next
+// entry of the (head-major, longest-first) split order from a global cursor. The producer warp
+// claims a round when it needs it and publishes the position through a small ring; the issuer,
+// math and store roles read it in the same round order. A static snake assignment left the CTAs'
+// loads 1.27x apart under C3's mix of single-pair and split heavy items (measured busy max / mean
+// 1.25, per-CTA busy tracking a pair + item cost model with r = 0.995). Results do not depend on
+// which CTA runs an entry.
+constexpr int kSchedRing = 8;
+constexpr int kSchedReaders = 10;  // warp leaders that read a slot: issuer, 8 math warps, store warp
+
 struct DkvBars {
   uint64_t kv_full, kv_empty;
   uint64_t q_full[kStages], q_empty[kStages];    // Q_i (+ its augmented slice) ring
@@ -313,8 +323,11 @@ struct DkvBars {
   uint64_t acc_done;           // UMMA -> epilogue: the item's dV / dK are final
   uint64_t epi_free[kStages];  // epilogue -> producer: the item's dV / dK store read ring stage st
   uint64_t epi_staged[kStages];  // math -> store warp: the item's dV / dK are staged in ring stage st
+  uint64_t sched_full[kSchedRing], sched_empty[kSchedRing];  // producer <-> roles: schedule ring
+  int32_t sched_pos[kSchedRing];  // split-order position of round k in slot k % kSchedRing (-1: end)
   uint32_t tmem_base;
 };
+static_assert(sizeof(DkvBars) <= 512, "DkvBars fits the reserved tail of the dK/dV shared memory");
 
 // TMEM column (relative to dP^T) of the packed-bf16 P^T (dS^T: + 16) for UMMA K step kk.
 // Warpgroup hf owns query columns [hf * B/2, (hf + 1) * B/2) of dP^T; it writes chunk c2 (32
@@ -382,12 +395,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
     const int32_t* __restrict__ cu, const int32_t* __restrict__ blk_off, int nseq, int hq, int hkv, int hsel,
     const int32_t* __restrict__ tr_off, const int32_t* __restrict__ tr_ent, const float* __restrict__ lse2,
     const float* __restrict__ dvec, int tp, float scale, float scale_log2, uint16_t* __restrict__ dk,
-    uint16_t* __restrict__ dv, const KvRec* __restrict__ recs, const int32_t* __restrict__ n_items_dev,
+    uint16_t* __restrict__ dv, const KvRec* __restrict__ recs, int32_t* __restrict__ sched_counts,
     const int32_t* __restrict__ slot_base, float* __restrict__ partials, unsigned long long* trace) {
   pdl_wait();  // see launch() (common.cuh)
   pdl_trigger();
   using C = DkvCfg<D, B>;
-  const int n_items = __ldg(n_items_dev);  // entries of the split order (dkv_split_kernel)
+  const int n_items = sched_counts[0];  // entries of the split order (dkv_split_kernel); [2] is the cursor
+  // Debug: per-CTA start / end (globaltimer ns) at trace[8192 + 2 * cta + {0, 1}].
+  if (trace != nullptr && threadIdx.x == 0) trace[8192 + 2 * blockIdx.x] = globaltimer_ns();
   // D = B = 128: an item's dV / dK (32 KB each) are stored by TMA through the Q / dO slots of
   // the ring stage its last pair used, free once acc_done fires (see the epilogue).
   constexpr bool kStagedEpi = D == 128 && B == 128;
@@ -436,6 +451,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
       mbar_init(&bars->epi_free[st], 1);
       mbar_init(&bars->epi_staged[st], 256);
     }
+    for (int r = 0; r < kSchedRing; ++r) {
+      mbar_init(&bars->sched_full[r], 1);
+      mbar_init(&bars->sched_empty[r], kStagedEpi ? kSchedReaders : kSchedReaders - 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kCols>(&bars->tmem_base);
@@ -454,10 +473,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  // Chunk of schedule round k of this CTA (false past the end).
+  // Split-order position of round k. The producer warp (whole warp, in round order) claims it
+  // and publishes it in ring slot k % kSchedRing; every other role (whole warp, in round order)
+  // reads it there and releases the slot.
+  auto round_pos = [&](int k) {
+    const int slot = k % kSchedRing;
+    const uint32_t ph = (k / kSchedRing) & 1;
+    int pos;
+    if (warp == 0) {
+      if (lane == 0) {
+        if (k >= kSchedRing) mbar_wait(&bars->sched_empty[slot], ph ^ 1);
+        pos = k == 0 ? cta : grid + atomicAdd(sched_counts + 2, 1);
+        if (pos >= n_items) pos = -1;
+        bars->sched_pos[slot] = pos;
+        mbar_arrive(&bars->sched_full[slot]);  // release: the position is visible to the waiters
+      }
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+    } else {
+      mbar_wait(&bars->sched_full[slot], ph);
+      pos = *reinterpret_cast<volatile int32_t*>(&bars->sched_pos[slot]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->sched_empty[slot]);
+    }
+    return pos;
+  };
+  // Chunk of schedule round k of this CTA (false past the end). Each role calls it once per
+  // round, in round order, until it returns false.
   auto next_chunk = [&](int k, KvChunk& ch) {
-    const int pos = k * grid + ((k & 1) ? (grid - 1 - cta) : cta);
-    if (pos >= n_items) return false;
+    const int pos = round_pos(k);
+    if (pos < 0) return false;
     const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + pos));
     const int4 r1 = __ldg(reinterpret_cast<const int4*>(recs + pos) + 1);
     const int e = r0.x;
@@ -908,6 +952,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dkv_kernel(
   }
   tc_fence_before();
   __syncthreads();
+  if (trace != nullptr && threadIdx.x == 0) trace[8192 + 2 * blockIdx.x + 1] = globaltimer_ns();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::kCols>(tmem);
@@ -1952,6 +1997,7 @@ __global__ void __launch_bounds__(1024) dkv_split_kernel(const int32_t* __restri
   if (threadIdx.x == 1023) {
     counts[0] = oa;
     counts[1] = ob;
+    counts[2] = 0;  // the dK/dV pass's dynamic schedule cursor
   }
 }
 

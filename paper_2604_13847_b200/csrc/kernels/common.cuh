@@ -51,6 +51,11 @@ inline void cuda_check(cudaError_t e, const char* where) {
 // once the predecessor grid has completed and its writes are visible), then pdl_trigger() so its
 // own dependent may be scheduled. A successor can only occupy resources that are free, so a
 // persistent kernel's successor starts on SMs as its CTAs exit.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {  // debug timelines (SM-independent clock)
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -27,7 +27,7 @@ else:
 S = ops.block_scores(q, k, lay)
 idx, cnt = ops.topk_select(S, lay, torch.from_numpy(k_seq).cuda(), int(k_seq.max()))
 o, lse = ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)
-buf = torch.zeros(256 * 16 + 64 * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(8192 + 2 * 256, dtype=torch.int64, device="cuda")
 for it in range(3):
     lib.sb_debug_set_trace_bwd(ctypes.c_void_p(buf.data_ptr() if it == 2 else 0))
     ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
