@@ -2164,19 +2164,32 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   launch(transpose_sel_kernel, (kv_items + 3) / 4, 128, 0, st, idx, cnt, blk_off, nseq, hkv, rows_per_kv, k_max, 1,
                                                             tr_cnt, tr_off, tr_ent);
   launched("sb_sparse_attn_bwd/transpose_fill");
-  const int32_t* order_kv_lpt = sched::build_order(sched::CostFromLists{tr_off, hq / hsel, kMaxKvCost, nb_total, hkv},
-                                                   kv_items, ws + w.order_kv, st, "sb_sparse_attn_bwd/order_kv");
+  // Two-pass dK/dV (dynamic claiming): long items lead their head (CostFromLists::lead). Fused
+  // (static snake + round matching): plain head-major longest-first.
+  const int grid_kv = std::min(kv_items, sms);
+  sched::CostFromLists kv_cost{tr_off, hq / hsel, kMaxKvCost, nb_total, hkv};
+#ifndef SB_DKV_LEAD
+#define SB_DKV_LEAD 1
+#endif
+  if (!fused && SB_DKV_LEAD) {
+    // Long = over a quarter of the split cap; a cap-sized entry lasts ~hkv / 4 heads' stretch of
+    // the list (cap = total / (kSplitPerCta * grid) pairs, one head = total / (hkv * grid) per CTA).
+    kv_cost.long_div = 4 * kSplitPerCta * grid_kv;
+    kv_cost.long_min = kSplitMinPairs;
+    kv_cost.lead = (hkv + kSplitPerCta - 1) / kSplitPerCta;
+  }
+  const int32_t* order_kv_lpt = sched::build_order(kv_cost, kv_items, ws + w.order_kv, st, "sb_sparse_attn_bwd/order_kv");
   // Round matching (sched.cuh) runs its rounds in sequence on one CTA, ~5.3 us per round of 148
   // (both cost constants below were calibrated on B200)
   // items on B200; it wins ~6 % of the dK/dV pass where items are long (C5: -4 to -10 % bwd) and
   // loses where they are short (C2: 295 us of matching for ~110 us won). Use it only when 6 % of
   // the dK/dV upper-bound estimate (hq * NB * k_max q tiles at ~2.3 us, causal half) exceeds it.
-  const int grid_kv = std::min(kv_items, sms);
   const double match_us = 5.3 * ((kv_items + grid_kv - 1) / grid_kv);
   const double dkv_est_us = static_cast<double>(hq) * nb_total * k_max * 2.3 / 2.0 / grid_kv;
   const int32_t* order_kv = order_kv_lpt;
   // match_rounds_kernel keeps per-CTA state in 256-entry shared arrays: grid_kv <= 256 (B200: 148).
-  if (grid_kv <= sched::kMatchMaxGrid && match_us < 0.06 * dkv_est_us) {
+  // Only the fused kernel walks a static snake; the two-pass dK/dV kernel claims entries dynamically.
+  if (fused && grid_kv <= sched::kMatchMaxGrid && match_us < 0.06 * dkv_est_us) {
     int32_t* matched = reinterpret_cast<int32_t*>(ws + w.order_kv_matched);
     launch(sched::match_rounds_kernel<sched::ListCost>, 1, sched::kMatchThreads, 0, st, sched::ListCost{tr_off, hq / hsel}, order_kv_lpt,
                                                                    kv_items, grid_kv, matched);

@@ -33,9 +33,20 @@ struct CostFromLists {  // dkv: item = hk * NB + gj, cost = (#selection rows lis
   int per_entry;
   int max_cost;
   int nb_total, hkv;
+  // lead > 0 (dK/dV, dynamic claiming): an item longer than thr = max(long_min, ceil(total /
+  // long_div)) pairs is ordered with head hk - lead instead of its own head, so no long item is
+  // claimed in the last `lead` heads' stretch of the list and the pass ends on short items. With
+  // plain head-major order the last head's long items (split chunks and items just under the
+  // split cap, ~100 us each at C3) ran alone after every other CTA had finished.
+  int lead = 0, long_div = 1, long_min = 0;
   __device__ int operator()(int item) const {
-    const int hk = item / nb_total;
+    int hk = item / nb_total;
     const int c = (tr_off[item + 1] - tr_off[item]) * per_entry;
+    if (lead > 0) {
+      const int total = tr_off[nb_total * hkv] * per_entry;
+      const int thr = max(long_min, (total + long_div - 1) / long_div);
+      if (c > thr) hk = max(0, hk - lead);
+    }
     return hk * (max_cost + 1) + (max_cost - min(c, max_cost));
   }
   int bins() const { return hkv * (max_cost + 1); }
