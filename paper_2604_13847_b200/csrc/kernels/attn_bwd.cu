@@ -1010,6 +1010,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
   pdl_trigger();
   using C = DqCfg<D, B>;
   constexpr int kKS = C::kKStages, kVS = C::kVStages;
+  if (trace != nullptr && threadIdx.x == 0) trace[8192 + 2 * blockIdx.x] = globaltimer_ns();  // per-CTA span
   auto tr = [&](int slot, int g) {
     if (trace != nullptr && blockIdx.x == 0 && g < 256 && (threadIdx.x & 31) == 0) trace[g * 16 + slot] = clock64();
   };
@@ -1387,6 +1388,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_dq_kernel(
   }
   tc_fence_before();
   __syncthreads();
+  if (trace != nullptr && threadIdx.x == 0) trace[8192 + 2 * blockIdx.x + 1] = globaltimer_ns();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::kCols>(tmem);

@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
   pdl_wait();  // see launch() (common.cuh)
   pdl_trigger();
   using C = Fwd2Cfg<D, B>;
+  if (trace != nullptr && threadIdx.x == 0) trace[8192 + 2 * blockIdx.x] = globaltimer_ns();  // per-CTA span
   // Debug timeline: CTA 0, per stream s and block g < 256: [s][g][slot] (slots: 0 QK issued,
   // 1 PV issued, 2 S seen by softmax warp 0, 3 P arrived, 4 epilogue start, 5 end, 6 k_full seen).
   // An L2 prefetch of block j+1's K / V one block early was measured 4% slower.
@@ -430,6 +431,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
   }
   tc_fence_before();
   __syncthreads();
+  if (trace != nullptr && threadIdx.x == 0) trace[8192 + 2 * blockIdx.x + 1] = globaltimer_ns();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);

@@ -84,19 +84,30 @@ print(f"fwd {timeit(lambda: ops.sparse_attn_fwd(q, k, v, lay, idx, cnt)):.3f} ms
 
 import ctypes
 lib = ops._lib()
-lib.sb_debug_set_trace_bwd.argtypes = [ctypes.c_void_p]
-buf = torch.zeros(8192 + 2 * 256, dtype=torch.int64, device="cuda")
-lib.sb_debug_set_trace_bwd(ctypes.c_void_p(buf.data_ptr()))
-ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
-torch.cuda.synchronize()
-lib.sb_debug_set_trace_bwd(ctypes.c_void_p(0))
-st = buf.cpu().numpy()[8192:8192 + 2 * grid].reshape(grid, 2).astype(np.int64)
-t0 = st[:, 0].min()
-dur = (st[:, 1] - st[:, 0]) / 1e3
-end = (st[:, 1] - t0) / 1e3
-beg = (st[:, 0] - t0) / 1e3
-print(f"dkv per-CTA (us): start max {beg.max():.1f}; busy min {dur.min():.0f} median {np.median(dur):.0f} "
-      f"max {dur.max():.0f}; span {end.max():.0f}; mean busy / span {dur.mean() / end.max():.3f}")
-print("dkv per-CTA busy sorted (us):", np.sort(dur).astype(int).tolist())
-cyc = load / 1.635e3
-print("model vs measured corr:", float(np.corrcoef(cyc, dur)[0, 1]))
+for nm in ("sb_debug_set_trace_bwd", "sb_debug_set_trace_dq", "sb_debug_set_trace"):
+    getattr(lib, nm).argtypes = [ctypes.c_void_p]
+
+
+def spans(setter, fn, label):
+    """Per-CTA busy spans (globaltimer stamps at trace[8192 + 2 cta + {0, 1}]) of one launch."""
+    buf = torch.zeros(8192 + 2 * 256, dtype=torch.int64, device="cuda")
+    getattr(lib, setter)(ctypes.c_void_p(buf.data_ptr()))
+    fn()
+    torch.cuda.synchronize()
+    getattr(lib, setter)(ctypes.c_void_p(0))
+    st = buf.cpu().numpy()[8192:8192 + 2 * 256].reshape(256, 2).astype(np.int64)
+    st = st[st[:, 0] > 0]
+    t0 = st[:, 0].min()
+    dur = (st[:, 1] - st[:, 0]) / 1e3
+    end = (st[:, 1] - t0) / 1e3
+    beg = (st[:, 0] - t0) / 1e3
+    print(f"{label} per-CTA (us), {len(st)} CTAs: start max {beg.max():.1f}; busy min {dur.min():.0f} median "
+          f"{np.median(dur):.0f} max {dur.max():.0f}; span {end.max():.0f}; mean busy / span {dur.mean() / end.max():.3f}")
+    print(f"{label} per-CTA busy sorted (us):", np.sort(dur).astype(int).tolist())
+    return dur
+
+
+bwd = lambda: ops.sparse_attn_bwd(q, k, v, o, do, lse, lay, idx, cnt)
+spans("sb_debug_set_trace_bwd", bwd, "dkv")
+spans("sb_debug_set_trace_dq", bwd, "dq")
+spans("sb_debug_set_trace", lambda: ops.sparse_attn_fwd(q, k, v, lay, idx, cnt), "fwd")

@@ -34,7 +34,7 @@ for it in range(3):
 torch.cuda.synchronize()
 allb = buf.cpu().numpy().astype(np.int64)
 t = allb[:4096].reshape(256, 16)
-ti = allb[4096:].reshape(64, 8)
+ti = allb[4096:4608].reshape(64, 8)
 n = int((t[:, 0] > 0).sum())
 r = slice(2, n - 2)
 print("pairs traced", n)
