@@ -2176,8 +2176,14 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
   if (!fused && SB_DKV_LEAD) {
     // Long = over a quarter of the split cap; a cap-sized entry lasts ~hkv / 4 heads' stretch of
     // the list (cap = total / (kSplitPerCta * grid) pairs, one head = total / (hkv * grid) per CTA).
-    kv_cost.long_div = 4 * kSplitPerCta * grid_kv;
-    kv_cost.long_min = kSplitMinPairs;
+#ifndef SB_DKV_LONG_FRAC
+#define SB_DKV_LONG_FRAC 4
+#endif
+#ifndef SB_DKV_LONG_MIN
+#define SB_DKV_LONG_MIN kSplitMinPairs
+#endif
+    kv_cost.long_div = SB_DKV_LONG_FRAC * kSplitPerCta * grid_kv;
+    kv_cost.long_min = SB_DKV_LONG_MIN;
     kv_cost.lead = (hkv + kSplitPerCta - 1) / kSplitPerCta;
   }
   const int32_t* order_kv_lpt = sched::build_order(kv_cost, kv_items, ws + w.order_kv, st, "sb_sparse_attn_bwd/order_kv");

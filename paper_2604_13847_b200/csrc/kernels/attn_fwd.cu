@@ -131,14 +131,25 @@ struct Fwd2Cfg {
   static constexpr int kSmemTiles = 2 * kQBytes + 4 * kKVBytes + 2 * kStageBytes;  // per stream: Q, K, V, stage
   static constexpr int kTmemO = 2 * B;                          // S_s at s * B, O_s at 2B + s * D
   static constexpr uint32_t kTmemCols = (2 * B + 2 * D) <= 256 ? 256 : 512;
-  static constexpr int kSmemBytes = kSmemTiles + 1024 + 256;
+  static constexpr int kSmemBytes = kSmemTiles + 1024 + 1024;  // + alignment slack + Fwd2Bars
 };
+
+// Items are claimed dynamically, per stream: stream s of CTA c starts at its snake slot of round
+// s (c, or 2G - 1 - c), and every later item comes from a global cursor (reset by
+// q_records_kernel) in the head-major, longest-first order. The stream's producer claims one item
+// ahead and publishes the 32-byte record in a shared-memory ring that the stream's issuer and
+// softmax warps read in order. The static snake left C2's per-CTA busy spans 1.08x apart.
+constexpr int kFwdRing = 8;
+constexpr int kFwdRingReaders = 5;  // the stream's issuer warp and its 4 softmax warps
 
 struct Fwd2Bars {
   uint64_t q_full[2], q_empty[2], k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t s_full[2], p_full[2], o_done[2], o_free[2];
+  uint64_t sched_full[2][kFwdRing], sched_empty[2][kFwdRing];
+  int4 sched_rec[2][kFwdRing][2];  // sched::ItemRec of round k in slot k % kFwdRing
   uint32_t tmem_base;
 };
+static_assert(sizeof(Fwd2Bars) <= 1024, "Fwd2Bars fits the reserved tail of the forward's shared memory");
 
 template <int D, int B>
 __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
@@ -183,6 +194,10 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
       mbar_init(&bars->p_full[s], 128);
       mbar_init(&bars->o_done[s], 1);
       mbar_init(&bars->o_free[s], 128);
+      for (int i = 0; i < kFwdRing; ++i) {
+        mbar_init(&bars->sched_full[s][i], 1);
+        mbar_init(&bars->sched_empty[s][i], kFwdRingReaders);
+      }
     }
     fence_barrier_init();
   }
@@ -191,6 +206,31 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  int* cursor = const_cast<int*>(reinterpret_cast<const int*>(recs + n_items));  // sched::rec_workspace_bytes slack
+  // Round k of stream s: claimed and published by the stream's producer (lane 0) ...
+  auto claim = [&](int s, int k) {
+    const int slot = k % kFwdRing;
+    if (k >= kFwdRing) mbar_wait_spin(&bars->sched_empty[s][slot], ((k / kFwdRing) & 1) ^ 1);
+    const int pos = k == 0 ? (s == 0 ? cta : 2 * grid - 1 - cta) : 2 * grid + atomicAdd(cursor, 1);
+    int4 a = make_int4(-1, 0, 0, 0), b = make_int4(0, 0, 0, 0);
+    if (pos < n_items) {
+      a = __ldg(reinterpret_cast<const int4*>(recs + pos));
+      b = __ldg(reinterpret_cast<const int4*>(recs + pos) + 1);
+    }
+    bars->sched_rec[s][slot][0] = a;
+    bars->sched_rec[s][slot][1] = b;
+    mbar_arrive(&bars->sched_full[s][slot]);  // release: the record is visible to the waiters
+    return sched::ItemRec{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  };
+  // ... and read, in round order, by each of its issuer and softmax warps (whole warp).
+  auto take = [&](int s, int k) {
+    const int slot = k % kFwdRing;
+    mbar_wait_spin(&bars->sched_full[s][slot], (k / kFwdRing) & 1);
+    const int4 a = bars->sched_rec[s][slot][0], b = bars->sched_rec[s][slot][1];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars->sched_empty[s][slot]);
+    return sched::ItemRec{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  };
 
   if (warp < 4) {
     setmaxnreg_dec<56>();
@@ -205,23 +245,19 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
         uint8_t* ks = k_smem + s * C::kKVBytes;
         uint8_t* vs = v_smem + s * C::kKVBytes;
         int g = 0, q = 0;
-        for (sched::RecCursor cur(recs, n_items, grid, cta, s, 2);;) {
-          const sched::ItemRec rec = cur.next();
+        sched::ItemRec nr = claim(s, 0);
+        for (int k = 0;; ++k) {
+          const sched::ItemRec rec = nr;
           if (rec.it < 0) break;
+          nr = claim(s, k + 1);
           const Item w = from_rec(rec, nbt, idx, k_max);
           if (w.n <= 0) continue;
           const int hk = w.h / (hq / hkv);
-          {  // L2 prefetch of this stream's next item's Q tile: its load waits for this item's last
-             // QK, so with few blocks per item a DRAM round trip would sit on the stream's chain
-            sched::RecCursor peek = cur;
-            for (int e = 0; e < 4; ++e) {
-              const sched::ItemRec nr = peek.next();
-              if (nr.it < 0) break;
-              if (nr.n <= 0) continue;
-              for (int c = 0; c < C::kChunks; ++c)
-                tma_prefetch_l2_3d(&tm_q, c * 64, nr.it / nbt, nr.seq0 + nr.loc * B);
-              break;
-            }
+          if (nr.it >= 0 && nr.n > 0) {
+            // L2 prefetch of this stream's next item's Q tile: its load waits for this item's last
+            // QK, so with few blocks per item a DRAM round trip would sit on the stream's chain
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_prefetch_l2_3d(&tm_q, c * 64, nr.it / nbt, nr.seq0 + nr.loc * B);
           }
           mbar_wait_spin(&bars->q_empty[s], (q & 1) ^ 1);
           mbar_expect_tx(&bars->q_full[s], C::kQBytes);
@@ -250,8 +286,8 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
       const uint32_t k_addr = smem_u32(k_smem + s * C::kKVBytes), v_addr = smem_u32(v_smem + s * C::kKVBytes);
       const uint32_t d_s = tmem + s * B, d_o = tmem + C::kTmemO + s * D;
       int g = 0, q = 0;
-      for (sched::RecCursor cur(recs, n_items, grid, cta, s, 2);;) {
-        const sched::ItemRec rec = cur.next();
+      for (int k = 0;; ++k) {
+        const sched::ItemRec rec = take(s, k);
         if (rec.it < 0) break;
         const int n = rec.n;
         if (n <= 0) continue;
@@ -296,8 +332,8 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(
     const uint32_t lane_field = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t t_s = tmem + lane_field + s * B, t_o = tmem + lane_field + C::kTmemO + s * D;
     int g = 0, q = 0;
-    for (sched::RecCursor cur(recs, n_items, grid, cta, s, 2);;) {
-      const sched::ItemRec rec = cur.next();
+    for (int k = 0;; ++k) {
+      const sched::ItemRec rec = take(s, k);
       if (rec.it < 0) break;
       const Item w = from_rec(rec, nbt, idx, k_max);
       const int row0 = w.seq0 + w.i * B;

@@ -340,6 +340,7 @@ __global__ void q_records_kernel(const int32_t* __restrict__ order, int n_items,
   pdl_wait();  // see launch() (common.cuh)
   pdl_trigger();
   const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos == 0) *reinterpret_cast<int*>(rec + n_items) = 0;  // the forward's dynamic-claim cursor
   if (pos >= n_items) return;
   rec[pos] = q_record(order[pos], cu, blk_off, nseq, nbt, hq, hsel, idx, cnt, k_max);
 }
