@@ -6,7 +6,12 @@ from paper_2604_13847_b200 import ops
 import bench
 lib = ops._lib()
 lib.sb_debug_set_trace_dq.argtypes = [ctypes.c_void_p]
-cu, k_seq = bench.workload(0)
+if os.environ.get("C3K"):  # C3 rank micro-batch [2048 x3, 32768, 2048] at a fixed keep count
+    lens = [2048, 2048, 2048, 32768, 2048]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    k_seq = np.minimum(int(os.environ["C3K"]), (np.array(lens) + 127) // 128).astype(np.int32)
+else:
+    cu, k_seq = bench.workload(0)
 T = int(cu[-1]); H, D, B = 32, 128, 128
 lay = ops.VarlenLayout.build(cu, B)
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -48,3 +53,11 @@ nq = int((ti[:, 0] > 0).sum())
 print("items", nq, "; math dq_done -> epilogue stores done:", med(ti[1:nq, 1] - ti[1:nq, 0]))
 print("issuer stage_full wait (Q/dO staging for the next item):", med(ti[2:nq, 3] - ti[2:nq, 2]))
 print("issuer load_qdo start - math dq_done of the previous item:", med(ti[2:nq, 2] - ti[1:nq - 1, 0]))
+if os.environ.get("ROWS"):  # raw per-block stamps relative to block 0's ds-wait start
+    names = {0: "ds wait", 1: "ds seen", 2: "iss_s start", 3: "k_full seen", 4: "v wait", 5: "v seen", 6: "dQ issued",
+             8: "math s seen", 9: "P done", 10: "dp seen", 11: "ds stored"}
+    base = t[0, 0]
+    for gg in range(int(os.environ["ROWS"])):
+        print(gg, "  ".join(f"{nm}={int(t[gg, sl] - base)}" for sl, nm in names.items()))
+    for qq in range(min(nq, 8)):
+        print("item", qq, [int(ti[qq, j] - base) for j in range(4)])
