@@ -47,6 +47,7 @@ __device__ __forceinline__ int block_excl_scan(bool flag, int* warp_tot, int* to
 }
 
 constexpr int kWarpRow = 256;  // rows up to this many candidates: one warp per row
+constexpr int kArgmaxRounds = 8;  // keep counts up to this: iterated warp argmax instead of the radix select
 
 __global__ void __launch_bounds__(256) topk_select_warp_kernel(
     const float* __restrict__ scores, const int32_t* __restrict__ blk_off, const int64_t* __restrict__ tri_off,
@@ -93,6 +94,47 @@ __global__ void __launch_bounds__(256) topk_select_warp_kernel(
     key[r] = j < m ? order_key(v) : 0u;
   }
   const int slots = (m + 31) >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  if (want <= kArgmaxRounds) {
+    // Few to keep (C3: k = 5): `want` rounds of a warp argmax over (key, ~index), i.e. score
+    // descending, index ascending -- the same set as the radix select below in ~1/3 of its
+    // instructions. Valid keys are > 0 (order_key(-inf) = 0x007FFFFF), so 0 marks taken / past m.
+    uint32_t taken = 0;  // bit r: candidate r * 32 + lane is kept
+#pragma unroll 1
+    for (int t = 0; t < want; ++t) {
+      unsigned long long best = 0ull;
+#pragma unroll
+      for (int r = 0; r < kWarpRow / 32; ++r) {
+        if (r >= slots) break;
+        const int j = r * 32 + lane;
+        const unsigned long long c =
+            (j < m && !((taken >> r) & 1u)) ? (static_cast<unsigned long long>(key[r]) << 32) | static_cast<uint32_t>(~j)
+                                            : 0ull;
+        best = c > best ? c : best;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+        best = x > best ? x : best;
+      }
+      const int jw = static_cast<int>(~static_cast<uint32_t>(best));
+      if ((jw & 31) == lane) taken |= 1u << (jw >> 5);
+    }
+    int kept_before = 0;
+#pragma unroll
+    for (int r = 0; r < kWarpRow / 32; ++r) {
+      if (r >= slots) break;
+      const bool keep = (taken >> r) & 1u;
+      const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+      if (keep) out[kept_before + __popc(kb & lt)] = r * 32 + lane;
+      kept_before += __popc(kb);
+    }
+    for (int r = lane; r < k_max; r += 32) {
+      if (r == want && force_diag) out[r] = i;
+      else if (r >= k) out[r] = -1;
+    }
+    return;
+  }
   // Bitwise radix select of the want-th largest key among the m candidates.
   uint32_t prefix = 0;
   int remaining = want;
@@ -114,7 +156,6 @@ __global__ void __launch_bounds__(256) topk_select_warp_kernel(
     }
   }
   const uint32_t thresh = prefix;  // keys > thresh all kept; `remaining` of the == thresh kept
-  const uint32_t lt = (1u << lane) - 1u;
   int ties_before = 0, kept_before = 0;
 #pragma unroll
   for (int r = 0; r < kWarpRow / 32; ++r) {

@@ -75,7 +75,7 @@ def test_topk_select_bitexact(force_diag, group, ties, nans):
     lay = _layout(cu, 64)
     hs = 8
     S = _rand_scores(lay, hs, 7 + group, ties, nans)
-    for k_seq in ([1, 2, 3, 4], [16, 8, 1, 40], [71, 301, 1, 1501], [5, 200, 2, 700]):
+    for k_seq in ([1, 2, 3, 4], [16, 8, 1, 40], [71, 301, 1, 1501], [5, 200, 2, 700], [9, 8, 1, 9], [10, 9, 1, 3]):
         k_max = max(k_seq)
         idx, cnt = ops.topk_select(torch.from_numpy(S).cuda(), lay, torch.tensor(k_seq, dtype=torch.int32).cuda(),
                                    k_max, group=group, force_diag=bool(force_diag))
