@@ -21,11 +21,15 @@ collectives are the step-3 all-gather and the caller's gradient all-reduce.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import List, Sequence
 
 import numpy as np
 import torch
+
+# SB_NVTX=1: an NVTX range per layer phase (select + fwd, bwd) for nsys / ncu --nvtx timelines.
+_NVTX = os.environ.get("SB_NVTX", "0") == "1"
 
 from . import ops
 from .host import DEFAULT_BUDGET_GRID, ProfileTable, api
@@ -302,12 +306,20 @@ class DPStep:
         for l, s_l in enumerate(self.layer_scales):
             k_max = int(max(1, k_all[l].max()))
             scale = s_l / math.sqrt(self.d)
+            if _NVTX:
+                torch.cuda.nvtx.range_push(f"layer {l} k<={k_max}: select + fwd")
             idx, cnt = ops.topk_select(scores[l], lay, k_dev[l], k_max, group=self.sel_group)
             o, lse = ops.sparse_attn_fwd(self.q, self.k, self.v, lay, idx, cnt, scale)
+            if _NVTX:
+                torch.cuda.nvtx.range_pop()
             if mark:
                 mark("fwd")
+            if _NVTX and backward:
+                torch.cuda.nvtx.range_push(f"layer {l}: bwd")
             grads = (ops.sparse_attn_bwd(self.q, self.k, self.v, o, self.do, lse, lay, idx, cnt, scale,
                                          fused=self.fused_bwd) if backward else None)
+            if _NVTX and backward:
+                torch.cuda.nvtx.range_pop()
             if mark:
                 mark("bwd")
             if grad_buckets is not None and self.world > 1:

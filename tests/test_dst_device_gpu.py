@@ -97,3 +97,31 @@ def test_dpstep_on_device_matches_host_path():
         assert got == k_final[0].tolist(), (p, got, k_final[0].tolist())
         changed = changed or any(d.micro_batch_id == 0 and d.k_final != d.k_base for d in decisions)
     assert changed  # the coverage test compressed this rank at least once: the comparison is not trivial
+
+
+def test_dpstep_nvtx_ranges(monkeypatch):
+    """SB_NVTX=1 (dp._NVTX): the host-DST step pushes / pops one NVTX range per layer phase and
+    returns the same selections as without them."""
+    from paper_2604_13847_b200 import dp, ops
+    from paper_2604_13847_b200.host import api
+
+    lens = [4096, 2048]
+    X = int(sum(lens))
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    B, H, D, L = 128, 4, 128, 3
+    lay = ops.VarlenLayout.build(cu, B)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v, do = (torch.randn((X, H, D), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+    scales = np.ones(L)
+    batch = dp.RankBatch(np.asarray(lens), list(range(len(lens))), lay)
+    step = dp.DPStep(batch, q, k, v, do, scales, api().synthesize_table(block_size=B), dp.DstSettings())
+    plain = step.run(backward=True)
+    pushes = []
+    monkeypatch.setattr(dp, "_NVTX", True)
+    monkeypatch.setattr(torch.cuda.nvtx, "range_push", lambda msg: pushes.append(msg))
+    monkeypatch.setattr(torch.cuda.nvtx, "range_pop", lambda: None)
+    traced = step.run(backward=True)
+    torch.cuda.synchronize()
+    assert len(pushes) == 2 * L and pushes[0].startswith("layer 0")
+    for (i0, c0, *_), (i1, c1, *_) in zip(plain, traced):
+        assert torch.equal(i0, i1) and torch.equal(c0, c1)
