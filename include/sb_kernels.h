@@ -11,6 +11,10 @@
  *  - All pointers are caller-owned DEVICE memory unless named *_host. bf16 tensors are
  *    passed as uint16_t*. No allocation and no host synchronisation inside any call; every
  *    call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *  - A workspace belongs to one call at a time: the attention kernels keep their work order
+ *    and a work-claiming cursor in it (reset inside the call), so calls that may overlap in
+ *    time (different streams) need separate workspaces. Results do not depend on which CTA
+ *    claims which work item: outputs are bit-identical run to run.
  *  - Packed varlen batch: cu_seqlens int32 [nseq+1] (cu[0] = 0, T = cu[nseq]).
  *    Block size B in {64, 128}; nb_s = ceil(L_s / B).
  *    blk_off int32 [nseq+1]: prefix sums of nb_s (NB = blk_off[nseq] blocks in total).
