@@ -5,9 +5,10 @@
 // the key (head, cost descending): keeping one head's items together makes the ~148 resident
 // CTAs share that head's K/V (or Q/dO) slabs in L2 (16 MB per head at 32K tokens, d=128),
 // while longest-first inside the head and across the whole list keeps the tail short. CTAs
-// of the forward and dQ passes walk the list in snake order (c, 2G-1-c, 2G+c, ...); the dK/dV
-// pass claims entries past round 0 from a global cursor (attn_bwd.cu, kSchedRing). The sort is
-// a counting sort on the device (histogram, scan, scatter).
+// of the dQ pass walk the list in snake order (c, 2G-1-c, 2G+c, ...); the forward (per item
+// stream) and the dK/dV pass take their first round there and claim every later entry from a
+// global cursor (attn_fwd.cu kFwdRing, attn_bwd.cu kSchedRing). The sort is a counting sort on
+// the device (histogram, scan, scatter).
 #pragma once
 
 #include "common.cuh"
