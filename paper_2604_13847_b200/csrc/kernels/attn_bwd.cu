@@ -1942,34 +1942,17 @@ __global__ void __launch_bounds__(1024) dkv_split_kernel(const int32_t* __restri
   const int cap = max(kSplitMinPairs, (total + kSplitPerCta * grid - 1) / (kSplitPerCta * grid));
   const int per = (n + 1023) / 1024;
   const int i0 = min(n, threadIdx.x * per), i1 = min(n, i0 + per);
-  // Batches of 8 entries: all order / tr_off loads of a batch in flight before any use (the
-  // one-entry-at-a-time walk was a chain of ~20 dependent global loads per thread, 13.7 us at C3).
-  auto batch = [&](int b0, int (&it)[8], int (&nc)[8]) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) it[u] = b0 + u < i1 ? __ldg(order + b0 + u) : -1;
-    int lo[8], hi[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      lo[u] = it[u] >= 0 ? __ldg(tr_off + it[u]) : 0;
-      hi[u] = it[u] >= 0 ? __ldg(tr_off + it[u] + 1) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int P = (hi[u] - lo[u]) * sg;
-      nc[u] = it[u] < 0 ? 0 : (P > cap ? min(kSplitMaxChunks, (P + cap - 1) / cap) : 1);
-    }
+  auto nchunks = [&](int it) {
+    const int P = (__ldg(tr_off + it + 1) - __ldg(tr_off + it)) * sg;
+    return P > cap ? min(kSplitMaxChunks, (P + cap - 1) / cap) : 1;
   };
   int v[3] = {0, 0, 0};  // entries, split items, partial slots
-  for (int b0 = i0; b0 < i1; b0 += 8) {
-    int it[8], nc[8];
-    batch(b0, it, nc);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      v[0] += nc[u];
-      if (nc[u] > 1) {
-        v[1] += 1;
-        v[2] += nc[u];
-      }
+  for (int i = i0; i < i1; ++i) {
+    const int nc = nchunks(__ldg(order + i));
+    v[0] += nc;
+    if (nc > 1) {
+      v[1] += 1;
+      v[2] += nc;
     }
   }
   int x[3];
@@ -2000,22 +1983,17 @@ __global__ void __launch_bounds__(1024) dkv_split_kernel(const int32_t* __restri
   }
   __syncthreads();
   int oa = x[0] + wsum[0][warp], ob = x[1] + wsum[1][warp], oc = x[2] + wsum[2][warp];
-  for (int b0 = i0; b0 < i1; b0 += 8) {
-    int itb[8], ncb[8];
-    batch(b0, itb, ncb);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int it = itb[u], nc = ncb[u];
-      if (it < 0) break;
-      for (int q = 0; q < nc; ++q) out[oa + q] = it | (q << kSplitItemBits) | (nc << (kSplitItemBits + 4));
-      oa += nc;
-      if (nc > 1) {
-        SB_DCHECK(oc + nc <= split_slots(grid));
-        slot_base[it] = oc;
-        split_list[ob] = make_int4(it, nc, oc, 0);
-        ++ob;
-        oc += nc;
-      }
+  for (int i = i0; i < i1; ++i) {
+    const int it = __ldg(order + i);
+    const int nc = nchunks(it);
+    for (int q = 0; q < nc; ++q) out[oa + q] = it | (q << kSplitItemBits) | (nc << (kSplitItemBits + 4));
+    oa += nc;
+    if (nc > 1) {
+      SB_DCHECK(oc + nc <= split_slots(grid));
+      slot_base[it] = oc;
+      split_list[ob] = make_int4(it, nc, oc, 0);
+      ++ob;
+      oc += nc;
     }
   }
   if (threadIdx.x == 1023) {
