@@ -304,22 +304,11 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(
 // the sorted output are bit-identical to row_sorted_mass_kernel, without its ~30 CTA-wide
 // barriers per row (bitonic network in registers: shuffles for strides < 32, register pairs
 // above; the compare-exchange keeps the block kernel's predicate, NaNs included).
+// One row's softmax masses sorted descending, E values per lane (rows of n <= 32 * E). The sum
+// over e adds exact zeros for slots past the row, so z, the masses and the sorted output are
+// bit-identical for any E that covers the row.
 template <int E>
-__global__ void __launch_bounds__(256) row_sorted_mass_warp_kernel(const float* __restrict__ scores,
-                                                                   const int32_t* __restrict__ blk_off,
-                                                                   const int64_t* __restrict__ tri_off, int nseq,
-                                                                   int nb_total, float* __restrict__ sorted) {
-  pdl_wait();  // see launch() (common.cuh)
-  pdl_trigger();
-  const int gi = blockIdx.x * 8 + (threadIdx.x >> 5), h = blockIdx.y, lane = threadIdx.x & 31;
-  if (gi >= nb_total) return;
-  const int64_t tri = tri_off[nseq];
-  const int s = seq_of_block(blk_off, nseq, gi);
-  const int i = gi - blk_off[s];
-  const int n = i + 1;
-  if (n > 32 * E) return;  // the block kernel's rows
-  const size_t off = static_cast<size_t>(h) * tri + tri_off[s] + static_cast<int64_t>(i) * (i + 1) / 2;
-  const float* row = scores + off;
+__device__ __forceinline__ void sorted_mass_row(const float* __restrict__ row, int n, int lane, float* __restrict__ dst) {
   float v[E];
   float mx = -INFINITY;
 #pragma unroll
@@ -375,10 +364,40 @@ __global__ void __launch_bounds__(256) row_sorted_mass_warp_kernel(const float* 
       }
     }
   }
-  float* dst = sorted + off;
+  
 #pragma unroll
   for (int e = 0; e < E; ++e)
     if (e * 32 + lane < n) dst[e * 32 + lane] = v[e];
+}
+
+template <int E>
+__global__ void __launch_bounds__(256) row_sorted_mass_warp_kernel(const float* __restrict__ scores,
+                                                                   const int32_t* __restrict__ blk_off,
+                                                                   const int64_t* __restrict__ tri_off, int nseq,
+                                                                   int nb_total, float* __restrict__ sorted) {
+  pdl_wait();  // see launch() (common.cuh)
+  pdl_trigger();
+  const int gi = blockIdx.x * 8 + (threadIdx.x >> 5), h = blockIdx.y, lane = threadIdx.x & 31;
+  if (gi >= nb_total) return;
+  const int64_t tri = tri_off[nseq];
+  const int s = seq_of_block(blk_off, nseq, gi);
+  const int i = gi - blk_off[s];
+  const int n = i + 1;
+  if (n > 32 * E) return;  // the block kernel's rows
+  const size_t off = static_cast<size_t>(h) * tri + tri_off[s] + static_cast<int64_t>(i) * (i + 1) / 2;
+  const float* row = scores + off;
+  float* dst = sorted + off;
+  // The smallest bitonic width that covers this row (C3: most rows are far shorter than the
+  // longest, whose width E the host picked).
+  if (E >= 8 && n > 128) {
+    sorted_mass_row<E>(row, n, lane, dst);
+  } else if (E >= 4 && n > 64) {
+    sorted_mass_row<(E < 4 ? E : 4)>(row, n, lane, dst);
+  } else if (E >= 2 && n > 32) {
+    sorted_mass_row<(E < 2 ? E : 2)>(row, n, lane, dst);
+  } else {
+    sorted_mass_row<1>(row, n, lane, dst);
+  }
 }
 
 __global__ void row_sorted_mass_kernel(const float* __restrict__ scores, const int32_t* __restrict__ blk_off,
