@@ -474,14 +474,14 @@ __global__ void profile_partial_kernel(const float* __restrict__ sorted, const i
   const int64_t tri = tri_off[nseq];
   double acc = 0.0;
   const float* base = sorted + static_cast<size_t>(h) * tri + tri_off[s];
-  // Same summation order (i ascending); 8 loads in flight per step instead of one per add.
+  // Same summation order (i ascending); 16 loads in flight per step instead of one per add.
   int i = r;
-  for (; i + 8 <= nb; i += 8) {
-    float v[8];
+  for (; i + 16 <= nb; i += 16) {
+    float v[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(base + static_cast<int64_t>(i + u) * (i + u + 1) / 2 + r);
+    for (int u = 0; u < 16; ++u) v[u] = __ldg(base + static_cast<int64_t>(i + u) * (i + u + 1) / 2 + r);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, static_cast<double>(v[u]));
+    for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, static_cast<double>(v[u]));
   }
   for (; i < nb; ++i) acc = __dadd_rn(acc, static_cast<double>(base[static_cast<int64_t>(i) * (i + 1) / 2 + r]));
   partial[(static_cast<size_t>(h) * nseq + s) * nb_max + r] = acc;

@@ -4,7 +4,7 @@ OUT=gpurun_out/${OUT:-ab_mass}; mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q -k "coverage or profile or dst or closed or driver" > $OUT/pytest.log 2>&1; echo "pytest rc $?"; tail -n 2 $OUT/pytest.log
 for lib in default $1; do
   if [ $lib = default ]; then unset SB_LIB_PATH; else export SB_LIB_PATH=alt_lib/$lib.so; fi
-  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:row_sorted_mass -c 6 --csv python bench.py --profile-only 2>/dev/null | grep gpu__time | awk -F'","' '{print $NF}' | tr -d '"' | tr '\n' ' ' | sed "s/^/$lib sorted_mass ns: /"; echo
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"row_sorted_mass|profile_partial" -c 6 --csv python bench.py --profile-only 2>/dev/null | grep gpu__time | awk -F'","' '{print $NF}' | tr -d '"' | tr '\n' ' ' | sed "s/^/$lib sorted_mass ns: /"; echo
 done
 for r in 1 2; do for lib in default $1; do
   if [ $lib = default ]; then unset SB_LIB_PATH; else export SB_LIB_PATH=alt_lib/$lib.so; fi
