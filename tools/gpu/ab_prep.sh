@@ -1,6 +1,7 @@
 #!/bin/bash
-# bwd_prep A/B under ncu (serialized per-kernel durations; PDL makes profiler-event kernel times
-# include the wait on the predecessor).
-for lib in pdl1 prepA prepB; do
-  SB_LIB_PATH=alt_lib/$lib.so timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:"bwd_prep" -c 6 --csv python tools/time_kernels.py 2>/dev/null | grep bwd_prep | grep gpu__time | awk -F'","' '{print $NF}' | tr -d '"' | tr '\n' ' ' | sed "s/^/$lib /"; echo
+# prep launch-shape A/B: bwd_prep kernel time (ncu, C3 profile-only, 4 launches) per library.
+for lib in default "$@"; do
+  if [ $lib = default ]; then unset SB_LIB_PATH; else export SB_LIB_PATH=alt_lib/$lib.so; fi
+  timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:bwd_prep -c 4 --csv python bench.py --profile-only 2>/dev/null | grep "gpu__time" | awk -F'","' '{print $NF}' | tr -d '"' | tr '\n' ' ' | sed "s/^/$lib prep ns: /"; echo
 done
+unset SB_LIB_PATH
