@@ -2037,7 +2037,19 @@ __global__ void __launch_bounds__(256) dkv_records_kernel(const int32_t* __restr
 // granules (256 / (D / 4) key rows) of one part of one split item, grid-strided. All of a
 // granule's nc (<= 15) partial loads are issued before the adds.
 template <int D, int B>
-__global__ void __launch_bounds__(256) dkv_split_reduce_kernel(const int4* __restrict__ split_list,
+// Split reduce launch shape (ncu, C3 profile-only launches): all chunk loads in flight at 78
+// registers, 8 CTAs per SM grid, 27-28 us; 4-chunk batches at 32 registers (8 CTAs of 256 per
+// SM), 16 CTAs per SM grid, 16-19 us.
+#ifndef SB_REDUCE_BATCHED
+#define SB_REDUCE_BATCHED 1
+#endif
+#ifndef SB_REDUCE_MINB
+#define SB_REDUCE_MINB 8
+#endif
+#ifndef SB_REDUCE_GRID
+#define SB_REDUCE_GRID 16
+#endif
+__global__ void __launch_bounds__(256, SB_REDUCE_MINB) dkv_split_reduce_kernel(const int4* __restrict__ split_list,
                                                                const int32_t* __restrict__ counts,
                                                                const float* __restrict__ partials,
                                                                const int32_t* __restrict__ cu,
@@ -2063,6 +2075,25 @@ __global__ void __launch_bounds__(256) dkv_split_reduce_kernel(const int4* __res
     const int nkv = min(B, cu[s + 1] - kv0);
     if (row >= nkv) continue;
     const float4* p = reinterpret_cast<const float4*>(partials) + (static_cast<size_t>(slot0) * 2 + part) * kG + gidx;
+#if SB_REDUCE_BATCHED
+    // Chunks in batches of 4 loads, summed in chunk order from chunk 0's value (bit-identical).
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q0 = 0; q0 < nc; q0 += 4) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + u < nc) v[u] = __ldg(p + static_cast<size_t>(q0 + u) * 2 * kG);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (q0 + u >= nc) break;
+        if (q0 + u == 0) {
+          a = v[u];
+        } else {
+          a.x += v[u].x, a.y += v[u].y, a.z += v[u].z, a.w += v[u].w;
+        }
+      }
+    }
+#else
     float4 v[kSplitMaxChunks];
 #pragma unroll
     for (int q = 0; q < kSplitMaxChunks; ++q)
@@ -2071,6 +2102,7 @@ __global__ void __launch_bounds__(256) dkv_split_reduce_kernel(const int4* __res
 #pragma unroll
     for (int q = 1; q < kSplitMaxChunks; ++q)
       if (q < nc) a.x += v[q].x, a.y += v[q].y, a.z += v[q].z, a.w += v[q].w;
+#endif
     const float mul = part ? scale : 1.0f;
     uint2 o;
     o.x = pack_bf16x2(a.x * mul, a.y * mul);
@@ -2275,7 +2307,7 @@ void launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const u
                                                                    scale_log2, dk, dv, recs_split, split_counts,
                                                                    slot_base, partials, g_trace_bwd);
     launched("sb_sparse_attn_bwd/dkv");
-    launch(dkv_split_reduce_kernel<D, B>, 8 * sms, 256, 0, st, split_list, split_counts, partials, cu, blk_off, nseq,
+    launch(dkv_split_reduce_kernel<D, B>, SB_REDUCE_GRID * sms, 256, 0, st, split_list, split_counts, partials, cu, blk_off, nseq,
                                                             nb_total, hkv, scale, dk, dv);
     launched("sb_sparse_attn_bwd/split_reduce");
   }
